@@ -1,0 +1,134 @@
+/*
+ * mertens_sm100.h — C ABI of the B200 (sm_100a) exact-Mertens engine.
+ *
+ * Drop-in boundary for the reference package `mertens` (pkg/src/mertens).
+ * Plain pointers and sizes only; all buffers are HOST memory owned by the
+ * caller (the library owns device memory for the duration of one call and
+ * retains no pointer across calls).  Calls are synchronous; ctypes releases
+ * the GIL around them.  Return codes map onto the reference exceptions
+ * (errors.py:4-50) in the Python shim paper_1108_0135_b200/_lib.py.
+ *
+ * Two layers, mirroring the reference:
+ *   1. Backend-protocol ops — exactly the functions the engine calls through
+ *      `_kernels.get_backend(name)` (_kernels/__init__.py:15-33), with the
+ *      same argument meaning; used for per-kernel parity tests.
+ *   2. The job-level production entry mt_run(): one call per
+ *      mertens_exact / mertens_exact_multi (engine.py:405-446), covering the
+ *      whole sieve -> update -> resolve pipeline on the GPU.
+ */
+#ifndef MERTENS_SM100_H
+#define MERTENS_SM100_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MT_ABI_VERSION 1
+
+/* return codes */
+#define MT_OK 0
+#define MT_ERR_RESOURCE 1 /* -> ResourceLimitError  (errors.py:8)  */
+#define MT_ERR_CONTRACT 2 /* -> ContractViolationError (errors.py:16) */
+#define MT_ERR_CUDA 3     /* -> RuntimeError (device / driver failure) */
+#define MT_ERR_VALUE 4    /* -> ValueError   */
+#define MT_ERR_OVERFLOW 5 /* -> OverflowError (_native.pyx:308-309) */
+
+/* last error message of the calling thread ("" if none) */
+const char* mt_last_error(void);
+int mt_abi_version(void);
+/* number of visible CUDA devices (0 when no GPU / no driver) */
+int mt_device_count(void);
+/* select the device for subsequent calls of this thread */
+int mt_set_device(int device);
+
+/* ---- 1. backend-protocol ops (host buffers) -------------------------------- */
+
+/* replaces _native.pyx:127-160 sieve_logprime(y1, y2, primes, logs, wheel):
+ * mu over [y1, y2], y1 >= 2.  Uses primes[i] with primes[i]^2 <= y2, logs[i]
+ * added for p >= 11, 0x80 for p^2 | y, p >= 5, on top of wheel[13860]. */
+int mt_sieve_logprime(uint64_t y1, uint64_t y2, const uint64_t* primes, const uint8_t* logs,
+                      uint64_t nprimes, const uint8_t* wheel, int8_t* mu_out);
+
+/* replaces _native.pyx:113-124 logprime_states(...): raw 8-bit states */
+int mt_logprime_states(uint64_t y1, uint64_t y2, const uint64_t* primes, const uint8_t* logs,
+                       uint64_t nprimes, const uint8_t* wheel, uint8_t* states_out);
+
+/* replaces _native.pyx:163-206 sieve_naive(y1, y2, primes): mu over [y1, y2]
+ * (y1 >= 1, y2 < 2^63).  Same mu; computed by the GPU log-prime sieve. */
+int mt_sieve_naive(uint64_t y1, uint64_t y2, const uint64_t* primes, uint64_t nprimes,
+                   int8_t* mu_out);
+
+/* replaces _native.pyx:227-310 apply_block(acc, v, lo, xcut, mcut, dnext, ynext,
+ * y1, y2, mprefix, divtable): folds one block's M values (mprefix[i] = M(y1+i))
+ * into every element; acc/dnext/ynext updated in place; signed-128 partial sums
+ * with the |acc| <= 2^62 guard (MT_ERR_OVERFLOW).  The divisor table argument
+ * of the reference is not needed (exact fp64-reciprocal division on device). */
+int mt_apply_block(uint64_t K, int64_t* acc, const uint64_t* v, const uint64_t* lo,
+                   const uint64_t* xcut, const uint64_t* mcut, uint64_t* dnext, uint64_t* ynext,
+                   uint64_t y1, uint64_t y2, const int64_t* mprefix, uint64_t* counted_out,
+                   uint64_t* dense_out);
+
+/* replaces _native.pyx:313-334 finalize_recursion(tails, D) */
+int mt_finalize(uint64_t K, const int64_t* tails, const uint64_t* D, int64_t* final_out);
+
+/* replaces _native.pyx:32-68 build_divisor_arrays(cap): arrays of cap+1 */
+int mt_build_divisor_arrays(uint64_t cap, uint64_t* magic, uint8_t* shift, uint8_t* scheme);
+
+/* M(y) for y in [y1, y2] (y1 >= 1): GPU sieve + scan from 1.  Backs the
+ * direct path (engine.py:449-458) and the naive oracle (engine.py:553-603). */
+int mt_mertens_range(uint64_t y1, uint64_t y2, int64_t* m_out);
+
+/* M(y) at sorted points pts[0..npts) (each >= 1): one GPU sieve pass over
+ * [1, max pts].  Backs mertens_naive(n, checkpoints) (engine.py:553-603). */
+int mt_mertens_at(const uint64_t* pts, uint64_t npts, int64_t* m_out);
+
+/* ---- 2. job-level production entry ----------------------------------------- */
+
+typedef struct {
+  uint32_t n_targets;      /* N >= 1 (mertens_exact: 1; mertens_exact_multi: N) */
+  const uint64_t* n_lo;    /* n_i mod 2^64, n_i >= 4 (any order, distinct)       */
+  const uint64_t* n_hi;    /* n_i >> 64 (n_i < 2^75)                              */
+  uint64_t u;              /* sieve bound, from choose_u (engine.py:116-131)     */
+  /* quotient capture for target 0 (engine.py:242-252): M(floor(n0/c)) for
+   * c in [cap_c_lo, cap_c_hi] (floor(n0/c) <= u) into cap_m_out, and M(y) for
+   * y in [0, cap_small] into small_m_out.  Zero-length ranges disable. */
+  uint64_t cap_c_lo, cap_c_hi;
+  uint64_t cap_small;
+  /* tuning (0 = default) */
+  uint64_t q_budget_bytes; /* device bytes for the Q tables (default 48 GiB)       */
+  uint32_t seg_log2_head;  /* head segment length 2^x (default 25)                 */
+  uint32_t seg_log2_tail;  /* tail segment length 2^x (default 27)                 */
+  int32_t device;          /* CUDA device ordinal (-1: current)                    */
+  /* y-range sharding for multi-GPU (rank r of w owns tail y-blocks); w<=1: all */
+  uint32_t shard_rank, shard_world;
+} mt_job;
+
+typedef struct {
+  /* reference RunStats fields (engine.py:188-197), counters in closed form */
+  uint64_t blocks, counted_items, dense_items;
+  uint64_t divtable_cap, divtable_released_at, r4_block_len;
+  /* engine-specific */
+  uint64_t head_end, n_head_segments, n_tail_segments, kernel_launches;
+  uint64_t max_mcut;
+  uint64_t windowed_items, qgather_items, q_entries;
+  double ms_total, ms_sieve_head, ms_update_head, ms_sieve_tail, ms_qgather, ms_finalize;
+  double ms_counted_kernel, ms_dense_kernel;  /* event-timed (when enabled) */
+} mt_stats;
+
+typedef struct {
+  int64_t* finals;         /* concatenated: target i's M(floor(n_i/k)), k=1..K_i, K_i = n_i//u,
+                              in the order of mt_job.n_lo                         */
+  int64_t* cap_m_out;      /* cap_c_hi - cap_c_lo + 1 entries (or null)         */
+  int64_t* small_m_out;    /* cap_small + 1 entries (or null)                   */
+  uint64_t* acc_out;       /* optional: raw accumulators (ΣK_i) before resolve   */
+  mt_stats stats;
+} mt_result;
+
+/* one exact job: sieve 1..u, update every element, resolve */
+int mt_run(const mt_job* job, mt_result* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,133 @@
+"""ctypes binding of the C ABI in include/mertens_sm100.h.
+
+The shared library ``libmertens_sm100.so`` (built in-tree by
+``paper_1108_0135_b200.build.build()``) is the only compute path: there is no
+CPU fallback.  A missing library raises ImportError; a missing GPU raises
+DeviceError at the first compute call.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import ContractViolationError, DeviceError, ResourceLimitError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmertens_sm100.so")
+
+MT_OK, MT_ERR_RESOURCE, MT_ERR_CONTRACT, MT_ERR_CUDA, MT_ERR_VALUE, MT_ERR_OVERFLOW = range(6)
+
+_u64 = ctypes.c_uint64
+_pu64 = ctypes.POINTER(ctypes.c_uint64)
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+
+
+class MtJob(ctypes.Structure):
+    _fields_ = [
+        ("n_targets", ctypes.c_uint32),
+        ("n_lo", _pu64),
+        ("n_hi", _pu64),
+        ("u", _u64),
+        ("cap_c_lo", _u64),
+        ("cap_c_hi", _u64),
+        ("cap_small", _u64),
+        ("q_budget_bytes", _u64),
+        ("seg_log2_head", ctypes.c_uint32),
+        ("seg_log2_tail", ctypes.c_uint32),
+        ("device", ctypes.c_int32),
+        ("shard_rank", ctypes.c_uint32),
+        ("shard_world", ctypes.c_uint32),
+    ]
+
+
+class MtStats(ctypes.Structure):
+    _fields_ = [(f, _u64) for f in (
+        "blocks", "counted_items", "dense_items", "divtable_cap", "divtable_released_at",
+        "r4_block_len", "head_end", "n_head_segments", "n_tail_segments", "kernel_launches",
+        "max_mcut", "windowed_items", "qgather_items", "q_entries")] + [
+        (f, ctypes.c_double) for f in (
+            "ms_total", "ms_sieve_head", "ms_update_head", "ms_sieve_tail", "ms_qgather",
+            "ms_finalize", "ms_counted_kernel", "ms_dense_kernel")]
+
+
+class MtResult(ctypes.Structure):
+    _fields_ = [
+        ("finals", _pi64),
+        ("cap_m_out", _pi64),
+        ("small_m_out", _pi64),
+        ("acc_out", _pu64),
+        ("stats", MtStats),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load (once) and return the engine library; raise if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    L.mt_last_error.restype = ctypes.c_char_p
+    L.mt_abi_version.restype = ctypes.c_int
+    L.mt_device_count.restype = ctypes.c_int
+    vp = ctypes.c_void_p
+    sigs = {
+        "mt_set_device": [ctypes.c_int],
+        "mt_sieve_logprime": [_u64, _u64, vp, vp, _u64, vp, vp],
+        "mt_logprime_states": [_u64, _u64, vp, vp, _u64, vp, vp],
+        "mt_sieve_naive": [_u64, _u64, vp, _u64, vp],
+        "mt_apply_block": [_u64, vp, vp, vp, vp, vp, vp, vp, _u64, _u64, vp, _pu64, _pu64],
+        "mt_finalize": [_u64, vp, vp, vp],
+        "mt_build_divisor_arrays": [_u64, vp, vp, vp],
+        "mt_mertens_range": [_u64, _u64, vp],
+        "mt_mertens_at": [vp, _u64, vp],
+        "mt_run": [ctypes.POINTER(MtJob), ctypes.POINTER(MtResult)],
+    }
+    for name, args in sigs.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def require_device():
+    L = lib()
+    if L.mt_device_count() < 1:
+        raise DeviceError("no CUDA device visible: the sm_100a engine has no CPU fallback")
+    return L
+
+
+def check(rc: int):
+    """Map an ABI return code onto the reference's exception classes."""
+    if rc == MT_OK:
+        return
+    msg = lib().mt_last_error().decode(errors="replace")
+    if rc == MT_ERR_RESOURCE:
+        raise ResourceLimitError(msg)
+    if rc == MT_ERR_CONTRACT:
+        raise ContractViolationError(msg)
+    if rc == MT_ERR_VALUE:
+        raise ValueError(msg)
+    if rc == MT_ERR_OVERFLOW:
+        raise OverflowError(msg)
+    raise DeviceError(msg or f"engine error {rc}")
+
+
+def ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+EXPORTED_SYMBOLS = (
+    "mt_last_error", "mt_abi_version", "mt_device_count", "mt_set_device",
+    "mt_sieve_logprime", "mt_logprime_states", "mt_sieve_naive", "mt_apply_block",
+    "mt_finalize", "mt_build_divisor_arrays", "mt_mertens_range", "mt_mertens_at", "mt_run",
+)

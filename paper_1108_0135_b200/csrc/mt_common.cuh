@@ -1,0 +1,78 @@
+// Shared device helpers for the B200 exact-Mertens engine.
+//
+// Division strategy (replaces the reference's Granlund-Montgomery table,
+// _native.pyx:32-68,209-224, and its hardware-divide fallback):
+//   floor(v/m) = est + corr, est = round(double(v) * rcp(m)) read straight out
+//   of the mantissa of fma(vd, r, 2^52) (FP64 pipe, full rate on B200), and
+//   corr in {0,-1} from the sign of the remainder v - est*m computed on the low
+//   32 (or 64) bits with one IMAD.  Exact whenever m >= 2^(bitlen(v)-50),
+//   i.e. v/m < 2^50 (|est - v/m| <= 0.375).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+typedef uint64_t u64;
+typedef int64_t i64;
+typedef uint32_t u32;
+typedef unsigned __int128 u128;
+typedef __int128 i128;
+
+#define MT_TWO52 4503599627370496.0
+#define MT_EXP52 0x4330000000000000ull
+
+// est in {f, f+1} -> f, using a 32-bit remainder (needs m < 2^31)
+__device__ __forceinline__ u64 qdiv32(double vd, double r, u32 vlo, u32 m) {
+  u64 b = (u64)__double_as_longlong(fma(vd, r, MT_TWO52)) - MT_EXP52;
+  int t = (int)(vlo - (u32)b * m);
+  return b + (u64)(i64)(t >> 31);
+}
+
+// same with a 64-bit remainder (any m < 2^63)
+__device__ __forceinline__ u64 qdiv64(double vd, double r, u64 vlo, u64 m) {
+  u64 b = (u64)__double_as_longlong(fma(vd, r, MT_TWO52)) - MT_EXP52;
+  i64 t = (i64)(vlo - b * m);
+  return b + (u64)(t >> 63);
+}
+
+__device__ __forceinline__ int bitlen128(u64 lo, u64 hi) {
+  return hi ? 128 - __clzll((long long)hi) : (lo ? 64 - __clzll((long long)lo) : 0);
+}
+
+// true when qdiv64 is exact for this (v, m) pair
+__device__ __forceinline__ bool qdiv_ok(int vbits, u64 m) {
+  int need = vbits - 50;
+  return m >= 1 && (need <= 0 || m >= (1ull << need));
+}
+
+__device__ __forceinline__ double u128_to_double(u64 lo, u64 hi) {
+  // correctly rounded for hi < 2^53 is not required: only used as an estimate
+  // whose error is covered by qdiv_ok (relative error < 2^-52).
+  return hi ? fma((double)hi, 18446744073709551616.0, (double)lo) : __ull2double_rn(lo);
+}
+
+// exact floor((hi:lo)/m) for any m >= 1 (slow path)
+__device__ __forceinline__ u128 udiv128(u64 lo, u64 hi, u64 m) {
+  u128 v = ((u128)hi << 64) | lo;
+  return v / m;
+}
+
+// exact floor(v/m) choosing the fast path when it is provably exact
+__device__ __forceinline__ u64 udiv_any(u64 vlo, u64 vhi, double vd, int vbits, u64 m) {
+  if (qdiv_ok(vbits, m)) {
+    double r = __drcp_rn((double)m);
+    return qdiv64(vd, r, vlo, m);
+  }
+  return (u64)udiv128(vlo, vhi, m);
+}
+
+#define MT_CUDA_CHECK(x)                                                   \
+  do {                                                                     \
+    cudaError_t _e = (x);                                                  \
+    if (_e != cudaSuccess) {                                               \
+      mt_set_error("CUDA error %s at %s:%d", cudaGetErrorString(_e),       \
+                   __FILE__, __LINE__);                                    \
+      return MT_ERR_CUDA;                                                  \
+    }                                                                      \
+  } while (0)
+
+void mt_set_error(const char* fmt, ...);

@@ -1,0 +1,90 @@
+// Internal (non-ABI) declarations shared by the engine's translation units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/mertens_sm100.h"
+
+#define MT_TILE 65536u          // sieve tile: cells (bytes) held in shared memory
+#define MT_SIEVE_THREADS 512    // threads per sieve tile (128 cells each)
+#define MT_WHEEL 13860u
+#define MT_WHEEL_WORDS (MT_WHEEL / 4)
+#define MT_CT 256               // elements per counted-walk tile (threads per CTA)
+#define MT_CM 2048              // m values per counted-walk work unit
+
+struct SieveTileArgs {
+  uint64_t Y0;                   // segment start (multiple of MT_TILE)
+  uint64_t y2;                   // prime bound rule: primes with p*p <= y2
+  const uint32_t* wheel32x;      // 13860-periodic wheel as words, extended by MT_TILE/4 words
+  const uint32_t* big;           // per-segment large-prime marks (or null)
+  const uint32_t* primes;
+  const double* rprimes;         // __drcp_rn(p)
+  const uint8_t* logs;
+  uint32_t p_first;              // first prime index sieved in-tile (prime 5)
+  uint32_t p_warp_end;           // [p_first, p_warp_end): warp-per-prime
+  uint32_t p_small_end;          // [p_warp_end, p_small_end): thread-per-prime
+  uint32_t log_min;              // logs added for p >= log_min (11: reference wheel)
+  int do_logs;
+  int* tile_sum;                 // [ntiles]
+  int8_t* mu_out;                // segment mu (or null)
+  int* m_out;                    // segment partial/absolute M (or null)
+  uint8_t* states_out;           // raw states (instrumented) or null
+  const void* caps;              // CaptureTarget[n_cap] (device)
+  int n_cap;
+};
+
+struct SieveSegment {
+  uint64_t Y0, R, y2;
+  uint32_t* big;                 // R bytes
+  const uint32_t* primes;
+  const double* rprimes;
+  const uint8_t* logs;
+  uint32_t p_large_begin, p_large_end;
+  int do_logs_large;
+  int64_t* running;              // device scalar M(Y0-1) (null: no scan)
+  int64_t* tile_base;            // [ntiles]
+  SieveTileArgs tile;
+};
+
+int mt_launch_sieve_segment(const SieveSegment& s, cudaStream_t st);
+
+// element arrays (device, SoA), one entry per harmonic-array element of every target
+struct ElemDev {
+  const double* vd;      // double(v)
+  const uint64_t* vlo;   // v mod 2^64
+  const uint64_t* vhi;   // v >> 64
+  const uint8_t* vbits;  // bit length of v
+  const uint64_t* k;     // array index k (1-based, within its target)
+  const uint32_t* tgt;   // target id
+  const uint64_t* mcut;
+  const uint64_t* xcut;
+  const uint64_t* lo;    // max(2, D+1)
+  const uint64_t* lo_w;  // first d of the windowed dense walk: max(lo, J/k + 1)
+  const uint64_t* dq_hi; // last d of the Q-gather walk: min(xcut, J/k)
+  uint64_t n;            // total elements
+};
+
+struct TargetDev {       // per-target constants for Q lookups
+  int* Q;                // Q[j - jq0]
+  uint64_t jq0;
+};
+
+// update-side launchers (mt_update.cu)
+struct UpdateCtx;
+int mt_update_create(UpdateCtx** ctx, const ElemDev& E, uint64_t* acc, int32_t* Mmc,
+                     const uint64_t* tile_mcut_max, const uint8_t* tile_vbits_max,
+                     uint64_t ntiles, const TargetDev* tgts, int ntgt, cudaStream_t st);
+void mt_update_destroy(UpdateCtx* ctx);
+int mt_update_head_segment(UpdateCtx* ctx, uint64_t Y0, uint64_t R, const int8_t* mu,
+                           const int* M, cudaStream_t st);
+int mt_update_qgather(UpdateCtx* ctx, cudaStream_t st);
+int mt_update_finish(UpdateCtx* ctx, cudaStream_t st);  // acc -= M(mcut)*xcut
+int mt_finalize_dev(const uint64_t* acc, const uint64_t* D, uint64_t K, int64_t* final_out,
+                    cudaStream_t st);
+int mt_apply_block_dev(uint64_t K, int64_t* acc, const uint64_t* v, const uint64_t* lo,
+                       const uint64_t* xcut, const uint64_t* mcut, uint64_t* dnext,
+                       uint64_t* ynext, uint64_t y1, uint64_t y2, const int64_t* mp,
+                       uint64_t* counters /*[3]: counted, dense, overflow*/, cudaStream_t st);
+int mt_divisor_arrays_dev(uint64_t cap, uint64_t* magic, uint8_t* shift, uint8_t* scheme,
+                          cudaStream_t st);
+uint64_t mt_update_launches(UpdateCtx* ctx);

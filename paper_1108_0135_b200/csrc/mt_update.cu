@@ -1,0 +1,552 @@
+// Harmonic-array update on sm_100a — the paper's accelerator contribution
+// and the reference's hot loop apply_block
+// (_native.pyx:227-310, pure.py:110-148), restructured for the GPU.
+//
+// For element k (v = floor(n/k)) the reference accumulates, over all y-blocks,
+//   acc_k = sum_{m=1}^{mcut} M(m) (q_m - q'_{m+1})     counted walk (:263-284)
+//         + sum_{d=lo}^{xcut} M(floor(v/d))            dense walk   (:285-307)
+// with q_m = floor(v/m) and the top term clipped at xcut.  By summation by
+// parts the counted walk equals
+//   sum_{m=1}^{mcut} mu(m) floor(v/m)  -  M(mcut) * xcut
+// (floor(v/(mcut+1)) <= xcut always), so it needs only mu(m) != 0 (61% of m),
+// one exact division per item and no prefix values.  acc_k is therefore
+// computed as (all mod 2^64):
+//   counted  : tiles of (256 elements x 2048 m) per head segment; the tile's
+//              squarefree m are staged in shared memory as (1/m, m) and every
+//              thread walks them with the fp64-reciprocal exact division.
+//   windowed : dense items whose quotient y = v/d lies in the head, gathered
+//              from the segment's M array (load-balanced item ranges).
+//   Q-gather : dense items with k*d <= J read M(floor(n/(kd))) straight from
+//              the captured quotient table Q[j] (no division at all).
+// The split (xcut, mcut) is the reference's own, so RunStats counters match.
+#include <cub/cub.cuh>
+
+#include "mt_common.cuh"
+#include "mt_internal.h"
+
+#define IPT 32  // items per lane per work chunk
+
+struct UpdateCtx {
+  ElemDev E;
+  uint64_t* acc;
+  int32_t* Mmc;
+  const uint64_t* tile_mcut_max;
+  const uint8_t* tile_vbits_max;
+  uint64_t ntiles;
+  TargetDev* tgts;  // device
+  int ntgt;
+  // scratch
+  uint64_t* units;   // [ntiles+1]
+  uint64_t* cnt;     // [n+1]
+  uint64_t* dtop;    // [n]
+  uint64_t* off;     // [n+1]
+  uint64_t* qcnt;    // [n+1]
+  uint64_t* qoff;    // [n+1]
+  uint64_t* counter; // work counters [4]
+  void* cub_tmp;
+  size_t cub_bytes;
+  uint64_t launches;
+  int nsm;
+};
+
+// ---------------------------------------------------------------- counted walk
+__global__ void k_counted_plan(const uint64_t* __restrict__ tile_mcut_max, uint64_t ntiles, u64 Y0,
+                               u64 R, uint64_t* __restrict__ units) {
+  u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > ntiles) return;
+  if (t == ntiles) { units[t] = 0; return; }
+  u64 mx = tile_mcut_max[t];
+  u64 n = 0;
+  if (mx >= Y0 && mx >= 1) {
+    n = (mx - Y0) / MT_CM + 1;
+    u64 cap = R / MT_CM;
+    if (n > cap) n = cap;
+  }
+  units[t] = n;
+}
+
+__device__ __forceinline__ u64 upper_idx(const uint64_t* __restrict__ off, u64 n, u64 x) {
+  // largest i in [0, n) with off[i] <= x   (off non-decreasing, off[0] = 0)
+  u64 lo = 0, hi = n;
+  while (hi - lo > 1) {
+    u64 mid = (lo + hi) >> 1;
+    if (off[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+struct CountedArgs {
+  ElemDev E;
+  uint64_t* acc;
+  const uint64_t* tile_mcut_max;
+  const uint8_t* tile_vbits_max;
+  const uint64_t* off;  // [ntiles+1] exclusive scan of units
+  uint64_t ntiles;
+  const int8_t* mu;     // segment mu
+  u64 Y0;
+  uint64_t* counter;
+};
+
+__global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
+  __shared__ double rmL[MT_CM];
+  __shared__ u32 mL[MT_CM];
+  __shared__ u64 s_unit;
+  __shared__ int wp[MT_CT / 32], wn[MT_CT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u64 total = a.off[a.ntiles];
+  for (;;) {
+    if (tid == 0) s_unit = atomicAdd((unsigned long long*)a.counter, 1ull);
+    __syncthreads();
+    const u64 unit = s_unit;
+    if (unit >= total) break;
+    const u64 tau = upper_idx(a.off, a.ntiles + 1, unit);
+    const u64 c = unit - a.off[tau];
+    const u64 mlo = a.Y0 + c * MT_CM;
+    u64 mhi = mlo + MT_CM;  // exclusive
+    const u64 mx = a.tile_mcut_max[tau];
+    if (mhi > mx + 1) mhi = mx + 1;
+
+    // ---- build the squarefree lists: plus from the front, minus from the back
+    constexpr int PER = MT_CM / MT_CT;  // 8 m per thread
+    const u64 m0 = mlo + (u64)tid * PER;
+    u64 bits = 0;
+    if (m0 < mhi) bits = *(const u64*)(a.mu + (m0 - a.Y0));
+    int np = 0, nn = 0;
+#pragma unroll
+    for (int b = 0; b < PER; b++) {
+      int8_t mu = (int8_t)((bits >> (8 * b)) & 0xff);
+      bool in = m0 + b < mhi;
+      np += (in && mu > 0);
+      nn += (in && mu < 0);
+    }
+    // block exclusive scan of (np, nn)
+    int ip = np, in_ = nn;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int tp = __shfl_up_sync(0xffffffffu, ip, o), tn = __shfl_up_sync(0xffffffffu, in_, o);
+      if (lane >= o) { ip += tp; in_ += tn; }
+    }
+    if (lane == 31) { wp[warp] = ip; wn[warp] = in_; }
+    __syncthreads();
+    int bp = 0, bn = 0, totp = 0, totn = 0;
+#pragma unroll
+    for (int w = 0; w < MT_CT / 32; w++) {
+      if (w < warp) { bp += wp[w]; bn += wn[w]; }
+      totp += wp[w]; totn += wn[w];
+    }
+    int op = bp + ip - np, on = bn + in_ - nn;
+#pragma unroll
+    for (int b = 0; b < PER; b++) {
+      int8_t mu = (int8_t)((bits >> (8 * b)) & 0xff);
+      u64 m = m0 + b;
+      if (m < mhi && mu != 0) {
+        double r = __drcp_rn((double)m);
+        if (mu > 0) { rmL[op] = r; mL[op] = (u32)m; op++; }
+        else { int idx = MT_CM - 1 - on; rmL[idx] = r; mL[idx] = (u32)m; on++; }  // low word; chunks never straddle 2^32
+      }
+    }
+    __syncthreads();
+
+    // ---- per-element walk
+    const u64 e = tau * MT_CT + tid;
+    if (e < a.E.n) {
+      const u64 mc = a.E.mcut[e];
+      if (mc >= mlo) {
+        const u64 mhw = mlo & 0xFFFFFFFF00000000ull;  // high word shared by the chunk
+        int bp_ = totp, bn_ = totn;
+        if (mc + 1 < mhi) {  // partial: count entries with m <= mc (lists ascending in m)
+          int lo = 0, hi = totp;
+          while (lo < hi) { int mid = (lo + hi) >> 1; if ((mhw | mL[mid]) <= mc) lo = mid + 1; else hi = mid; }
+          bp_ = lo;
+          lo = 0; hi = totn;
+          while (lo < hi) { int mid = (lo + hi) >> 1; if ((mhw | mL[MT_CM - 1 - mid]) <= mc) lo = mid + 1; else hi = mid; }
+          bn_ = lo;
+        }
+        const double vd = a.E.vd[e];
+        const u64 vlo = a.E.vlo[e];
+        const int vb = a.tile_vbits_max[tau];
+        const bool ok = (vb <= 50) || (mlo >= (1ull << (vb - 50)));
+        u64 S;
+        if (ok && mhi <= (1ull << 31)) {
+          const u32 v32 = (u32)vlo;
+          u64 ap = 0, an = 0;
+          u32 cp = 0, cn = 0;
+#pragma unroll 8
+          for (int i = 0; i < bp_; i++) {
+            u64 b = (u64)__double_as_longlong(fma(vd, rmL[i], MT_TWO52));
+            int t = (int)(v32 - (u32)b * mL[i]);
+            ap += b; cp += (u32)t >> 31;
+          }
+#pragma unroll 8
+          for (int i = 0; i < bn_; i++) {
+            int idx = MT_CM - 1 - i;
+            u64 b = (u64)__double_as_longlong(fma(vd, rmL[idx], MT_TWO52));
+            int t = (int)(v32 - (u32)b * mL[idx]);
+            an += b; cn += (u32)t >> 31;
+          }
+          S = (ap - (u64)bp_ * MT_EXP52 - cp) - (an - (u64)bn_ * MT_EXP52 - cn);
+        } else if (ok) {
+          u64 ap = 0, an = 0, cp = 0, cn = 0;
+          for (int i = 0; i < bp_; i++) {
+            u64 b = (u64)__double_as_longlong(fma(vd, rmL[i], MT_TWO52));
+            i64 t = (i64)(vlo - b * (mhw | mL[i]));
+            ap += b; cp += (u64)t >> 63;
+          }
+          for (int i = 0; i < bn_; i++) {
+            int idx = MT_CM - 1 - i;
+            u64 b = (u64)__double_as_longlong(fma(vd, rmL[idx], MT_TWO52));
+            i64 t = (i64)(vlo - b * (mhw | mL[idx]));
+            an += b; cn += (u64)t >> 63;
+          }
+          S = (ap - (u64)bp_ * MT_EXP52 - cp) - (an - (u64)bn_ * MT_EXP52 - cn);
+        } else {  // exact slow path (small m with wide v)
+          const u64 vhi = a.E.vhi[e];
+          u64 sp = 0, sn = 0;
+          for (int i = 0; i < bp_; i++) sp += (u64)udiv128(vlo, vhi, mhw | mL[i]);
+          for (int i = 0; i < bn_; i++) sn += (u64)udiv128(vlo, vhi, mhw | mL[MT_CM - 1 - i]);
+          S = sp - sn;
+        }
+        if (bp_ + bn_) atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)S);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------- dense: item machinery
+struct ItemsArgs {
+  ElemDev E;
+  uint64_t* acc;
+  const uint64_t* off;   // [n+1]
+  const uint64_t* dtop;  // [n]
+  uint64_t n;
+  uint64_t* counter;
+  // windowed mode
+  const int* M;
+  u64 Y0;
+  // Q mode
+  const TargetDev* tgts;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_items(ItemsArgs a) {
+  const int lane = threadIdx.x & 31;
+  const u64 total = a.off[a.n];
+  for (;;) {
+    u64 w = 0;
+    if (lane == 0) w = atomicAdd((unsigned long long*)a.counter, 1ull);
+    w = __shfl_sync(0xffffffffu, w, 0);
+    const u64 base = w * (32ull * IPT);
+    if (base >= total) break;
+    u64 i = base + lane;
+    if (i >= total) continue;
+    u64 e = upper_idx(a.off, a.n + 1, i);
+    u64 e_lo = a.off[e], e_hi = a.off[e + 1];
+    u64 top = a.dtop[e];
+    double vd = a.E.vd[e];
+    u64 vlo = a.E.vlo[e], vhi = a.E.vhi[e];
+    int vb = a.E.vbits[e];
+    u64 kk = a.E.k[e];
+    const int* Qt = nullptr;
+    u64 jq0 = 0;
+    if (MODE == 1) { TargetDev t = a.tgts[a.E.tgt[e]]; Qt = t.Q; jq0 = t.jq0; }
+    i64 sum = 0;
+    for (int s = 0; s < IPT; s++, i += 32) {
+      if (i >= total) break;
+      if (i >= e_hi) {
+        if (sum) atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)sum);
+        sum = 0;
+        e = upper_idx(a.off, a.n + 1, i);
+        e_lo = a.off[e]; e_hi = a.off[e + 1];
+        top = a.dtop[e];
+        vd = a.E.vd[e]; vlo = a.E.vlo[e]; vhi = a.E.vhi[e]; vb = a.E.vbits[e];
+        kk = a.E.k[e];
+        if (MODE == 1) { TargetDev t = a.tgts[a.E.tgt[e]]; Qt = t.Q; jq0 = t.jq0; }
+      }
+      const u64 d = top - (i - e_lo);
+      if (MODE == 0) {
+        u64 y;
+        const bool ok = (vb <= 50) || (d >= (1ull << (vb - 50)));
+        if (ok && d < (1ull << 31)) y = qdiv32(vd, __drcp_rn((double)d), (u32)vlo, (u32)d);
+        else if (ok) y = qdiv64(vd, __drcp_rn((double)d), vlo, d);
+        else y = (u64)udiv128(vlo, vhi, d);
+        sum += a.M[y - a.Y0];
+      } else {
+        sum += Qt[kk * d - jq0];
+      }
+    }
+    if (sum) atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)sum);
+  }
+}
+
+// floor(v/m) clamped to `clamp` (v may exceed 2^64)
+__device__ __forceinline__ u64 div_clamp(u64 vlo, u64 vhi, double vd, int vb, u64 m, u64 clamp) {
+  if (vhi) {
+    u128 q = udiv128(vlo, vhi, m);
+    return q > (u128)clamp ? clamp : (u64)q;
+  }
+  u64 q = udiv_any(vlo, 0, vd, vb, m);
+  return q > clamp ? clamp : q;
+}
+
+// windowed dense plan for one head segment: items d in [max(lo_w, v/(Y0+R)+1), min(xcut, v/Y0)]
+__global__ void k_dense_plan(ElemDev E, u64 Y0, u64 R, uint64_t* __restrict__ cnt,
+                             uint64_t* __restrict__ dtop) {
+  u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e > E.n) return;
+  if (e == E.n) { cnt[e] = 0; return; }
+  const u64 xc = E.xcut[e], lw = E.lo_w[e];
+  u64 c = 0, top = 0;
+  if (lw <= xc) {
+    const u64 vlo = E.vlo[e], vhi = E.vhi[e];
+    const double vd = E.vd[e];
+    const int vb = E.vbits[e];
+    const u64 dhi = Y0 ? div_clamp(vlo, vhi, vd, vb, Y0, xc) : xc;
+    u64 dlo = div_clamp(vlo, vhi, vd, vb, Y0 + R, xc) + 1;  // xc+1 means empty
+    if (dlo < lw) dlo = lw;
+    if (dhi >= dlo) { c = dhi - dlo + 1; top = dhi; }
+  }
+  cnt[e] = c;
+  dtop[e] = top;
+}
+
+__global__ void k_mcut_capture(ElemDev E, u64 Y0, u64 R, const int* __restrict__ M,
+                               int32_t* __restrict__ Mmc) {
+  u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E.n) return;
+  u64 mc = E.mcut[e];
+  if (mc >= Y0 && mc < Y0 + R) Mmc[e] = M[mc - Y0];
+}
+
+__global__ void k_acc_finish(ElemDev E, uint64_t* __restrict__ acc, const int32_t* __restrict__ Mmc) {
+  u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E.n) return;
+  acc[e] -= (u64)(i64)Mmc[e] * E.xcut[e];
+}
+
+__global__ void k_qgather_plan(ElemDev E, uint64_t* __restrict__ cnt) {
+  u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e > E.n) return;
+  if (e == E.n) { cnt[e] = 0; return; }
+  u64 hi = E.dq_hi[e], lo = E.lo[e];
+  cnt[e] = hi >= lo ? hi - lo + 1 : 0;
+}
+
+static int scan_u64(UpdateCtx* c, const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t st) {
+  size_t need = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, (int64_t)n, st);
+  if (need > c->cub_bytes) {
+    if (c->cub_tmp) cudaFree(c->cub_tmp);
+    MT_CUDA_CHECK(cudaMalloc(&c->cub_tmp, need));
+    c->cub_bytes = need;
+  }
+  MT_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, need, in, out, (int64_t)n, st));
+  c->launches += 1;
+  return MT_OK;
+}
+
+int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* Mmc,
+                     const uint64_t* tile_mcut_max, const uint8_t* tile_vbits_max, uint64_t ntiles,
+                     const TargetDev* tgts, int ntgt, cudaStream_t st) {
+  UpdateCtx* c = new UpdateCtx();
+  c->E = E; c->acc = acc; c->Mmc = Mmc;
+  c->tile_mcut_max = tile_mcut_max; c->tile_vbits_max = tile_vbits_max; c->ntiles = ntiles;
+  c->ntgt = ntgt;
+  c->launches = 0;
+  *out = c;
+  MT_CUDA_CHECK(cudaMalloc(&c->tgts, sizeof(TargetDev) * (ntgt ? ntgt : 1)));
+  MT_CUDA_CHECK(cudaMemcpyAsync(c->tgts, tgts, sizeof(TargetDev) * ntgt, cudaMemcpyHostToDevice, st));
+  MT_CUDA_CHECK(cudaMalloc(&c->units, sizeof(uint64_t) * (ntiles + 1) * 2));
+  MT_CUDA_CHECK(cudaMalloc(&c->cnt, sizeof(uint64_t) * (E.n + 1)));
+  MT_CUDA_CHECK(cudaMalloc(&c->dtop, sizeof(uint64_t) * (E.n + 1)));
+  MT_CUDA_CHECK(cudaMalloc(&c->off, sizeof(uint64_t) * (E.n + 1)));
+  MT_CUDA_CHECK(cudaMalloc(&c->qcnt, sizeof(uint64_t) * (E.n + 1)));
+  MT_CUDA_CHECK(cudaMalloc(&c->qoff, sizeof(uint64_t) * (E.n + 1)));
+  MT_CUDA_CHECK(cudaMalloc(&c->counter, sizeof(uint64_t) * 4));
+  c->cub_tmp = nullptr; c->cub_bytes = 0;
+  int dev; cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev);
+  return MT_OK;
+}
+
+void mt_update_destroy(UpdateCtx* c) {
+  if (!c) return;
+  cudaFree(c->tgts); cudaFree(c->units); cudaFree(c->cnt); cudaFree(c->dtop); cudaFree(c->off);
+  cudaFree(c->qcnt); cudaFree(c->qoff); cudaFree(c->counter);
+  if (c->cub_tmp) cudaFree(c->cub_tmp);
+  delete c;
+}
+
+uint64_t mt_update_launches(UpdateCtx* c) { return c->launches; }
+
+int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const int* M,
+                           cudaStream_t st) {
+  const ElemDev& E = c->E;
+  // counted walk
+  {
+    uint64_t* units = c->units;
+    uint64_t* off = c->units + (c->ntiles + 1);
+    k_counted_plan<<<(unsigned)((c->ntiles + 1 + 255) / 256), 256, 0, st>>>(c->tile_mcut_max, c->ntiles, Y0, R, units);
+    c->launches++;
+    int rc = scan_u64(c, units, off, c->ntiles + 1, st);
+    if (rc) return rc;
+    MT_CUDA_CHECK(cudaMemsetAsync(c->counter, 0, sizeof(uint64_t), st));
+    CountedArgs a{E, c->acc, c->tile_mcut_max, c->tile_vbits_max, off, c->ntiles, mu, Y0, c->counter};
+    k_counted<<<c->nsm * 6, MT_CT, 0, st>>>(a);
+    c->launches++;
+    MT_CUDA_CHECK(cudaGetLastError());
+  }
+  // M(mcut) captures
+  k_mcut_capture<<<(unsigned)((E.n + 255) / 256), 256, 0, st>>>(E, Y0, R, M, c->Mmc);
+  c->launches++;
+  // windowed dense walk
+  {
+    k_dense_plan<<<(unsigned)((E.n + 1 + 255) / 256), 256, 0, st>>>(E, Y0, R, c->cnt, c->dtop);
+    c->launches++;
+    int rc = scan_u64(c, c->cnt, c->off, E.n + 1, st);
+    if (rc) return rc;
+    MT_CUDA_CHECK(cudaMemsetAsync(c->counter + 1, 0, sizeof(uint64_t), st));
+    ItemsArgs a{E, c->acc, c->off, c->dtop, E.n, c->counter + 1, M, Y0, nullptr};
+    k_items<0><<<c->nsm * 8, 256, 0, st>>>(a);
+    c->launches++;
+    MT_CUDA_CHECK(cudaGetLastError());
+  }
+  return MT_OK;
+}
+
+int mt_update_qgather(UpdateCtx* c, cudaStream_t st) {
+  const ElemDev& E = c->E;
+  k_qgather_plan<<<(unsigned)((E.n + 1 + 255) / 256), 256, 0, st>>>(E, c->qcnt);
+  c->launches++;
+  int rc = scan_u64(c, c->qcnt, c->qoff, E.n + 1, st);
+  if (rc) return rc;
+  MT_CUDA_CHECK(cudaMemsetAsync(c->counter + 2, 0, sizeof(uint64_t), st));
+  ItemsArgs a{E, c->acc, c->qoff, E.dq_hi, E.n, c->counter + 2, nullptr, 0, c->tgts};
+  k_items<1><<<c->nsm * 8, 256, 0, st>>>(a);
+  c->launches++;
+  MT_CUDA_CHECK(cudaGetLastError());
+  return MT_OK;
+}
+
+int mt_update_finish(UpdateCtx* c, cudaStream_t st) {
+  k_acc_finish<<<(unsigned)((c->E.n + 255) / 256), 256, 0, st>>>(c->E, c->acc, c->Mmc);
+  c->launches++;
+  MT_CUDA_CHECK(cudaGetLastError());
+  return MT_OK;
+}
+
+// ---------------------------------------------------------------- final resolve
+// final[k] = 1 - acc[k] - sum_{d=2}^{D_k} final[k d]   (_native.pyx:313-334)
+// Level-parallel: k in (K/2^{L+1}, K/2^L] depends only on levels above.
+__global__ void k_fin_level(const uint64_t* __restrict__ acc, const uint64_t* __restrict__ D,
+                            int64_t* __restrict__ fin, u64 klo, u64 khi) {
+  const u64 wid = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const u64 k = klo + 1 + wid;
+  if (k > khi) return;
+  const u64 dk = D[k - 1];
+  u64 s = 0;
+  for (u64 d = 2 + lane; d <= dk; d += 32) s += (u64)fin[k * d - 1];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) fin[k - 1] = (int64_t)(1ull - acc[k - 1] - s);
+}
+
+int mt_finalize_dev(const uint64_t* acc, const uint64_t* D, uint64_t K, int64_t* fin, cudaStream_t st) {
+  if (K == 0) return MT_OK;
+  u64 khi = K;
+  while (khi > 0) {
+    u64 klo = khi / 2;
+    u64 n = khi - klo;
+    u64 threads = n * 32;
+    k_fin_level<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(acc, D, fin, klo, khi);
+    MT_CUDA_CHECK(cudaGetLastError());
+    khi = klo;
+  }
+  return MT_OK;
+}
+
+// ------------------------------------------------------ plugin: apply_block
+// Exact per-block semantics of _native.pyx:227-310 (thread per element).
+__global__ void k_apply_block(u64 K, int64_t* __restrict__ acc, const uint64_t* __restrict__ v,
+                              const uint64_t* __restrict__ lo, const uint64_t* __restrict__ xcut,
+                              const uint64_t* __restrict__ mcut, uint64_t* __restrict__ dnext,
+                              uint64_t* __restrict__ ynext, u64 a, u64 b,
+                              const int64_t* __restrict__ mp, uint64_t* __restrict__ counters) {
+  u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const u64 vk = v[k];
+  const double vd = __ull2double_rn(vk);
+  const int vb = vk ? 64 - __clzll((long long)vk) : 0;
+  u64 counted = 0, dense = 0;
+  const u64 mc = mcut[k];
+  if (mc >= a) {
+    u64 hi = mc < b ? mc : b;
+    u64 qn = udiv_any(vk, 0, vd, vb, hi + 1);
+    if (hi == mc && qn < xcut[k]) qn = xcut[k];
+    i128 delta = 0;
+    for (u64 m = hi; m >= a && m >= 1; m--) {
+      u64 q = udiv_any(vk, 0, vd, vb, m);
+      delta += (i128)(i64)(q - qn) * mp[m - a];
+      qn = q;
+    }
+    counted = hi - a + 1;
+    delta += acc[k];
+    const i128 lim = (i128)1 << 62;
+    if (delta > lim || delta < -lim) { atomicAdd((unsigned long long*)&counters[2], 1ull); return; }
+    acc[k] = (int64_t)delta;
+  }
+  if (ynext[k] <= b) {
+    u64 d = dnext[k];
+    const u64 lok = lo[k];
+    u64 d_lo = udiv_any(vk, 0, vd, vb, b + 1) + 1;
+    if (d_lo < lok) d_lo = lok;
+    u64 q = ynext[k];
+    i64 delta = 0;
+    for (;;) {
+      delta += mp[q - a];
+      dense++;
+      if (d == d_lo) break;
+      d--;
+      q = udiv_any(vk, 0, vd, vb, d);
+    }
+    acc[k] += delta;
+    dnext[k] = d_lo - 1;
+    ynext[k] = (d_lo - 1 >= lok) ? udiv_any(vk, 0, vd, vb, d_lo - 1) : ~0ull;
+  }
+  if (counted) atomicAdd((unsigned long long*)&counters[0], (unsigned long long)counted);
+  if (dense) atomicAdd((unsigned long long*)&counters[1], (unsigned long long)dense);
+}
+
+int mt_apply_block_dev(uint64_t K, int64_t* acc, const uint64_t* v, const uint64_t* lo,
+                       const uint64_t* xcut, const uint64_t* mcut, uint64_t* dnext, uint64_t* ynext,
+                       uint64_t y1, uint64_t y2, const int64_t* mp, uint64_t* counters, cudaStream_t st) {
+  if (K == 0) return MT_OK;
+  k_apply_block<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(K, acc, v, lo, xcut, mcut, dnext, ynext, y1, y2, mp, counters);
+  MT_CUDA_CHECK(cudaGetLastError());
+  return MT_OK;
+}
+
+// ------------------------------------------------ plugin: build_divisor_arrays
+// _native.pyx:32-68 (Granlund-Montgomery constants), one thread per divisor.
+__global__ void k_divisor(u64 cap, uint64_t* magic, uint8_t* shift, uint8_t* scheme) {
+  u64 d = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (d > cap) return;
+  if (d == 0) { magic[0] = 0; shift[0] = 0; scheme[0] = 0; return; }
+  int s = 63 - __clzll((long long)d);
+  if ((d & (d - 1)) == 0) { magic[d] = 0; shift[d] = (uint8_t)s; scheme[d] = 2; return; }
+  u128 num = (u128)1 << (64 + s);
+  u64 m0 = (u64)(num / d);
+  u64 rem = (u64)(num - (u128)m0 * d);
+  if (d - rem < (1ull << s)) { magic[d] = m0 + 1; shift[d] = (uint8_t)s; scheme[d] = 0; }
+  else {
+    u128 big = (s == 63) ? (~(u128)0) / d + 1 : (((u128)1 << (64 + s + 1)) + d - 1) / d;
+    magic[d] = (u64)big; shift[d] = (uint8_t)s; scheme[d] = 1;
+  }
+}
+
+int mt_divisor_arrays_dev(uint64_t cap, uint64_t* magic, uint8_t* shift, uint8_t* scheme, cudaStream_t st) {
+  k_divisor<<<(unsigned)((cap + 1 + 255) / 256), 256, 0, st>>>(cap, magic, shift, scheme);
+  MT_CUDA_CHECK(cudaGetLastError());
+  return MT_OK;
+}
