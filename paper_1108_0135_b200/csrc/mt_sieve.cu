@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(NT) k_sieve_tile(SieveTileArgs a) {
   if (a.states_out) {  // instrumented export (logprime_states parity)
     uint32_t* so = (uint32_t*)(a.states_out + tile_off);
     for (int i = tid; i < MT_TILE / 4; i += NT) so[i] = st[i];
+    __syncthreads();  // the export must finish before cells are classified in place
   }
 
   // 3. classify in place: each thread owns CH = MT_TILE/NT consecutive cells

@@ -1,0 +1,195 @@
+"""GPU parity: the sm100 engine through the C ABI vs the oracle and the
+reference's golden vectors.  Bit-exact for every integer output."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _tables(oracle, ymax):
+    pr = oracle.generate_primes(oracle.ceil_sqrt(ymax) + 1)
+    return pr, oracle.build_logs(pr), oracle.build_wheel()
+
+
+def test_sieve_golden_blocks(engine, golden, oracle):
+    from paper_1108_0135_b200._kernels import sm100
+
+    G, _ = golden
+    pr, lg, wh = _tables(oracle, 10**12 + 5000)
+    for i, y1 in enumerate(G["sieve_y1"].tolist()):
+        y2 = y1 + 4999
+        assert np.array_equal(sm100.sieve_logprime(y1, y2, pr, lg, wh), G["sieve_mu"][i])
+        sel = pr <= oracle.ceil_sqrt(y2) + 1
+        assert np.array_equal(sm100.logprime_states(y1, y2, pr[sel], lg[sel], wh), G["sieve_states"][i])
+
+
+@pytest.mark.parametrize("y1,length", [(2, 3 << 20), (10**9 - 123457, 3 << 20), (2**33 - 70000, 200000),
+                                       (4_641_588_833_612 - 10**6, 2 * 10**6)])
+def test_sieve_vs_oracle(engine, oracle, y1, length):
+    from paper_1108_0135_b200._kernels import sm100
+
+    y2 = y1 + length - 1
+    pr, lg, wh = _tables(oracle, y2)
+    a = sm100.sieve_logprime(y1, y2, pr, lg, wh)
+    b = oracle.get_kernels("c").sieve_logprime(y1, y2, pr, lg, wh)
+    assert np.array_equal(a, b)
+    assert np.array_equal(sm100.sieve_naive(y1, y2, pr), b)
+
+
+def test_mertens_range_vs_oracle(engine, oracle):
+    from paper_1108_0135_b200 import _lib
+
+    L = _lib.lib()
+    n = 3_000_000
+    m = np.zeros(n, np.int64)
+    _lib.check(L.mt_mertens_range(1, n, _lib.ptr(m)))
+    assert np.array_equal(m, oracle.mertens_table(n))
+
+
+def test_divisor_arrays(engine, golden):
+    from paper_1108_0135_b200._kernels import sm100
+
+    G, _ = golden
+    m, s, c = sm100.build_divisor_arrays(4096)
+    assert np.array_equal(m, G["div_magic"]) and np.array_equal(s, G["div_shift"]) and np.array_equal(c, G["div_scheme"])
+
+
+def test_finalize_golden(engine, golden):
+    from paper_1108_0135_b200._kernels import sm100
+
+    G, _ = golden
+    assert np.array_equal(sm100.finalize_recursion(G["e10_tails"], G["e10_D"]), G["e10_final"])
+
+
+def test_apply_block_chain_golden(engine, golden, oracle):
+    """Per-block acc/dnext/ynext and counters of the reference's apply_block."""
+    from paper_1108_0135_b200._kernels import sm100
+
+    G, J = golden
+    blk = J["blk"]
+    H = oracle.HarmonicArray(blk["n"], blk["u"])
+    y, m_run, nb, cnt = 1, 0, 0, [0, 0]
+    k = oracle.get_kernels("c")
+    snaps = {s["tag"]: s for s in blk["snaps"]}
+    while y <= blk["u"]:
+        y2 = min(y + blk["block_len"] - 1, blk["u"])
+        mp = np.cumsum(oracle.mu_range(k, y, y2), dtype=np.int64) + m_run
+        c, d = sm100.apply_block(H.acc, H.v, H.lo, H.xcut, H.mcut, H.dnext, H.ynext, y, y2, mp)
+        cnt[0] += c
+        cnt[1] += d
+        m_run, y, nb = int(mp[-1]), y2 + 1, nb + 1
+        tag = {1: "b1", 3: "b3"}.get(nb)
+        if tag:
+            assert np.array_equal(H.acc, G[f"blk_{tag}_acc"])
+            assert np.array_equal(H.dnext, G[f"blk_{tag}_dnext"])
+            assert np.array_equal(H.ynext, G[f"blk_{tag}_ynext"])
+            assert cnt == [snaps[tag]["counted"], snaps[tag]["dense"]]
+    assert np.array_equal(H.acc, G["blk_end_acc"])
+
+
+def test_apply_block_overflow_guard(engine):
+    from paper_1108_0135_b200._kernels import sm100
+
+    acc = np.array([2**62 - 5], np.int64)
+    v = np.array([10**6], np.uint64)
+    one = np.array([1], np.uint64)
+    with pytest.raises(OverflowError):
+        sm100.apply_block(acc, v, np.array([2], np.uint64), one * 250, one * 3984, one * 250,
+                          np.array([4000], np.uint64), 1, 10, np.full(10, 1000, np.int64))
+
+
+def test_small_n_all(engine, golden):
+    G, _ = golden
+    ms = G["m_upto_1e4"]
+    for n in list(range(1, 60)) + [100, 1000, 1023, 1024, 1025, 2048, 4096, 5000, 9999, 10000]:
+        assert engine.mertens_exact(n).value == int(ms[n - 1]), n
+
+
+def test_seeded_100(engine, golden):
+    G, _ = golden
+    for n, m in zip(G["seeded_n"].tolist(), G["seeded_m"].tolist()):
+        assert engine.mertens_exact(n).value == m, n
+
+
+def test_e10_full_quotient_map(engine, golden):
+    G, J = golden
+    r = engine.mertens_exact(10**10)
+    assert r.value == -33722 and r.backend == "sm100" and r.u == J["e10"]["u"]
+    assert np.array_equal(r._final, G["e10_final"])
+    assert np.array_equal(r._cp_q, G["e10_cp_q"]) and np.array_equal(r._cp_m, G["e10_cp_m"])
+    assert (r.stats.counted_items, r.stats.dense_items, r.stats.blocks, r.stats.divtable_released_at) == (
+        J["e10"]["counted_items"], J["e10"]["dense_items"], J["e10"]["blocks"], J["e10"]["divtable_released_at"])
+    assert r.quotient(3) == 14572
+    assert engine.mertens_identity_residual(r) == 0
+    qs = list(r.quotients())
+    assert len(qs) == 2154 + len(G["e10_cp_q"]) - sum(1 for q in G["e10_cp_q"].tolist() if q >= 10**10 // 2154)
+
+
+@pytest.mark.parametrize("n,key", [(10**11, "e11"), (10**12, "e12"), (7_766_842_813, "7766842813"),
+                                   (999_999_999_989, "999999999989"), (2**40 + 12345, "1099511640121")])
+def test_reference_values(engine, golden, n, key):
+    _, J = golden
+    assert engine.mertens_exact(n).value == J[key]
+
+
+def test_ac2_ratio(engine):
+    r = engine.mertens_exact(7_766_842_813)
+    assert round(abs(r.ratio), 6) == 0.570591
+
+
+def test_multi(engine, golden):
+    G, J = golden
+    mm = engine.mertens_exact_multi([10**10, 10**10 + 1, 10**10 + 2])
+    assert {str(k): v.value for k, v in mm.items()} == J["multi_e10"]
+    assert np.array_equal(mm[10**10 + 1]._final, G["multi_e10_final_1"])
+
+
+def test_multi_vs_oracle(engine, oracle):
+    ns = [10**9 + 3 * i for i in range(8)]
+    got = engine.mertens_exact_multi(ns)
+    ref = oracle.mertens_exact_multi(ns)
+    for n in ns:
+        assert got[n].value == ref[n].value
+        assert np.array_equal(got[n]._final, ref[n].final)
+
+
+def test_u_invariance(engine):
+    """M values do not depend on u."""
+    n = 3 * 10**11 + 17
+    base = engine.mertens_exact(n).value
+    for alpha in (0.5, 2.0):
+        assert engine.mertens_exact(n, engine.EngineConfig(u_alpha=alpha)).value == base
+
+
+def test_segment_size_invariance(engine):
+    n = 10**13
+    a = engine.mertens_exact(n)
+    b = engine.mertens_exact(n, engine.EngineConfig(seg_log2_head=20, seg_log2_tail=22))
+    c = engine.mertens_exact(n, engine.EngineConfig(q_budget_bytes=1 << 20))
+    assert a.value == b.value == c.value == 599582
+    assert np.array_equal(a._final, b._final) and np.array_equal(a._final, c._final)
+
+
+def test_naive_and_verify(engine, golden):
+    G, _ = golden
+    v, cp = engine.mertens_naive(10**6, checkpoints=np.array([1, 10, 100, 10**4, 10**6], np.uint64))
+    assert v == 212 and cp.tolist() == [1, -1, 1, -23, 212]
+    rep = engine.verify_paired(10**6, 20, 42)
+    assert rep["mismatches"] == [] and rep["checked"] == 20
+    rep = engine.verify_paired(10**5, 5, 42, fault_inject=2)
+    assert len(rep["mismatches"]) == 1
+
+
+@pytest.mark.parametrize("e", [13, 14, 15])
+def test_survey_reference_values(engine, golden, e):
+    _, J = golden
+    assert engine.mertens_exact(10**e).value == J["reference_measured_survey"][f"1e{e}"]
+
+
+@pytest.mark.slow
+def test_paper_1e16_and_quotients(engine, golden):
+    _, J = golden
+    r = engine.mertens_exact(10**16)
+    assert r.value == J["paper"]["1e16"] == -3195437
+    assert r.quotient(10) == J["reference_measured_survey"]["1e15"]
+    assert r.quotient(1000) == J["reference_measured_survey"]["1e13"]
