@@ -431,6 +431,50 @@ __global__ void k_elem_split(u64 n_elem, const u64* __restrict__ k, const uint32
   lo_w[e] = lw > l ? lw : l;
 }
 
+// windowed-walk split d_sp: shared-memory windows for d >= d_sp (y up to ~C sqrt(v)),
+// C = min(64, cbrt(sqrt(v)/2)) so the incremental quotient walk needs <= 1
+// correction per step (second difference 2y/d^2 <= 1).
+__global__ void k_elem_dsp(u64 n_elem, const double* __restrict__ vd, u64* __restrict__ dsp) {
+  u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_elem) return;
+  double s = sqrt(vd[e]);
+  double c = cbrt(0.5 * s);
+  if (c > MT_WIN_SPLIT) c = MT_WIN_SPLIT;
+  if (c < 1.0) c = 1.0;
+  dsp[e] = (u64)ceil(s / c);
+}
+
+// per group: y-range of the window walk and the wide-walk flag
+__global__ void k_group_meta(const u64* __restrict__ gstart, u64 ng, const u64* __restrict__ vlo,
+                             const u64* __restrict__ vhi, const u64* __restrict__ xcut,
+                             const u64* __restrict__ lo_w, const u64* __restrict__ dsp,
+                             u64* __restrict__ ylo, u64* __restrict__ yhi, uint8_t* __restrict__ wide) {
+  u64 g = blockIdx.x;
+  if (g >= ng) return;
+  u64 mn = ~0ull, mx = 0;
+  int w = 0;
+  for (u64 e = gstart[g] + threadIdx.x; e < gstart[g + 1]; e += blockDim.x) {
+    u64 xc = xcut[e], lw = lo_w[e] > dsp[e] ? lo_w[e] : dsp[e];
+    if (lw > xc) continue;
+    u128 v = ((u128)vhi[e] << 64) | vlo[e];
+    u128 a = v / xc, b = v / lw;
+    u64 a64 = a > (u128)~0ull ? ~0ull : (u64)a, b64 = b > (u128)~0ull ? ~0ull : (u64)b;
+    if (a64 < mn) mn = a64;
+    if (b64 > mx) mx = b64;
+    if (xc >= (1ull << 30)) w = 1;
+  }
+  typedef cub::BlockReduce<u64, 256> BR;
+  __shared__ typename BR::TempStorage t1, t2;
+  __shared__ int sw;
+  if (threadIdx.x == 0) sw = 0;
+  __syncthreads();
+  if (w) sw = 1;
+  u64 rmn = BR(t1).Reduce(mn, cub::Min());
+  u64 rmx = BR(t2).Reduce(mx, cub::Max());
+  __syncthreads();
+  if (threadIdx.x == 0) { ylo[g] = rmn; yhi[g] = rmx; wide[g] = (uint8_t)sw; }
+}
+
 __global__ void k_tile_meta(u64 n_elem, const u64* __restrict__ mcut, const uint8_t* __restrict__ vbits,
                             u64* __restrict__ tmax, uint8_t* __restrict__ tbits) {
   u64 t = blockIdx.x;
@@ -472,11 +516,12 @@ __global__ void k_window_extent(u64 n_elem, const u64* __restrict__ vlo, const u
   atomicMax(out, (unsigned long long)(y > (u128)~0ull ? ~0ull : (u64)y));
 }
 
-__global__ void k_copy_small(const int* __restrict__ M, u64 Y0, u64 R, u64 ymax, int64_t* __restrict__ out) {
+__global__ void k_copy_small(const int16_t* __restrict__ M16, const int64_t* __restrict__ bk, u64 Y0, u64 R,
+                             u64 ymax, int64_t* __restrict__ out) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   u64 y = Y0 + i;
   if (i >= R || y > ymax) return;
-  out[y] = M[i];
+  out[y] = M16[i] + bk[i / MT_BLK];
 }
 
 __global__ void k_copy_caps(const int* __restrict__ Q, u64 jq0, u64 c_lo, u64 cnt, int64_t* __restrict__ out) {
@@ -514,12 +559,12 @@ extern "C" int mt_run(const mt_job* job, mt_result* out) {
   u64 launches = 0;
 
   // ---- elements
-  DevBuf d_nlo, d_nhi, d_e0, d_vd, d_vlo, d_vhi, d_vb, d_k, d_tgt, d_D, d_x, d_mc, d_lo, d_low, d_dq, d_acc, d_mmc;
+  DevBuf d_nlo, d_nhi, d_e0, d_vd, d_vlo, d_vhi, d_vb, d_k, d_tgt, d_D, d_x, d_mc, d_lo, d_low, d_dq, d_acc, d_mmc, d_dsp;
   RC(dalloc(d_nlo, N * 8)); RC(dalloc(d_nhi, N * 8)); RC(dalloc(d_e0, (N + 1) * 8));
   RC(dalloc(d_vd, NE * 8)); RC(dalloc(d_vlo, NE * 8)); RC(dalloc(d_vhi, NE * 8)); RC(dalloc(d_vb, NE));
   RC(dalloc(d_k, NE * 8)); RC(dalloc(d_tgt, NE * 4)); RC(dalloc(d_D, NE * 8)); RC(dalloc(d_x, NE * 8));
   RC(dalloc(d_mc, NE * 8)); RC(dalloc(d_lo, NE * 8)); RC(dalloc(d_low, NE * 8)); RC(dalloc(d_dq, NE * 8));
-  RC(dalloc(d_acc, NE * 8)); RC(dalloc(d_mmc, NE * 4));
+  RC(dalloc(d_acc, NE * 8)); RC(dalloc(d_mmc, NE * 4)); RC(dalloc(d_dsp, NE * 8));
   MT_CUDA_CHECK(cudaMemcpyAsync(d_nlo.p, job->n_lo, N * 8, cudaMemcpyHostToDevice, st));
   MT_CUDA_CHECK(cudaMemcpyAsync(d_nhi.p, job->n_hi, N * 8, cudaMemcpyHostToDevice, st));
   MT_CUDA_CHECK(cudaMemcpyAsync(d_e0.p, e0.data(), (N + 1) * 8, cudaMemcpyHostToDevice, st));
@@ -596,7 +641,26 @@ extern "C" int mt_run(const mt_job* job, mt_result* out) {
   RC(dalloc(d_J, N * 8));
   MT_CUDA_CHECK(cudaMemcpyAsync(d_J.p, J.data(), N * 8, cudaMemcpyHostToDevice, st));
   if (NE) k_elem_split<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, d_k.as<u64>(), d_tgt.as<uint32_t>(), d_J.as<u64>(), d_lo.as<u64>(), d_x.as<u64>(), d_low.as<u64>(), d_dq.as<u64>());
+  if (NE) k_elem_dsp<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, d_vd.as<double>(), d_dsp.as<u64>());
+  launches += 2;
+  // element groups for the window walk: consecutive k of one target, size clamp(k/8, 32, 1024)
+  std::vector<u64> gstart;
+  for (int i = 0; i < N; i++) {
+    u64 k0 = 1;
+    while (k0 <= K[i]) {
+      gstart.push_back(e0[i] + k0 - 1);
+      u64 g = std::min<u64>(1024, std::max<u64>(32, k0 / 8));
+      k0 += g;
+    }
+  }
+  const u64 ng = gstart.size();
+  gstart.push_back(NE);
+  DevBuf d_gs, d_gylo, d_gyhi, d_gw;
+  RC(dalloc(d_gs, (ng + 1) * 8)); RC(dalloc(d_gylo, ng * 8)); RC(dalloc(d_gyhi, ng * 8)); RC(dalloc(d_gw, ng));
+  MT_CUDA_CHECK(cudaMemcpyAsync(d_gs.p, gstart.data(), (ng + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (ng) k_group_meta<<<(unsigned)ng, 256, 0, st>>>(d_gs.as<u64>(), ng, d_vlo.as<u64>(), d_vhi.as<u64>(), d_x.as<u64>(), d_low.as<u64>(), d_dsp.as<u64>(), d_gylo.as<u64>(), d_gyhi.as<u64>(), d_gw.as<uint8_t>());
   launches++;
+  GroupDev grp{d_gs.as<u64>(), d_gylo.as<u64>(), d_gyhi.as<u64>(), d_gw.as<uint8_t>(), ng};
   {
     DevBuf d_we;
     RC(dalloc(d_we, 8));
@@ -619,7 +683,7 @@ extern "C" int mt_run(const mt_job* job, mt_result* out) {
   launches++;
 
   // ---- segments
-  const u64 Rh = 1ull << (job->seg_log2_head ? job->seg_log2_head : 25);
+  const u64 Rh = 1ull << (job->seg_log2_head ? job->seg_log2_head : 24);
   const u64 Rt = 1ull << (job->seg_log2_tail ? job->seg_log2_tail : 27);
   if (Rh < MT_TILE || Rt < Rh || (Rt % Rh)) { mt_set_error("bad segment sizes"); return MT_ERR_VALUE; }
   const u64 head_segs = (head_end + 1 + Rh - 1) / Rh;
@@ -635,14 +699,14 @@ extern "C" int mt_run(const mt_job* job, mt_result* out) {
   std::vector<uint32_t> w32;
   build_wheel_words(wheel, w32);
   const u64 np = pt.p.size();
-  DevBuf d_p, d_rp, d_lg, d_w32, d_big, d_mu, d_m, d_tsum, d_tbase, d_run, d_caps, d_small;
+  DevBuf d_p, d_rp, d_lg, d_w32, d_big, d_mu, d_m, d_half, d_bk, d_tsum, d_tbase, d_run, d_caps, d_small;
   RC(dalloc(d_p, np * 4)); RC(dalloc(d_rp, np * 8)); RC(dalloc(d_lg, np));
   RC(dalloc(d_w32, w32.size() * 4));
   MT_CUDA_CHECK(cudaMemcpyAsync(d_p.p, pt.p.data(), np * 4, cudaMemcpyHostToDevice, st));
   MT_CUDA_CHECK(cudaMemcpyAsync(d_rp.p, pt.r.data(), np * 8, cudaMemcpyHostToDevice, st));
   MT_CUDA_CHECK(cudaMemcpyAsync(d_lg.p, pt.lg.data(), np, cudaMemcpyHostToDevice, st));
   MT_CUDA_CHECK(cudaMemcpyAsync(d_w32.p, w32.data(), w32.size() * 4, cudaMemcpyHostToDevice, st));
-  RC(dalloc(d_big, Rt)); RC(dalloc(d_mu, Rh)); RC(dalloc(d_m, Rh * 4));
+  RC(dalloc(d_big, Rt)); RC(dalloc(d_mu, Rh)); RC(dalloc(d_m, Rh * 2)); RC(dalloc(d_half, (Rt / MT_TILE) * 4)); RC(dalloc(d_bk, (Rh / MT_BLK) * 8 + 8));
   RC(dalloc(d_tsum, (Rt / MT_TILE) * 4)); RC(dalloc(d_tbase, (Rt / MT_TILE) * 8)); RC(dalloc(d_run, 8));
   MT_CUDA_CHECK(cudaMemsetAsync(d_run.p, 0, 8, st));
   RC(dalloc(d_caps, caps.size() * sizeof(CaptureTargetH)));
@@ -654,10 +718,10 @@ extern "C" int mt_run(const mt_job* job, mt_result* out) {
   ElemDev E;
   E.vd = d_vd.as<double>(); E.vlo = d_vlo.as<u64>(); E.vhi = d_vhi.as<u64>(); E.vbits = d_vb.as<uint8_t>();
   E.k = d_k.as<u64>(); E.tgt = d_tgt.as<uint32_t>(); E.mcut = d_mc.as<u64>(); E.xcut = d_x.as<u64>();
-  E.lo = d_lo.as<u64>(); E.lo_w = d_low.as<u64>(); E.dq_hi = d_dq.as<u64>(); E.n = NE;
+  E.lo = d_lo.as<u64>(); E.lo_w = d_low.as<u64>(); E.dq_hi = d_dq.as<u64>(); E.d_sp = d_dsp.as<u64>(); E.n = NE;
   UpdateCtx* uc = nullptr;
   RC(mt_update_create(&uc, E, d_acc.as<u64>(), d_mmc.as<int32_t>(), d_tmax.as<u64>(), d_tbits.as<uint8_t>(),
-                      ntiles, tdev.data(), N, st));
+                      ntiles, tdev.data(), N, grp, st));
   struct UcGuard { UpdateCtx* c; ~UcGuard() { mt_update_destroy(c); } } ug{uc};
 
   cudaEvent_t ev[6];
@@ -674,6 +738,7 @@ extern "C" int mt_run(const mt_job* job, mt_result* out) {
     s.primes = d_p.as<uint32_t>(); s.rprimes = d_rp.as<double>(); s.logs = d_lg.as<uint8_t>();
     s.p_large_begin = c.small_end; s.p_large_end = c.large_end; s.do_logs_large = 1;
     s.running = d_run.as<int64_t>(); s.tile_base = d_tbase.as<int64_t>();
+    s.bk = head ? d_bk.as<int64_t>() : nullptr;
     SieveTileArgs& a = s.tile;
     a.Y0 = Y0; a.y2 = y2; a.wheel32x = d_w32.as<uint32_t>(); a.big = s.big;
     a.primes = s.primes; a.rprimes = s.rprimes; a.logs = s.logs;
@@ -681,7 +746,9 @@ extern "C" int mt_run(const mt_job* job, mt_result* out) {
     a.log_min = 11; a.do_logs = 1;
     a.tile_sum = d_tsum.as<int>();
     a.mu_out = head ? d_mu.as<int8_t>() : nullptr;
-    a.m_out = head ? d_m.as<int>() : nullptr;
+    a.m_out = nullptr;
+    a.m16_out = head ? d_m.as<int16_t>() : nullptr;
+    a.half_out = d_half.as<int>();
     a.states_out = nullptr;
     a.caps = d_caps.p; a.n_cap = (int)caps.size();
     return s;
@@ -693,9 +760,9 @@ extern "C" int mt_run(const mt_job* job, mt_result* out) {
     SieveSegment sg = make_seg(Y0, Rh, true);
     RC(mt_launch_sieve_segment(sg, st));
     launches += 6;
-    RC(mt_update_head_segment(uc, Y0, Rh, d_mu.as<int8_t>(), d_m.as<int>(), st));
+    RC(mt_update_head_segment(uc, Y0, Rh, d_mu.as<int8_t>(), d_m.as<int16_t>(), d_bk.as<int64_t>(), st));
     if (nsmall && Y0 <= job->cap_small) {
-      k_copy_small<<<(unsigned)((Rh + 255) / 256), 256, 0, st>>>(d_m.as<int>(), Y0, Rh, job->cap_small, d_small.as<int64_t>());
+      k_copy_small<<<(unsigned)((Rh + 255) / 256), 256, 0, st>>>(d_m.as<int16_t>(), d_bk.as<int64_t>(), Y0, Rh, job->cap_small, d_small.as<int64_t>());
       launches++;
     }
   }

@@ -11,6 +11,8 @@
 #define MT_WHEEL_WORDS (MT_WHEEL / 4)
 #define MT_CT 256               // elements per counted-walk tile (threads per CTA)
 #define MT_CM 2048              // m values per counted-walk work unit
+#define MT_BLK 32768u           // M16 block: values stored relative to M(block start - 1)
+#define MT_WIN_SPLIT 64         // d_sp = ceil(sqrt(v)/64): windowed walk up to y ~ 64 sqrt(v)
 
 struct SieveTileArgs {
   uint64_t Y0;                   // segment start (multiple of MT_TILE)
@@ -27,7 +29,9 @@ struct SieveTileArgs {
   int do_logs;
   int* tile_sum;                 // [ntiles]
   int8_t* mu_out;                // segment mu (or null)
-  int* m_out;                    // segment partial/absolute M (or null)
+  int* m_out;                    // segment partial M (in-tile prefix) (or null)
+  int16_t* m16_out;              // M(y) - M(start of its 32K block - 1)   (or null)
+  int* half_out;                 // [ntiles] in-tile prefix at the tile's 32K midpoint
   uint8_t* states_out;           // raw states (instrumented) or null
   const void* caps;              // CaptureTarget[n_cap] (device)
   int n_cap;
@@ -43,6 +47,7 @@ struct SieveSegment {
   int do_logs_large;
   int64_t* running;              // device scalar M(Y0-1) (null: no scan)
   int64_t* tile_base;            // [ntiles]
+  int64_t* bk;                   // [2*ntiles] absolute M(start of 32K block - 1) (or null)
   SieveTileArgs tile;
 };
 
@@ -61,6 +66,7 @@ struct ElemDev {
   const uint64_t* lo;    // max(2, D+1)
   const uint64_t* lo_w;  // first d of the windowed dense walk: max(lo, J/k + 1)
   const uint64_t* dq_hi; // last d of the Q-gather walk: min(xcut, J/k)
+  const uint64_t* d_sp;  // windowed walk split: d >= d_sp in shared-memory windows, d < d_sp gathered from L2
   uint64_t n;            // total elements
 };
 
@@ -71,12 +77,20 @@ struct TargetDev {       // per-target constants for Q lookups
 
 // update-side launchers (mt_update.cu)
 struct UpdateCtx;
+struct GroupDev {        // element groups for the shared-memory window walk
+  const uint64_t* start; // [ng+1] first element of each group
+  const uint64_t* ylo;   // [ng] min first window-walk quotient
+  const uint64_t* yhi;   // [ng] max last window-walk quotient
+  const uint8_t* wide;   // [ng] 1 if some member has xcut >= 2^30 (64-bit walk)
+  uint64_t ng;
+};
 int mt_update_create(UpdateCtx** ctx, const ElemDev& E, uint64_t* acc, int32_t* Mmc,
                      const uint64_t* tile_mcut_max, const uint8_t* tile_vbits_max,
-                     uint64_t ntiles, const TargetDev* tgts, int ntgt, cudaStream_t st);
+                     uint64_t ntiles, const TargetDev* tgts, int ntgt, const GroupDev& grp,
+                     cudaStream_t st);
 void mt_update_destroy(UpdateCtx* ctx);
 int mt_update_head_segment(UpdateCtx* ctx, uint64_t Y0, uint64_t R, const int8_t* mu,
-                           const int* M, cudaStream_t st);
+                           const int16_t* M16, const int64_t* bk, cudaStream_t st);
 int mt_update_qgather(UpdateCtx* ctx, cudaStream_t st);
 int mt_update_finish(UpdateCtx* ctx, cudaStream_t st);  // acc -= M(mcut)*xcut
 int mt_finalize_dev(const uint64_t* acc, const uint64_t* D, uint64_t K, int64_t* final_out,

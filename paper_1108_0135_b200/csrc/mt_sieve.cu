@@ -194,11 +194,17 @@ __global__ void __launch_bounds__(NT) k_sieve_tile(SieveTileArgs a) {
   __syncthreads();
   int run = warp_tot[tid >> 5] + incl - tsum;  // exclusive prefix of this thread's chunk
 
-  // 4. outputs: mu (int8), partial M (int32, without the tile base), per-32 partials
+  // 4. outputs: mu (int8), in-tile prefix (int32), 32K-block-relative M (int16),
+  //    per-32-cell partials for the captures
+  __shared__ int s_half;
+  if (tid == NT / 2) s_half = run;  // exclusive prefix at the tile's 32K midpoint
+  __syncthreads();
   {
     const u32* my = st + tid * CW;
     int8_t* mu_out = a.mu_out ? a.mu_out + tile_off + (u64)tid * CH : nullptr;
     int* m_out = a.m_out ? a.m_out + tile_off + (u64)tid * CH : nullptr;
+    int16_t* m16 = a.m16_out ? a.m16_out + tile_off + (u64)tid * CH : nullptr;
+    const int hb = (tid >= NT / 2) ? s_half : 0;
     for (int wi = 0; wi < CW; wi++) {
       u32 w = my[wi];
       if (mu_out) ((u32*)mu_out)[wi] = w;
@@ -207,9 +213,16 @@ __global__ void __launch_bounds__(NT) k_sieve_tile(SieveTileArgs a) {
       int c2 = c1 + (int)(int8_t)((w >> 16) & 0xff);
       int c3 = c2 + (int)(int8_t)(w >> 24);
       if (m_out) ((int4*)m_out)[wi] = make_int4(c0, c1, c2, c3);
+      if (m16) {
+        uint2 pk;
+        pk.x = (u32)(uint16_t)(c0 - hb) | ((u32)(uint16_t)(c1 - hb) << 16);
+        pk.y = (u32)(uint16_t)(c2 - hb) | ((u32)(uint16_t)(c3 - hb) << 16);
+        ((uint2*)m16)[wi] = pk;
+      }
       run = c3;
       if ((wi & 7) == 7) pre32[(tid * CH + wi * 4) >> 5] = run;
     }
+    if (a.half_out && tid == 0) a.half_out[blockIdx.x] = s_half;
   }
   __syncthreads();
 
@@ -245,7 +258,8 @@ __global__ void __launch_bounds__(NT) k_sieve_tile(SieveTileArgs a) {
 
 // exclusive tile bases for one segment + running M (device scalar)
 __global__ void k_seg_scan(const int* __restrict__ tile_sum, int ntiles, i64* __restrict__ running,
-                           i64* __restrict__ tile_base) {
+                           i64* __restrict__ tile_base, const int* __restrict__ half,
+                           i64* __restrict__ bk) {
   // single block of 1024 threads, sequential over chunks of 1024 tiles
   __shared__ i64 wsum[32];
   __shared__ i64 carry;
@@ -272,7 +286,10 @@ __global__ void k_seg_scan(const int* __restrict__ tile_sum, int ntiles, i64* __
     }
     __syncthreads();
     i64 excl = carry + wsum[tid >> 5] + incl - v;
-    if (i < ntiles) tile_base[i] = excl;
+    if (i < ntiles) {
+      tile_base[i] = excl;
+      if (bk) { bk[2 * i] = excl; bk[2 * i + 1] = excl + half[i]; }
+    }
     __syncthreads();
     if (tid == 1023) carry = excl + v;
     __syncthreads();
@@ -329,7 +346,7 @@ int mt_launch_sieve_segment(const SieveSegment& s, cudaStream_t st) {
   k_sieve_tile<MT_SIEVE_THREADS><<<ntiles, MT_SIEVE_THREADS, smem, st>>>(a);
   MT_CUDA_CHECK(cudaGetLastError());
   if (s.running) {
-    k_seg_scan<<<1, 1024, 0, st>>>(a.tile_sum, ntiles, s.running, s.tile_base);
+    k_seg_scan<<<1, 1024, 0, st>>>(a.tile_sum, ntiles, s.running, s.tile_base, a.half_out, s.bk);
     MT_CUDA_CHECK(cudaGetLastError());
     if (a.m_out) {
       u64 n4 = s.R / 4;

@@ -43,6 +43,10 @@ struct UpdateCtx {
   uint64_t* qcnt;    // [n+1]
   uint64_t* qoff;    // [n+1]
   uint64_t* counter; // work counters [4]
+  GroupDev G;
+  uint64_t* gunits;  // [ng+1] windows per group, then exclusive offsets
+  uint64_t* guoff;   // [ng+1]
+  uint64_t* gwfirst; // [ng]
   void* cub_tmp;
   size_t cub_bytes;
   uint64_t launches;
@@ -213,69 +217,41 @@ __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
   }
 }
 
-// ------------------------------------------------------- dense: item machinery
-struct ItemsArgs {
-  ElemDev E;
-  uint64_t* acc;
-  const uint64_t* off;   // [n+1]
-  const uint64_t* dtop;  // [n]
-  uint64_t n;
-  uint64_t* counter;
-  // windowed mode
-  const int* M;
-  u64 Y0;
-  // Q mode
-  const TargetDev* tgts;
-};
-
-template <int MODE>
-__global__ void __launch_bounds__(256) k_items(ItemsArgs a) {
-  const int lane = threadIdx.x & 31;
-  const u64 total = a.off[a.n];
-  for (;;) {
-    u64 w = 0;
-    if (lane == 0) w = atomicAdd((unsigned long long*)a.counter, 1ull);
-    w = __shfl_sync(0xffffffffu, w, 0);
-    const u64 base = w * (32ull * IPT);
-    if (base >= total) break;
-    u64 i = base + lane;
-    if (i >= total) continue;
-    u64 e = upper_idx(a.off, a.n + 1, i);
-    u64 e_lo = a.off[e], e_hi = a.off[e + 1];
-    u64 top = a.dtop[e];
-    double vd = a.E.vd[e];
-    u64 vlo = a.E.vlo[e], vhi = a.E.vhi[e];
-    int vb = a.E.vbits[e];
-    u64 kk = a.E.k[e];
-    const int* Qt = nullptr;
-    u64 jq0 = 0;
-    if (MODE == 1) { TargetDev t = a.tgts[a.E.tgt[e]]; Qt = t.Q; jq0 = t.jq0; }
-    i64 sum = 0;
-    for (int s = 0; s < IPT; s++, i += 32) {
-      if (i >= total) break;
-      if (i >= e_hi) {
-        if (sum) atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)sum);
-        sum = 0;
-        e = upper_idx(a.off, a.n + 1, i);
-        e_lo = a.off[e]; e_hi = a.off[e + 1];
-        top = a.dtop[e];
-        vd = a.E.vd[e]; vlo = a.E.vlo[e]; vhi = a.E.vhi[e]; vb = a.E.vbits[e];
-        kk = a.E.k[e];
-        if (MODE == 1) { TargetDev t = a.tgts[a.E.tgt[e]]; Qt = t.Q; jq0 = t.jq0; }
+// ------------------------------------------------------- dense walk machinery
+// walk d = dh, dh-1, ..., dl with y = floor(v/d), calling f(y) for each;
+// incremental quotients: v = y (d+1) + r  =>  y(d) = y + floor((y + r)/d)
+template <bool WIDE, class F>
+__device__ __forceinline__ void walk_quotients(u64 vlo, u64 vhi, double vd, int vb, u64 dh, u64 dl, F f) {
+  double rd = __drcp_rn((double)dh);
+  u64 y = qdiv_ok(vb, dh) ? qdiv64(vd, rd, vlo, dh) : (u64)udiv128(vlo, vhi, dh);
+  u64 delta = (u64)((double)y * rd);
+  u64 d = dh;
+  if (!WIDE) {
+    u32 r = (u32)vlo - (u32)y * (u32)d;
+    for (;;) {
+      f(y);
+      if (d == dl) break;
+      --d;
+      u32 t = r + (u32)y - (u32)delta * (u32)d;
+      while (t >= (u32)d) {
+        if ((int)t < 0) { delta--; t += (u32)d; } else { delta++; t -= (u32)d; }
       }
-      const u64 d = top - (i - e_lo);
-      if (MODE == 0) {
-        u64 y;
-        const bool ok = (vb <= 50) || (d >= (1ull << (vb - 50)));
-        if (ok && d < (1ull << 31)) y = qdiv32(vd, __drcp_rn((double)d), (u32)vlo, (u32)d);
-        else if (ok) y = qdiv64(vd, __drcp_rn((double)d), vlo, d);
-        else y = (u64)udiv128(vlo, vhi, d);
-        sum += a.M[y - a.Y0];
-      } else {
-        sum += Qt[kk * d - jq0];
-      }
+      r = t;
+      y += delta;
     }
-    if (sum) atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)sum);
+  } else {
+    u64 r = vlo - y * d;
+    for (;;) {
+      f(y);
+      if (d == dl) break;
+      --d;
+      u64 t = r + y - delta * d;
+      while (t >= d) {
+        if ((i64)t < 0) { delta--; t += d; } else { delta++; t -= d; }
+      }
+      r = t;
+      y += delta;
+    }
   }
 }
 
@@ -289,33 +265,196 @@ __device__ __forceinline__ u64 div_clamp(u64 vlo, u64 vhi, double vd, int vb, u6
   return q > clamp ? clamp : q;
 }
 
-// windowed dense plan for one head segment: items d in [max(lo_w, v/(Y0+R)+1), min(xcut, v/Y0)]
-__global__ void k_dense_plan(ElemDev E, u64 Y0, u64 R, uint64_t* __restrict__ cnt,
-                             uint64_t* __restrict__ dtop) {
+// ---- shared-memory window walk: units (element group, 32K window of the segment)
+__global__ void k_win_plan(GroupDev G, u64 Y0, u64 R, uint64_t* __restrict__ units,
+                           uint64_t* __restrict__ wfirst) {
+  u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > G.ng) return;
+  if (g == G.ng) { units[g] = 0; return; }
+  u64 lo = G.ylo[g], hi = G.yhi[g];
+  u64 a = lo > Y0 ? lo : Y0, b = hi < Y0 + R - 1 ? hi : Y0 + R - 1;
+  if (lo > hi || a > b) { units[g] = 0; wfirst[g] = 0; return; }
+  u64 w0 = (a - Y0) / MT_BLK, w1 = (b - Y0) / MT_BLK;
+  units[g] = w1 - w0 + 1;
+  wfirst[g] = w0;
+}
+
+struct WinArgs {
+  ElemDev E;
+  uint64_t* acc;
+  GroupDev G;
+  const uint64_t* uoff;
+  const uint64_t* wfirst;
+  const int16_t* M16;
+  const int64_t* bk;
+  u64 Y0;
+  uint64_t* counter;
+};
+
+__global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
+  extern __shared__ int4 smem_win[];
+  int16_t* sw = (int16_t*)smem_win;
+  __shared__ u64 s_unit;
+  const int tid = threadIdx.x;
+  const u64 total = a.uoff[a.G.ng];
+  for (;;) {
+    if (tid == 0) s_unit = atomicAdd((unsigned long long*)a.counter, 1ull);
+    __syncthreads();
+    const u64 unit = s_unit;
+    if (unit >= total) break;
+    const u64 g = upper_idx(a.uoff, a.G.ng + 1, unit);
+    const u64 w = a.wfirst[g] + (unit - a.uoff[g]);
+    const u64 W0 = a.Y0 + w * MT_BLK, W1 = W0 + MT_BLK;  // [W0, W1)
+    {
+      const int4* src = (const int4*)(a.M16 + w * MT_BLK);
+      for (int i = tid; i < (int)(MT_BLK / 8); i += 256) smem_win[i] = src[i];
+    }
+    const i64 base = a.bk[w];
+    const bool wide = a.G.wide[g];
+    __syncthreads();
+    const u64 e1 = a.G.start[g + 1];
+    for (u64 e = a.G.start[g] + tid; e < e1; e += 256) {
+      const u64 xc = a.E.xcut[e];
+      u64 lw = a.E.lo_w[e];
+      const u64 sp = a.E.d_sp[e];
+      if (sp > lw) lw = sp;
+      if (lw > xc) continue;
+      const u64 vlo = a.E.vlo[e], vhi = a.E.vhi[e];
+      const double vd = a.E.vd[e];
+      const int vb = a.E.vbits[e];
+      const u64 dh = W0 ? div_clamp(vlo, vhi, vd, vb, W0, xc) : xc;
+      u64 dl = div_clamp(vlo, vhi, vd, vb, W1, xc) + 1;
+      if (dl < lw) dl = lw;
+      if (dh < dl) continue;
+      int s = 0;
+      auto f = [&](u64 y) { s += sw[(u32)(y - W0)]; };
+      if (wide) walk_quotients<true>(vlo, vhi, vd, vb, dh, dl, f);
+      else walk_quotients<false>(vlo, vhi, vd, vb, dh, dl, f);
+      const i64 tot = (i64)s + (i64)(dh - dl + 1) * base;
+      atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)tot);
+    }
+    __syncthreads();
+  }
+}
+
+// ---- sparse part (d < d_sp, y far above sqrt(v)): runs of consecutive d, L2 gathers
+#define SPARSE_RUN 32
+__global__ void k_sparse_plan(ElemDev E, u64 Y0, u64 R, uint64_t* __restrict__ runs,
+                              uint64_t* __restrict__ dtop, uint64_t* __restrict__ dbot) {
   u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (e > E.n) return;
-  if (e == E.n) { cnt[e] = 0; return; }
-  const u64 xc = E.xcut[e], lw = E.lo_w[e];
-  u64 c = 0, top = 0;
+  if (e == E.n) { runs[e] = 0; return; }
+  u64 xc = E.xcut[e];
+  const u64 sp = E.d_sp[e];
+  if (sp >= 1 && sp - 1 < xc) xc = sp - 1;
+  const u64 lw = E.lo_w[e];
+  u64 c = 0, top = 0, bot = 0;
   if (lw <= xc) {
     const u64 vlo = E.vlo[e], vhi = E.vhi[e];
     const double vd = E.vd[e];
     const int vb = E.vbits[e];
     const u64 dhi = Y0 ? div_clamp(vlo, vhi, vd, vb, Y0, xc) : xc;
-    u64 dlo = div_clamp(vlo, vhi, vd, vb, Y0 + R, xc) + 1;  // xc+1 means empty
+    u64 dlo = div_clamp(vlo, vhi, vd, vb, Y0 + R, xc) + 1;
     if (dlo < lw) dlo = lw;
-    if (dhi >= dlo) { c = dhi - dlo + 1; top = dhi; }
+    if (dhi >= dlo) { c = (dhi - dlo) / SPARSE_RUN + 1; top = dhi; bot = dlo; }
   }
-  cnt[e] = c;
+  runs[e] = c;
   dtop[e] = top;
+  dbot[e] = bot;
 }
 
-__global__ void k_mcut_capture(ElemDev E, u64 Y0, u64 R, const int* __restrict__ M,
-                               int32_t* __restrict__ Mmc) {
+struct SparseArgs {
+  ElemDev E;
+  uint64_t* acc;
+  const uint64_t* roff;
+  const uint64_t* dtop;
+  const uint64_t* dbot;
+  const int16_t* M16;
+  const int64_t* bk;
+  u64 Y0;
+  uint64_t* counter;
+};
+
+__global__ void __launch_bounds__(256) k_dsparse(SparseArgs a) {
+  const u64 total = a.roff[a.E.n];
+  for (;;) {
+    u64 base_unit = 0;
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) base_unit = atomicAdd((unsigned long long*)a.counter, 32ull);
+    base_unit = __shfl_sync(0xffffffffu, base_unit, 0);
+    if (base_unit >= total) break;
+    const u64 unit = base_unit + lane;
+    if (unit >= total) continue;
+    const u64 e = upper_idx(a.roff, a.E.n + 1, unit);
+    const u64 j = unit - a.roff[e];
+    const u64 dh = a.dtop[e] - j * SPARSE_RUN;
+    const u64 bot = a.dbot[e];
+    const u64 dl = dh >= bot + SPARSE_RUN - 1 ? dh - SPARSE_RUN + 1 : bot;
+    const u64 vlo = a.E.vlo[e], vhi = a.E.vhi[e];
+    const double vd = a.E.vd[e];
+    const int vb = a.E.vbits[e];
+    i64 s = 0;
+    for (u64 d = dh;; d--) {
+      const u64 y = qdiv_ok(vb, d) ? qdiv64(vd, __drcp_rn((double)d), vlo, d) : (u64)udiv128(vlo, vhi, d);
+      const u64 o = y - a.Y0;
+      s += (i64)a.M16[o] + a.bk[o / MT_BLK];
+      if (d == dl) break;
+    }
+    atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)s);
+  }
+}
+
+// ---- Q-gather: dense items with k*d <= J straight from the quotient table
+struct QArgs {
+  ElemDev E;
+  uint64_t* acc;
+  const uint64_t* off;   // [n+1]
+  uint64_t n;
+  uint64_t* counter;
+  const TargetDev* tgts;
+};
+
+__global__ void __launch_bounds__(256) k_qitems(QArgs a) {
+  const int lane = threadIdx.x & 31;
+  const u64 total = a.off[a.n];
+  for (;;) {
+    u64 w = 0;
+    if (lane == 0) w = atomicAdd((unsigned long long*)a.counter, 1ull);
+    w = __shfl_sync(0xffffffffu, w, 0);
+    const u64 base = w * (32ull * IPT);
+    if (base >= total) break;
+    u64 i = base + lane;
+    if (i >= total) continue;
+    u64 e = upper_idx(a.off, a.n + 1, i);
+    u64 e_lo = a.off[e], e_hi = a.off[e + 1];
+    u64 top = a.E.dq_hi[e];
+    u64 kk = a.E.k[e];
+    TargetDev t = a.tgts[a.E.tgt[e]];
+    i64 sum = 0;
+    for (int s = 0; s < IPT; s++, i += 32) {
+      if (i >= total) break;
+      if (i >= e_hi) {
+        if (sum) atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)sum);
+        sum = 0;
+        e = upper_idx(a.off, a.n + 1, i);
+        e_lo = a.off[e]; e_hi = a.off[e + 1];
+        top = a.E.dq_hi[e];
+        kk = a.E.k[e];
+        t = a.tgts[a.E.tgt[e]];
+      }
+      const u64 d = top - (i - e_lo);
+      sum += t.Q[kk * d - t.jq0];
+    }
+    if (sum) atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)sum);
+  }
+}
+
+__global__ void k_mcut_capture(ElemDev E, u64 Y0, u64 R, const int16_t* __restrict__ M16,
+                               const int64_t* __restrict__ bk, int32_t* __restrict__ Mmc) {
   u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E.n) return;
   u64 mc = E.mcut[e];
-  if (mc >= Y0 && mc < Y0 + R) Mmc[e] = M[mc - Y0];
+  if (mc >= Y0 && mc < Y0 + R) Mmc[e] = (int32_t)(M16[mc - Y0] + bk[(mc - Y0) / MT_BLK]);
 }
 
 __global__ void k_acc_finish(ElemDev E, uint64_t* __restrict__ acc, const int32_t* __restrict__ Mmc) {
@@ -347,8 +486,9 @@ static int scan_u64(UpdateCtx* c, const uint64_t* in, uint64_t* out, uint64_t n,
 
 int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* Mmc,
                      const uint64_t* tile_mcut_max, const uint8_t* tile_vbits_max, uint64_t ntiles,
-                     const TargetDev* tgts, int ntgt, cudaStream_t st) {
+                     const TargetDev* tgts, int ntgt, const GroupDev& grp, cudaStream_t st) {
   UpdateCtx* c = new UpdateCtx();
+  c->G = grp;
   c->E = E; c->acc = acc; c->Mmc = Mmc;
   c->tile_mcut_max = tile_mcut_max; c->tile_vbits_max = tile_vbits_max; c->ntiles = ntiles;
   c->ntgt = ntgt;
@@ -363,6 +503,10 @@ int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* 
   MT_CUDA_CHECK(cudaMalloc(&c->qcnt, sizeof(uint64_t) * (E.n + 1)));
   MT_CUDA_CHECK(cudaMalloc(&c->qoff, sizeof(uint64_t) * (E.n + 1)));
   MT_CUDA_CHECK(cudaMalloc(&c->counter, sizeof(uint64_t) * 4));
+  MT_CUDA_CHECK(cudaMalloc(&c->gunits, sizeof(uint64_t) * (grp.ng + 1)));
+  MT_CUDA_CHECK(cudaMalloc(&c->guoff, sizeof(uint64_t) * (grp.ng + 1)));
+  MT_CUDA_CHECK(cudaMalloc(&c->gwfirst, sizeof(uint64_t) * (grp.ng + 1)));
+  MT_CUDA_CHECK(cudaFuncSetAttribute(k_dwin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(MT_BLK * 2)));
   c->cub_tmp = nullptr; c->cub_bytes = 0;
   int dev; cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -373,14 +517,15 @@ void mt_update_destroy(UpdateCtx* c) {
   if (!c) return;
   cudaFree(c->tgts); cudaFree(c->units); cudaFree(c->cnt); cudaFree(c->dtop); cudaFree(c->off);
   cudaFree(c->qcnt); cudaFree(c->qoff); cudaFree(c->counter);
+  cudaFree(c->gunits); cudaFree(c->guoff); cudaFree(c->gwfirst);
   if (c->cub_tmp) cudaFree(c->cub_tmp);
   delete c;
 }
 
 uint64_t mt_update_launches(UpdateCtx* c) { return c->launches; }
 
-int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const int* M,
-                           cudaStream_t st) {
+int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const int16_t* M16,
+                           const int64_t* bk, cudaStream_t st) {
   const ElemDev& E = c->E;
   // counted walk
   {
@@ -390,24 +535,34 @@ int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const 
     c->launches++;
     int rc = scan_u64(c, units, off, c->ntiles + 1, st);
     if (rc) return rc;
-    MT_CUDA_CHECK(cudaMemsetAsync(c->counter, 0, sizeof(uint64_t), st));
+    MT_CUDA_CHECK(cudaMemsetAsync(c->counter, 0, sizeof(uint64_t) * 4, st));
     CountedArgs a{E, c->acc, c->tile_mcut_max, c->tile_vbits_max, off, c->ntiles, mu, Y0, c->counter};
     k_counted<<<c->nsm * 6, MT_CT, 0, st>>>(a);
     c->launches++;
     MT_CUDA_CHECK(cudaGetLastError());
   }
   // M(mcut) captures
-  k_mcut_capture<<<(unsigned)((E.n + 255) / 256), 256, 0, st>>>(E, Y0, R, M, c->Mmc);
+  k_mcut_capture<<<(unsigned)((E.n + 255) / 256), 256, 0, st>>>(E, Y0, R, M16, bk, c->Mmc);
   c->launches++;
-  // windowed dense walk
+  // windowed dense walk, shared-memory windows
+  if (c->G.ng) {
+    k_win_plan<<<(unsigned)((c->G.ng + 1 + 255) / 256), 256, 0, st>>>(c->G, Y0, R, c->gunits, c->gwfirst);
+    c->launches++;
+    int rc = scan_u64(c, c->gunits, c->guoff, c->G.ng + 1, st);
+    if (rc) return rc;
+    WinArgs a{E, c->acc, c->G, c->guoff, c->gwfirst, M16, bk, Y0, c->counter + 1};
+    k_dwin<<<c->nsm * 3, 256, MT_BLK * 2, st>>>(a);
+    c->launches++;
+    MT_CUDA_CHECK(cudaGetLastError());
+  }
+  // windowed dense walk, sparse part
   {
-    k_dense_plan<<<(unsigned)((E.n + 1 + 255) / 256), 256, 0, st>>>(E, Y0, R, c->cnt, c->dtop);
+    k_sparse_plan<<<(unsigned)((E.n + 1 + 255) / 256), 256, 0, st>>>(E, Y0, R, c->cnt, c->dtop, c->qoff);
     c->launches++;
     int rc = scan_u64(c, c->cnt, c->off, E.n + 1, st);
     if (rc) return rc;
-    MT_CUDA_CHECK(cudaMemsetAsync(c->counter + 1, 0, sizeof(uint64_t), st));
-    ItemsArgs a{E, c->acc, c->off, c->dtop, E.n, c->counter + 1, M, Y0, nullptr};
-    k_items<0><<<c->nsm * 8, 256, 0, st>>>(a);
+    SparseArgs a{E, c->acc, c->off, c->dtop, c->qoff, M16, bk, Y0, c->counter + 2};
+    k_dsparse<<<c->nsm * 8, 256, 0, st>>>(a);
     c->launches++;
     MT_CUDA_CHECK(cudaGetLastError());
   }
@@ -420,9 +575,9 @@ int mt_update_qgather(UpdateCtx* c, cudaStream_t st) {
   c->launches++;
   int rc = scan_u64(c, c->qcnt, c->qoff, E.n + 1, st);
   if (rc) return rc;
-  MT_CUDA_CHECK(cudaMemsetAsync(c->counter + 2, 0, sizeof(uint64_t), st));
-  ItemsArgs a{E, c->acc, c->qoff, E.dq_hi, E.n, c->counter + 2, nullptr, 0, c->tgts};
-  k_items<1><<<c->nsm * 8, 256, 0, st>>>(a);
+  MT_CUDA_CHECK(cudaMemsetAsync(c->counter + 3, 0, sizeof(uint64_t), st));
+  QArgs a{E, c->acc, c->qoff, E.n, c->counter + 3, c->tgts};
+  k_qitems<<<c->nsm * 8, 256, 0, st>>>(a);
   c->launches++;
   MT_CUDA_CHECK(cudaGetLastError());
   return MT_OK;
