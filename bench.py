@@ -1,0 +1,423 @@
+"""Benchmark: exact M(n) (default n = 10^19, BASELINE.json's metric) on N B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n 1e19] [--impl ours|reference]
+
+One step = one complete exact job: segmented Moebius sieve of y in [1, u],
+the harmonic-array update of all K = n // u elements, the quotient-table
+gather and the final resolve, giving M(n) and every M(floor(n/c)), c <= K.
+`value` is y-values/s = u / device time of the job (plan resident in HBM,
+CUDA events on the engine's stream, max over ranks).  `e2e` is the same
+metric through the public API `mertens_exact(n)` (host in, host out: M(n),
+the K finals and the 4M captured quotients copied back every step).
+
+--impl reference times the reference algorithm on the host cores instead
+(oracle/_ref's compiled kernels where they apply, else the oracle's C port),
+on a bounded sample of the same job, extrapolated to the whole job.
+Under torchrun (N > 1) rank 0 alone runs the reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+BASE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASE["metric"]
+PAPER = {10**16: -3195437, 10**17: -21830254, 10**18: -46758740, 10**19: 899990187,
+         10**20: 461113106, 10**21: 3395895277, 10**22: -2061910120,
+         11609864264058592345: -1995900927}
+
+
+def parse_n(s: str) -> int:
+    if "e" in s.lower():
+        m, e = s.lower().split("e")
+        return int(m) * 10 ** int(e)
+    return int(s)
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        return {}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.p is None:
+            return
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                self.rows.append(f)
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+# ---------------------------------------------------------------- CPU reference arm
+def _closed_form_items(n: int, u: int):
+    """counted / dense pair totals of the reference's block loop (engine.py:134-159)."""
+    from oracle import engine_port as E
+
+    if n < 2**64:
+        H = E.HarmonicArray(n, u)
+        counted = int(H.mcut.sum(dtype=np.uint64))
+        dense = int(np.where(H.xcut >= H.lo, H.xcut - H.lo + np.uint64(1), 0).sum(dtype=np.uint64))
+        return counted, dense, H
+    ps = E.big_params(n, u)
+    return sum(p[3] for p in ps), sum(max(0, p[2] - p[4] + 1) for p in ps), None
+
+
+def cpu_reference_sample(n: int, u: int, threads: int, budget_s: float = 12.0):
+    """Time the reference algorithm on a bounded sample of the job on `threads`
+    host cores and extrapolate to the whole job.
+
+    apply : the reference's apply_block on the first y-block [1, 2^20] for every
+            S-th element (oracle/_ref's compiled kernel when n <= 4e18, where it
+            is defined; above that the oracle's C port with mod-2^64 wrap, since
+            the reference's i128 guard rejects those n), element chunks on
+            `threads` threads -> pair rate.
+    sieve : the reference's sieve_logprime on 2^26 y-values at y = u/2 split
+            over `threads` threads (sieve.py:168-174) -> y rate.
+    job   ~= (counted + dense pairs) / pair rate + u / y rate."""
+    from oracle import engine_port as E
+
+    kern_c = E.get_kernels("c")
+    try:
+        kern_ref = E.get_kernels("ref")
+    except Exception:
+        kern_ref = None
+    counted, dense, H = _closed_form_items(n, u)
+    # ---- apply sample
+    L = 1 << 22
+    K = n // u
+    stride = max(1, K // 1024)
+    ks = np.arange(0, K, stride)
+    if H is None:
+        raise RuntimeError("CPU sample for n >= 2^64 not supported")
+    sub = {f: np.ascontiguousarray(getattr(H, f)[ks]) for f in ("v", "lo", "xcut", "mcut", "dnext", "ynext", "D")}
+    primes = E.generate_primes(E.ceil_sqrt(u) + 1)
+    logs, wheel = E.build_logs(primes), E.build_wheel()
+    mu = E.mu_range(kern_c, 1, L, primes, logs, wheel)
+    mp = np.cumsum(mu, dtype=np.int64)
+    use_ref_apply = kern_ref is not None and n <= 4 * 10**18
+    chunks = np.array_split(np.arange(len(ks)), threads)
+
+    def run_chunk(ix):
+        acc = np.zeros(len(ix), np.int64 if use_ref_apply else np.uint64)
+        a = {f: np.ascontiguousarray(sub[f][ix]) for f in sub}
+        if use_ref_apply:
+            c, d = kern_ref.apply_block(acc, a["v"], a["lo"], a["xcut"], a["mcut"], a["dnext"], a["ynext"],
+                                        1, L, mp, None)
+        else:
+            c, d = kern_c.apply_block_wrap(acc, a["v"], a["lo"], a["xcut"], a["mcut"], a["dnext"], a["ynext"],
+                                           1, L, mp)
+        return int(c) + int(d)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        pairs = sum(ex.map(run_chunk, chunks))
+    t_apply = time.perf_counter() - t0
+    pair_rate = pairs / t_apply
+    # ---- sieve sample
+    SL = 1 << 28
+    y0 = max(2, u // 2)
+    sk = kern_ref if kern_ref is not None else kern_c
+    rngs = E.split_ranges(y0, y0 + SL - 1, threads)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda r: sk.sieve_logprime(r[0], r[1], primes, logs, wheel), rngs))
+    t_sieve = time.perf_counter() - t0
+    y_rate = SL / t_sieve
+    est = (counted + dense) / pair_rate + u / y_rate
+    kind = "reference" if (use_ref_apply and kern_ref is not None) else "port"
+    sample = (f"apply_block on y in [1,2^22] for every {stride}-th of K={K} elements ({pairs:.3g} pairs, "
+              f"{'oracle/_ref compiled kernel' if use_ref_apply else 'oracle C port, mod-2^64 (reference kernel rejects n>4e18)'})"
+              f" + sieve_logprime of 2^28 y at y={y0} ({'oracle/_ref' if kern_ref is not None else 'oracle C port'}), "
+              f"{threads} threads; job extrapolated as {counted + dense:.4g} pairs / {pair_rate:.4g} pairs/s + "
+              f"u / {y_rate:.4g} y/s = {est:.4g} s")
+    return {"value": u / est, "unit": "y-values/s", "cores": threads, "kind": kind, "sample": sample,
+            "est_job_s": est, "pair_rate": pair_rate, "y_rate": y_rate, "sample_s": t_apply + t_sieve}
+
+
+def reference_arm(args, n, u, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_sample(n, u, threads)
+    vals = [cpu_reference_sample(n, u, threads) for _ in range(args.steps)]
+    v = statistics.median(r["value"] for r in vals)
+    last = vals[-1]
+    line = {
+        "metric": METRIC, "value": v, "unit": "y-values/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * u / v, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64", "data": f"synthetic: n={n} (deterministic, no dataset)",
+        "config": config_block(n, u, world), "impl": "reference",
+        "cpu_baseline": {k: last[k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "y-values/s"},
+        "e2e": {"value": v, "unit": "y-values/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(n, u, world):
+    return {"workload": f"M({n}) plus all M(floor(n/c)) for c <= K (exact, 1 target)", "n": str(n), "u": u,
+            "K": n // u, "parallelism": f"y-shard x{world} (head redundant, tail y-segments split, 1 int64 allreduce)",
+            "l2": "inputs larger than L2: the job streams u sieve cells and a multi-GB quotient table per step"}
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", default="1e19")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps")
+    args = ap.parse_args()
+    n = parse_n(args.n)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    import paper_1108_0135_b200 as P
+
+    u = P.choose_u(n)
+    if args.impl == "reference":
+        return reference_arm(args, n, u, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1108_0135_b200 import _lib, distributed, engine
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    cfg = P.EngineConfig(device=local, engine_flags=_lib.MT_FLAG_TIMING, stream=stream.cuda_stream)
+    job = engine.make_job([n], u, cfg, rank=rank, world=world)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-timed job: plan resident in HBM, phases + collectives per step
+    plan = distributed.DevicePlan(job) if world > 1 else None
+    if plan is None:
+        plan = _SinglePlan(job)
+    res = _lib.MtResult()
+    fin = np.zeros(n // u, np.int64)
+    res.finals = fin.ctypes.data_as(_lib._pi64)  # M(n) is read back once per step
+    for _ in range(args.warmup):
+        _one(plan, world, res)
+    barrier()
+    times, launches, kms, kcnt = [], 0, {}, {}
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _one(plan, world, res)
+            e1.record(stream)
+            barrier()
+            times.append(e0.elapsed_time(e1))
+            st = _lib.stats_dict(res.stats)
+            launches += int(st["kernel_launches"])
+            for k, v in st["kernel_ms"].items():
+                kms[k] = kms.get(k, 0.0) + v
+                kcnt[k] = kcnt.get(k, 0) + st["kernel_count"][k]
+    value_m = int(fin[0])
+    stats_last = _lib.stats_dict(res.stats)
+    plan.close()
+    ms = max(times)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        ms_all = ms
+    clocks = clk.summary()
+
+    # ---- end to end through the public API (host in, host out)
+    e2e_steps = args.e2e_steps or args.steps
+    e2e_cfg = P.EngineConfig(device=local)
+    r = P.mertens_exact(n, e2e_cfg)  # warm
+    wall = []
+    for _ in range(e2e_steps):
+        barrier()
+        t0 = time.perf_counter()
+        r = P.mertens_exact(n, e2e_cfg)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        wall.append(time.perf_counter() - t0)
+    e2e_s = max(wall)
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    K = n // u
+    d2h = 8 * K + 8 * len(r._cp_m)
+    h2d = 16
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    # ---- roofline of the dominant kernel (largest summed event time)
+    pk = peaks()
+    dom = max(kms, key=lambda k: kms[k])
+    avg_ms = kms[dom] / max(1, kcnt[dom])
+    roof = {"kernel": dom}
+    seg_tail = 1 << 27
+    if dom in ("sieve_tile", "sieve_large"):
+        # 10 algorithmic bytes per y-value (state write+read 2 B, M(y) 8 B)
+        ys_per_launch = (stats_last["n_tail_segments"] * seg_tail + stats_last["n_head_segments"] * (1 << 24)) \
+            / max(1, kcnt[dom] / args.steps)
+        A = 10 * ys_per_launch / (avg_ms * 1e-3) / 1e9
+        P_ = pk.get("hbm_gbs", 6650.0)
+        roof |= {"bound": "hbm", "achieved": A, "peak": P_, "unit": "GB/s", "frac": A / P_,
+                 "traffic": _ncu_traffic(dom), "per_unit": "10 B per y-value (SURVEY.md §8(d))",
+                 "units_per_launch": ys_per_launch, "avg_launch_ms": avg_ms,
+                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"}
+    else:
+        ops = 7 * stats_last["counted_items"] + 4 * stats_last["dense_items"]
+        A = ops / (kms[dom] / args.steps * 1e-3) / 1e12
+        roof |= {"bound": "int", "achieved": A, "peak": 18.56, "unit": "Tops/s", "frac": A / 18.56,
+                 "traffic": None}
+    # the update kernel against the INT-pipe roofline (7 IMAD/counted pair)
+    upd_ms = kms.get("counted", 0.0) / args.steps
+    upd = None
+    if upd_ms > 0:
+        A = 7 * stats_last["counted_items"] / (upd_ms * 1e-3) / 1e12
+        upd = {"kernel": "counted", "bound": "int", "achieved": A, "peak": 18.56, "unit": "T IMAD-op/s",
+               "frac": A / 18.56, "per_unit": "7 IMAD-pipe ops per counted pair (SURVEY.md §8(d))",
+               "peak_source": "profiles/r01_microbench.txt (32-bit IMAD chains, 148 SMs @ 1965 MHz)"}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(n, u, os.cpu_count() or 1)
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "y-values/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {ex!r}"}
+    line = {
+        "metric": METRIC, "value": u / (ms * 1e-3), "unit": "y-values/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": f"synthetic: n={n} (deterministic, no dataset)", "config": config_block(n, u, world),
+        "result": {"M": value_m, "paper": PAPER.get(n), "match": PAPER.get(n) in (None, value_m),
+                   "e2e_M": r.value},
+        "roofline": roof, "roofline_update": upd,
+        "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": u / e2e_s, "unit": "y-values/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "wall_s": e2e_s},
+        "gpu_launches": launches // args.steps,
+        "clocks": clocks,
+        "phases_ms": {k: stats_last[k] for k in ("ms_update_head", "ms_sieve_tail", "ms_qgather", "ms_finalize",
+                                                  "ms_setup")},
+        "kernel_ms_per_step": {k: v / args.steps for k, v in kms.items() if v},
+        "work": {"counted_items": stats_last["counted_items"], "dense_items": stats_last["dense_items"],
+                 "head_end": stats_last["head_end"], "q_entries": stats_last["q_entries"]},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+class _SinglePlan:
+    """The plan phases at world size 1 (no collectives)."""
+
+    def __init__(self, job):
+        import ctypes
+
+        from paper_1108_0135_b200 import _lib
+
+        self.L = _lib.require_device()
+        self.h = ctypes.c_void_p()
+        _lib.check(self.L.mt_plan_create(ctypes.byref(job), ctypes.byref(self.h)))
+
+    def run(self, res):
+        import ctypes
+
+        from paper_1108_0135_b200 import _lib
+
+        mh, tt = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(self.L.mt_plan_sieve_update(self.h, ctypes.byref(mh), ctypes.byref(tt)))
+        _lib.check(self.L.mt_plan_tail_offset(self.h, mh.value))
+        _lib.check(self.L.mt_plan_gather(self.h))
+        _lib.check(self.L.mt_plan_resolve(self.h, ctypes.byref(res)))
+
+    def close(self):
+        if self.h:
+            self.L.mt_plan_destroy(self.h)
+            self.h = None
+
+
+def _one(plan, world, res):
+    if world > 1:
+        from paper_1108_0135_b200 import distributed
+
+        distributed.run_phases(plan, None, res)
+    else:
+        plan.run(res)
+
+
+if __name__ == "__main__":
+    main()

@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define MT_ABI_VERSION 1
+#define MT_ABI_VERSION 2
 
 /* return codes */
 #define MT_OK 0
@@ -33,6 +33,11 @@ extern "C" {
 #define MT_ERR_CUDA 3     /* -> RuntimeError (device / driver failure) */
 #define MT_ERR_VALUE 4    /* -> ValueError   */
 #define MT_ERR_OVERFLOW 5 /* -> OverflowError (_native.pyx:308-309) */
+
+/* mt_job.flags */
+#define MT_FLAG_FORCE_WIDE 1u    /* tests: 64-bit remainders / 64-bit quotient walks everywhere */
+#define MT_FLAG_FORCE_SLOWDIV 2u /* tests: exact 128/64 division in the counted walk            */
+#define MT_FLAG_TIMING 4u        /* per-kernel-class CUDA-event timing into mt_stats.kernel_ms  */
 
 /* last error message of the calling thread ("" if none) */
 const char* mt_last_error(void);
@@ -100,8 +105,12 @@ typedef struct {
   uint32_t seg_log2_head;  /* head segment length 2^x (default 25)                 */
   uint32_t seg_log2_tail;  /* tail segment length 2^x (default 27)                 */
   int32_t device;          /* CUDA device ordinal (-1: current)                    */
-  /* y-range sharding for multi-GPU (rank r of w owns tail y-blocks); w<=1: all */
+  /* multi-GPU sharding: rank r of w sieves the head redundantly,
+   * takes every w-th work unit of the head update and of the Q-gather, and
+   * sieves the r-th contiguous share of the tail y-segments.  w <= 1: all. */
   uint32_t shard_rank, shard_world;
+  uint32_t flags;          /* MT_FLAG_*                                          */
+  void* stream;            /* cudaStream_t to run on (null: the engine's own)    */
 } mt_job;
 
 typedef struct {
@@ -113,7 +122,15 @@ typedef struct {
   uint64_t max_mcut;
   uint64_t windowed_items, qgather_items, q_entries;
   double ms_total, ms_sieve_head, ms_update_head, ms_sieve_tail, ms_qgather, ms_finalize;
-  double ms_counted_kernel, ms_dense_kernel;  /* event-timed (when enabled) */
+  double ms_counted_kernel, ms_dense_kernel;  /* event-timed (MT_FLAG_TIMING) */
+  /* multi-GPU algebra: M(head_end - 1) and this rank's local tail total */
+  int64_t m_head, tail_total;
+  /* per kernel class (sieve_tile, sieve_large, counted, dwin, dsparse, qgather,
+   * other): summed CUDA-event ms and launch counts (MT_FLAG_TIMING) */
+  double kernel_ms[8];
+  uint64_t kernel_count[8];
+  uint64_t tail_seg_begin, tail_seg_end; /* this rank's tail segments     */
+  double ms_setup;                        /* mt_plan_create wall time      */
 } mt_stats;
 
 typedef struct {
@@ -125,8 +142,29 @@ typedef struct {
   mt_stats stats;
 } mt_result;
 
-/* one exact job: sieve 1..u, update every element, resolve */
+/* one exact job: sieve 1..u, update every element, resolve (shard_world <= 1) */
 int mt_run(const mt_job* job, mt_result* out);
+
+/* ---- 3. plan API: the same job split at its two exchange points ---------------
+ * mt_run == create, sieve_update, tail_offset(m_head), gather, resolve, destroy.
+ * With shard_world = w > 1 every rank runs the phases and the caller performs
+ * the collectives between them (paper_1108_0135_b200/distributed.py):
+ *   after sieve_update : allgather tail_total -> offset_r = m_head + sum_{h<r} T_h
+ *   after tail_offset  : for every target t and rank h, broadcast the Q slice
+ *                        mt_plan_q_slice(t, h) from rank h (device int32)
+ *   after gather       : allreduce(sum, int64 two's complement) of mt_plan_acc
+ * A plan is re-executable (sieve_update re-initialises the accumulators), and
+ * all device memory of the job lives in the plan. */
+typedef struct mt_plan mt_plan;
+int mt_plan_create(const mt_job* job, mt_plan** out);
+int mt_plan_sieve_update(mt_plan* p, int64_t* m_head, int64_t* tail_total);
+int mt_plan_tail_offset(mt_plan* p, int64_t offset);
+int mt_plan_q_slice(mt_plan* p, uint32_t target, uint32_t rank, void** dptr, uint64_t* count);
+int mt_plan_acc(mt_plan* p, void** dptr, uint64_t* count);
+int mt_plan_gather(mt_plan* p);
+/* finalize every target; copies into the non-null host pointers of out */
+int mt_plan_resolve(mt_plan* p, mt_result* out);
+void mt_plan_destroy(mt_plan* p);
 
 #ifdef __cplusplus
 }

@@ -40,7 +40,13 @@ class MtJob(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("shard_rank", ctypes.c_uint32),
         ("shard_world", ctypes.c_uint32),
+        ("flags", ctypes.c_uint32),
+        ("stream", ctypes.c_void_p),
     ]
+
+
+MT_FLAG_FORCE_WIDE, MT_FLAG_FORCE_SLOWDIV, MT_FLAG_TIMING = 1, 2, 4
+KERNEL_CLASSES = ("sieve_tile", "sieve_large", "counted", "dwin", "dsparse", "qgather", "other", "unused")
 
 
 class MtStats(ctypes.Structure):
@@ -50,7 +56,10 @@ class MtStats(ctypes.Structure):
         "max_mcut", "windowed_items", "qgather_items", "q_entries")] + [
         (f, ctypes.c_double) for f in (
             "ms_total", "ms_sieve_head", "ms_update_head", "ms_sieve_tail", "ms_qgather",
-            "ms_finalize", "ms_counted_kernel", "ms_dense_kernel")]
+            "ms_finalize", "ms_counted_kernel", "ms_dense_kernel")] + [
+        ("m_head", ctypes.c_int64), ("tail_total", ctypes.c_int64),
+        ("kernel_ms", ctypes.c_double * 8), ("kernel_count", _u64 * 8),
+        ("tail_seg_begin", _u64), ("tail_seg_end", _u64), ("ms_setup", ctypes.c_double)]
 
 
 class MtResult(ctypes.Structure):
@@ -90,11 +99,22 @@ def lib():
         "mt_mertens_range": [_u64, _u64, vp],
         "mt_mertens_at": [vp, _u64, vp],
         "mt_run": [ctypes.POINTER(MtJob), ctypes.POINTER(MtResult)],
+        "mt_plan_create": [ctypes.POINTER(MtJob), ctypes.POINTER(ctypes.c_void_p)],
+        "mt_plan_sieve_update": [vp, _pi64, _pi64],
+        "mt_plan_tail_offset": [vp, ctypes.c_int64],
+        "mt_plan_q_slice": [vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(ctypes.c_void_p), _pu64],
+        "mt_plan_acc": [vp, ctypes.POINTER(ctypes.c_void_p), _pu64],
+        "mt_plan_gather": [vp],
+        "mt_plan_resolve": [vp, ctypes.POINTER(MtResult)],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
         f.argtypes = args
         f.restype = ctypes.c_int
+    L.mt_plan_destroy.argtypes = [vp]
+    L.mt_plan_destroy.restype = None
+    if L.mt_abi_version() != 2:
+        raise ImportError(f"{LIB_PATH}: ABI version {L.mt_abi_version()} != 2 (rebuild)")
     _lib = L
     return L
 
@@ -130,4 +150,18 @@ EXPORTED_SYMBOLS = (
     "mt_last_error", "mt_abi_version", "mt_device_count", "mt_set_device",
     "mt_sieve_logprime", "mt_logprime_states", "mt_sieve_naive", "mt_apply_block",
     "mt_finalize", "mt_build_divisor_arrays", "mt_mertens_range", "mt_mertens_at", "mt_run",
+    "mt_plan_create", "mt_plan_sieve_update", "mt_plan_tail_offset", "mt_plan_q_slice", "mt_plan_acc",
+    "mt_plan_gather", "mt_plan_resolve", "mt_plan_destroy",
 )
+
+
+def stats_dict(st) -> dict:
+    """Flatten an MtStats into plain Python values (per-class kernel timings keyed by name)."""
+    out = {}
+    for f, _ in MtStats._fields_:
+        v = getattr(st, f)
+        if f in ("kernel_ms", "kernel_count"):
+            out[f] = {KERNEL_CLASSES[i]: v[i] for i in range(7)}
+        else:
+            out[f] = v
+    return out

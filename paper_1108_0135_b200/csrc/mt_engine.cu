@@ -69,6 +69,10 @@ static u64 ceil_sqrt_u128(u128 x) {
 // ------------------------------------------------------------ device buffers
 struct DevBuf {
   void* p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
   ~DevBuf() { if (p) cudaFree(p); }
   template <class T> T* as() { return (T*)p; }
 };
@@ -530,206 +534,78 @@ __global__ void k_copy_caps(const int* __restrict__ Q, u64 jq0, u64 c_lo, u64 cn
   out[i] = Q[c_lo + i - jq0];
 }
 
+
+// Q[j] += off for j in [j0, j1] (one target's slice owned by this rank's tail)
+__global__ void k_q_offset(int* __restrict__ Q, u64 cnt, int off) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) Q[i] += off;
+}
+
 static double ms_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
-extern "C" int mt_run(const mt_job* job, mt_result* out) {
-  auto T0 = std::chrono::steady_clock::now();
-  g_err[0] = 0;
-  if (!job || !out || job->n_targets == 0) { mt_set_error("empty job"); return MT_ERR_VALUE; }
-  if (job->device >= 0) MT_CUDA_CHECK(cudaSetDevice(job->device));
-  const int N = (int)job->n_targets;
-  const u64 u = job->u;
-  std::vector<u128> n(N);
-  std::vector<u64> K(N), e0(N + 1);
-  e0[0] = 0;
-  for (int i = 0; i < N; i++) {
-    n[i] = ((u128)job->n_hi[i] << 64) | job->n_lo[i];
-    if (n[i] < 4) { mt_set_error("exact job requires n >= 4"); return MT_ERR_VALUE; }
-    if (job->n_hi[i] >= (1ull << 11)) { mt_set_error("n >= 2^75 is outside the engine's range"); return MT_ERR_RESOURCE; }
-    if ((u128)u <= ceil_sqrt_u128(n[i])) { mt_set_error("u must exceed ceil(sqrt(n))"); return MT_ERR_VALUE; }
-    K[i] = (u64)(n[i] / u);
-    e0[i + 1] = e0[i] + K[i];
-  }
-  const u64 NE = e0[N];
-  cudaStream_t st;
-  MT_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{st};
+// ============================================================================
+// the plan: one exact job (N targets sharing one sieve), split at its
+// exchange points so that a multi-GPU caller can run the collectives
+// ============================================================================
+struct mt_plan {
+  int device = -1;
+  int N = 0;
+  u64 u = 0;
+  uint32_t rank = 0, world = 1, flags = 0;
+  std::vector<u128> n;
+  std::vector<u64> n_lo, n_hi, K, e0;
+  u64 NE = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
   u64 launches = 0;
-
-  // ---- elements
-  DevBuf d_nlo, d_nhi, d_e0, d_vd, d_vlo, d_vhi, d_vb, d_k, d_tgt, d_D, d_x, d_mc, d_lo, d_low, d_dq, d_acc, d_mmc, d_dsp;
-  RC(dalloc(d_nlo, N * 8)); RC(dalloc(d_nhi, N * 8)); RC(dalloc(d_e0, (N + 1) * 8));
-  RC(dalloc(d_vd, NE * 8)); RC(dalloc(d_vlo, NE * 8)); RC(dalloc(d_vhi, NE * 8)); RC(dalloc(d_vb, NE));
-  RC(dalloc(d_k, NE * 8)); RC(dalloc(d_tgt, NE * 4)); RC(dalloc(d_D, NE * 8)); RC(dalloc(d_x, NE * 8));
-  RC(dalloc(d_mc, NE * 8)); RC(dalloc(d_lo, NE * 8)); RC(dalloc(d_low, NE * 8)); RC(dalloc(d_dq, NE * 8));
-  RC(dalloc(d_acc, NE * 8)); RC(dalloc(d_mmc, NE * 4)); RC(dalloc(d_dsp, NE * 8));
-  MT_CUDA_CHECK(cudaMemcpyAsync(d_nlo.p, job->n_lo, N * 8, cudaMemcpyHostToDevice, st));
-  MT_CUDA_CHECK(cudaMemcpyAsync(d_nhi.p, job->n_hi, N * 8, cudaMemcpyHostToDevice, st));
-  MT_CUDA_CHECK(cudaMemcpyAsync(d_e0.p, e0.data(), (N + 1) * 8, cudaMemcpyHostToDevice, st));
-  MT_CUDA_CHECK(cudaMemsetAsync(d_acc.p, 0, NE * 8, st));
-  MT_CUDA_CHECK(cudaMemsetAsync(d_mmc.p, 0, NE * 4, st));
-  {
-    ElemInitArgs a{d_nlo.as<u64>(), d_nhi.as<u64>(), d_e0.as<u64>(), N, u, NE,
-                   d_vd.as<double>(), d_vlo.as<u64>(), d_vhi.as<u64>(), d_vb.as<uint8_t>(), d_k.as<u64>(),
-                   d_tgt.as<uint32_t>(), d_D.as<u64>(), d_x.as<u64>(), d_mc.as<u64>(), d_lo.as<u64>()};
-    if (NE) k_elem_init<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(a);
-    launches++;
-    MT_CUDA_CHECK(cudaGetLastError());
-  }
-  std::vector<unsigned long long> tstat(3 * N, 0);
-  {
-    DevBuf d_ts;
-    RC(dalloc(d_ts, 3 * N * 8));
-    MT_CUDA_CHECK(cudaMemsetAsync(d_ts.p, 0, 3 * N * 8, st));
-    if (NE) k_elem_stats<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, d_tgt.as<uint32_t>(), d_mc.as<u64>(), d_x.as<u64>(), d_lo.as<u64>(), d_ts.as<unsigned long long>());
-    launches++;
-    MT_CUDA_CHECK(cudaMemcpyAsync(tstat.data(), d_ts.p, 3 * N * 8, cudaMemcpyDeviceToHost, st));
-    MT_CUDA_CHECK(cudaStreamSynchronize(st));
-  }
-  u64 Ymc = 0, counted_items = 0, dense_items = 0;
-  for (int i = 0; i < N; i++) {
-    Ymc = std::max<u64>(Ymc, tstat[3 * i]);
-    counted_items += tstat[3 * i + 1];
-    dense_items += tstat[3 * i + 2];
-  }
-
-  // ---- quotient tables: Q_t[j] = M(floor(n_t/j)), j in [jq0_t, jq1_t]
-  const u64 q_budget = job->q_budget_bytes ? job->q_budget_bytes : (48ull << 30);
-  std::vector<u64> J(N), jq0(N), jq1(N);
-  u64 q_total = 0;
-  for (int i = 0; i < N; i++) {
-    jq0[i] = (u64)(n[i] / ((u128)u + 1)) + 1;
-    J[i] = (u64)(n[i] / ((u128)Ymc + 1));
-  }
-  // cap the tables to the budget by scaling J down uniformly
-  for (int it = 0; it < 64; it++) {
-    q_total = 0;
-    for (int i = 0; i < N; i++) {
-      u64 hi = J[i];
-      if (i == 0 && job->cap_c_hi >= job->cap_c_lo && job->cap_c_hi > hi) hi = job->cap_c_hi;
-      jq1[i] = hi;
-      if (hi >= jq0[i]) q_total += (hi - jq0[i] + 1);
-    }
-    if (q_total * 4 <= q_budget) break;
-    for (int i = 0; i < N; i++) J[i] = J[i] / 2;
-  }
-  u64 head_end = Ymc;
-  for (int i = 0; i < N; i++) {
-    if (J[i] < jq0[i]) J[i] = 0;  // no Q-gather for this target
-  }
-  std::vector<DevBuf> d_Q(N);
-  std::vector<TargetDev> tdev(N);
-  std::vector<CaptureTargetH> caps;
-  for (int i = 0; i < N; i++) {
-    u64 cnt = jq1[i] >= jq0[i] ? jq1[i] - jq0[i] + 1 : 0;
-    RC(dalloc(d_Q[i], cnt * 4));
-    tdev[i].Q = d_Q[i].as<int>();
-    tdev[i].jq0 = jq0[i];
-    if (cnt) {
-      CaptureTargetH c;
-      c.n_lo = job->n_lo[i]; c.n_hi = job->n_hi[i];
-      c.nd = job->n_hi[i] ? (double)job->n_hi[i] * 18446744073709551616.0 + (double)job->n_lo[i] : (double)job->n_lo[i];
-      c.nbits = 0;
-      for (u128 x = n[i]; x; x >>= 1) c.nbits++;
-      c.jq0 = jq0[i]; c.jq1 = jq1[i]; c.Q = tdev[i].Q;
-      caps.push_back(c);
-    }
-  }
-  DevBuf d_J;
-  RC(dalloc(d_J, N * 8));
-  MT_CUDA_CHECK(cudaMemcpyAsync(d_J.p, J.data(), N * 8, cudaMemcpyHostToDevice, st));
-  if (NE) k_elem_split<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, d_k.as<u64>(), d_tgt.as<uint32_t>(), d_J.as<u64>(), d_lo.as<u64>(), d_x.as<u64>(), d_low.as<u64>(), d_dq.as<u64>());
-  if (NE) k_elem_dsp<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, d_vd.as<double>(), d_dsp.as<u64>());
-  launches += 2;
-  // element groups for the window walk: consecutive k of one target, size clamp(k/8, 32, 1024)
+  u64 counted_items = 0, dense_items = 0, Ymc = 0;
+  // elements
+  DevBuf d_nlo, d_nhi, d_e0, d_vd, d_vlo, d_vhi, d_vb, d_k, d_tgt, d_D, d_x, d_mc, d_lo, d_low, d_dq,
+      d_acc, d_mmc, d_dsp, d_J, d_gs, d_gylo, d_gyhi, d_gw, d_tmax, d_tbits, d_fin;
   std::vector<u64> gstart;
-  for (int i = 0; i < N; i++) {
-    u64 k0 = 1;
-    while (k0 <= K[i]) {
-      gstart.push_back(e0[i] + k0 - 1);
-      u64 g = std::min<u64>(1024, std::max<u64>(32, k0 / 8));
-      k0 += g;
-    }
-  }
-  const u64 ng = gstart.size();
-  gstart.push_back(NE);
-  DevBuf d_gs, d_gylo, d_gyhi, d_gw;
-  RC(dalloc(d_gs, (ng + 1) * 8)); RC(dalloc(d_gylo, ng * 8)); RC(dalloc(d_gyhi, ng * 8)); RC(dalloc(d_gw, ng));
-  MT_CUDA_CHECK(cudaMemcpyAsync(d_gs.p, gstart.data(), (ng + 1) * 8, cudaMemcpyHostToDevice, st));
-  if (ng) k_group_meta<<<(unsigned)ng, 256, 0, st>>>(d_gs.as<u64>(), ng, d_vlo.as<u64>(), d_vhi.as<u64>(), d_x.as<u64>(), d_low.as<u64>(), d_dsp.as<u64>(), d_gylo.as<u64>(), d_gyhi.as<u64>(), d_gw.as<uint8_t>());
-  launches++;
-  GroupDev grp{d_gs.as<u64>(), d_gylo.as<u64>(), d_gyhi.as<u64>(), d_gw.as<uint8_t>(), ng};
-  {
-    DevBuf d_we;
-    RC(dalloc(d_we, 8));
-    MT_CUDA_CHECK(cudaMemsetAsync(d_we.p, 0, 8, st));
-    if (NE) k_window_extent<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, d_vlo.as<u64>(), d_vhi.as<u64>(), d_low.as<u64>(), d_x.as<u64>(), d_we.as<unsigned long long>());
-    launches++;
-    unsigned long long we = 0;
-    MT_CUDA_CHECK(cudaMemcpyAsync(&we, d_we.p, 8, cudaMemcpyDeviceToHost, st));
-    MT_CUDA_CHECK(cudaStreamSynchronize(st));
-    head_end = std::max<u64>(head_end, we);
-  }
-  if (job->cap_small > head_end) head_end = job->cap_small;
-  if (head_end > u) head_end = u;
-
-  // tiles metadata for the counted walk
-  const u64 ntiles = (NE + MT_CT - 1) / MT_CT;
-  DevBuf d_tmax, d_tbits;
-  RC(dalloc(d_tmax, ntiles * 8)); RC(dalloc(d_tbits, ntiles));
-  if (ntiles) k_tile_meta<<<(unsigned)ntiles, MT_CT, 0, st>>>(NE, d_mc.as<u64>(), d_vb.as<uint8_t>(), d_tmax.as<u64>(), d_tbits.as<uint8_t>());
-  launches++;
-
-  // ---- segments
-  const u64 Rh = 1ull << (job->seg_log2_head ? job->seg_log2_head : 24);
-  const u64 Rt = 1ull << (job->seg_log2_tail ? job->seg_log2_tail : 27);
-  if (Rh < MT_TILE || Rt < Rh || (Rt % Rh)) { mt_set_error("bad segment sizes"); return MT_ERR_VALUE; }
-  const u64 head_segs = (head_end + 1 + Rh - 1) / Rh;
-  const u64 head_lim = head_segs * Rh;  // first y of the tail
-  u64 tail_segs = 0;
-  if (u + 1 > head_lim) tail_segs = (u + 1 - head_lim + Rt - 1) / Rt;
-  const u64 y_last = head_lim + tail_segs * Rt - 1;
-
+  u64 ng = 0, ntiles = 0;
+  // quotient tables
+  std::vector<u64> J, jq0, jq1;
+  std::vector<DevBuf> d_Q;
+  std::vector<TargetDev> tdev;
+  std::vector<CaptureTargetH> caps;
+  // segments
+  u64 Rh = 0, Rt = 0, head_end = 0, head_segs = 0, head_lim = 0, tail_segs = 0, y_last = 0;
+  u64 tseg0 = 0, tseg1 = 0;  // this rank's tail segments [tseg0, tseg1)
   PrimeTable pt;
-  build_primes(std::max<u64>(ceil_sqrt_u128(y_last) + 1, 2), pt);
-  uint8_t wheel[MT_WHEEL];
-  reference_wheel(wheel);
-  std::vector<uint32_t> w32;
-  build_wheel_words(wheel, w32);
-  const u64 np = pt.p.size();
   DevBuf d_p, d_rp, d_lg, d_w32, d_big, d_mu, d_m, d_half, d_bk, d_tsum, d_tbase, d_run, d_caps, d_small;
-  RC(dalloc(d_p, np * 4)); RC(dalloc(d_rp, np * 8)); RC(dalloc(d_lg, np));
-  RC(dalloc(d_w32, w32.size() * 4));
-  MT_CUDA_CHECK(cudaMemcpyAsync(d_p.p, pt.p.data(), np * 4, cudaMemcpyHostToDevice, st));
-  MT_CUDA_CHECK(cudaMemcpyAsync(d_rp.p, pt.r.data(), np * 8, cudaMemcpyHostToDevice, st));
-  MT_CUDA_CHECK(cudaMemcpyAsync(d_lg.p, pt.lg.data(), np, cudaMemcpyHostToDevice, st));
-  MT_CUDA_CHECK(cudaMemcpyAsync(d_w32.p, w32.data(), w32.size() * 4, cudaMemcpyHostToDevice, st));
-  RC(dalloc(d_big, Rt)); RC(dalloc(d_mu, Rh)); RC(dalloc(d_m, Rh * 2)); RC(dalloc(d_half, (Rt / MT_TILE) * 4)); RC(dalloc(d_bk, (Rh / MT_BLK) * 8 + 8));
-  RC(dalloc(d_tsum, (Rt / MT_TILE) * 4)); RC(dalloc(d_tbase, (Rt / MT_TILE) * 8)); RC(dalloc(d_run, 8));
-  MT_CUDA_CHECK(cudaMemsetAsync(d_run.p, 0, 8, st));
-  RC(dalloc(d_caps, caps.size() * sizeof(CaptureTargetH)));
-  if (!caps.empty())
-    MT_CUDA_CHECK(cudaMemcpyAsync(d_caps.p, caps.data(), caps.size() * sizeof(CaptureTargetH), cudaMemcpyHostToDevice, st));
-  const u64 nsmall = out->small_m_out ? job->cap_small + 1 : 0;
-  RC(dalloc(d_small, nsmall * 8));
-
-  ElemDev E;
-  E.vd = d_vd.as<double>(); E.vlo = d_vlo.as<u64>(); E.vhi = d_vhi.as<u64>(); E.vbits = d_vb.as<uint8_t>();
-  E.k = d_k.as<u64>(); E.tgt = d_tgt.as<uint32_t>(); E.mcut = d_mc.as<u64>(); E.xcut = d_x.as<u64>();
-  E.lo = d_lo.as<u64>(); E.lo_w = d_low.as<u64>(); E.dq_hi = d_dq.as<u64>(); E.d_sp = d_dsp.as<u64>(); E.n = NE;
+  u64 cap_c_lo = 1, cap_c_hi = 0, cap_small = 0, nsmall = 0;
   UpdateCtx* uc = nullptr;
-  RC(mt_update_create(&uc, E, d_acc.as<u64>(), d_mmc.as<int32_t>(), d_tmax.as<u64>(), d_tbits.as<uint8_t>(),
-                      ntiles, tdev.data(), N, grp, st));
-  struct UcGuard { UpdateCtx* c; ~UcGuard() { mt_update_destroy(c); } } ug{uc};
-
-  cudaEvent_t ev[6];
-  for (int i = 0; i < 6; i++) MT_CUDA_CHECK(cudaEventCreate(&ev[i]));
-  struct EvGuard { cudaEvent_t* e; ~EvGuard() { for (int i = 0; i < 6; i++) cudaEventDestroy(e[i]); } } eg{ev};
-  MT_CUDA_CHECK(cudaEventRecord(ev[0], st));
-
-  auto make_seg = [&](u64 Y0, u64 R, bool head) {
+  KTimer kt;
+  int64_t m_head = 0, tail_total = 0;
+  double ms_setup = 0, ms_head = 0, ms_tail = 0, ms_gather = 0, ms_fin = 0;
+  cudaEvent_t ev[6] = {};
+  int phase = 0;  // 1 after sieve_update, 2 after tail_offset, 3 after gather
+  ~mt_plan() {
+    if (device >= 0) cudaSetDevice(device);
+    mt_update_destroy(uc);
+    for (auto& e : ev) if (e) cudaEventDestroy(e);
+    kt.drain();
+    if (own_stream && st) cudaStreamDestroy(st);
+  }
+  // y of the first cell of tail segment s
+  u64 tail_y0(u64 s) const { return head_lim + s * Rt; }
+  // Q slice [j0, j1] of target t whose quotients fall in rank r's tail (empty: j0 > j1)
+  void q_slice(int t, uint32_t r, u64& j0, u64& j1) const {
+    u64 s0 = tail_segs * r / world, s1 = tail_segs * (r + 1) / world;
+    j0 = 1; j1 = 0;
+    if (s0 >= s1 || jq1[t] < jq0[t]) return;
+    const u64 ya = tail_y0(s0), yb = tail_y0(s1) - 1;  // y in [ya, yb]
+    // floor(n/j) in [ya, yb]  <=>  j in [floor(n/(yb+1)) + 1, floor(n/ya)]
+    u128 lo = n[t] / ((u128)yb + 1) + 1, hi = n[t] / (u128)ya;
+    if (lo < jq0[t]) lo = jq0[t];
+    if (hi > jq1[t]) hi = jq1[t];
+    if (lo > hi) return;
+    j0 = (u64)lo; j1 = (u64)hi;
+  }
+  SieveSegment make_seg(u64 Y0, u64 R, bool head) {
     SieveSegment s{};
     const u64 y2 = Y0 + R - 1;
     PrimeCut c = prime_cut(pt.p, y2);
@@ -752,72 +628,384 @@ extern "C" int mt_run(const mt_job* job, mt_result* out) {
     a.states_out = nullptr;
     a.caps = d_caps.p; a.n_cap = (int)caps.size();
     return s;
-  };
+  }
+};
 
-  // ---- head
-  for (u64 s = 0; s < head_segs; s++) {
-    const u64 Y0 = s * Rh;
-    SieveSegment sg = make_seg(Y0, Rh, true);
-    RC(mt_launch_sieve_segment(sg, st));
-    launches += 6;
-    RC(mt_update_head_segment(uc, Y0, Rh, d_mu.as<int8_t>(), d_m.as<int16_t>(), d_bk.as<int64_t>(), st));
-    if (nsmall && Y0 <= job->cap_small) {
-      k_copy_small<<<(unsigned)((Rh + 255) / 256), 256, 0, st>>>(d_m.as<int16_t>(), d_bk.as<int64_t>(), Y0, Rh, job->cap_small, d_small.as<int64_t>());
-      launches++;
+#define PLAN_DEV(p) do { if ((p)->device >= 0) MT_CUDA_CHECK(cudaSetDevice((p)->device)); } while (0)
+
+static int plan_setup(mt_plan* P, const mt_job* job) {
+  auto T0 = std::chrono::steady_clock::now();
+  if (!job || job->n_targets == 0) { mt_set_error("empty job"); return MT_ERR_VALUE; }
+  if (job->device >= 0) MT_CUDA_CHECK(cudaSetDevice(job->device));
+  MT_CUDA_CHECK(cudaGetDevice(&P->device));
+  const int N = (int)job->n_targets;
+  P->N = N;
+  P->u = job->u;
+  P->world = job->shard_world > 1 ? job->shard_world : 1;
+  P->rank = job->shard_rank;
+  P->flags = job->flags;
+  if (P->rank >= P->world) { mt_set_error("shard_rank %u >= shard_world %u", P->rank, P->world); return MT_ERR_VALUE; }
+  const u64 u = P->u;
+  P->n.resize(N); P->K.resize(N); P->e0.assign(N + 1, 0);
+  P->n_lo.assign(job->n_lo, job->n_lo + N);
+  P->n_hi.assign(job->n_hi, job->n_hi + N);
+  for (int i = 0; i < N; i++) {
+    P->n[i] = ((u128)job->n_hi[i] << 64) | job->n_lo[i];
+    if (P->n[i] < 4) { mt_set_error("exact job requires n >= 4"); return MT_ERR_VALUE; }
+    if (job->n_hi[i] >= (1ull << 11)) { mt_set_error("n >= 2^75 is outside the engine's range"); return MT_ERR_RESOURCE; }
+    if ((u128)u <= ceil_sqrt_u128(P->n[i])) { mt_set_error("u must exceed ceil(sqrt(n))"); return MT_ERR_VALUE; }
+    P->K[i] = (u64)(P->n[i] / u);
+    P->e0[i + 1] = P->e0[i] + P->K[i];
+  }
+  const u64 NE = P->NE = P->e0[N];
+  if (job->stream) { P->st = (cudaStream_t)job->stream; P->own_stream = false; }
+  else { MT_CUDA_CHECK(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking)); P->own_stream = true; }
+  cudaStream_t st = P->st;
+  P->kt.init((P->flags & MT_FLAG_TIMING) != 0);
+  for (auto& e : P->ev) MT_CUDA_CHECK(cudaEventCreate(&e));
+
+  // ---- elements (engine.py:134-159)
+  RC(dalloc(P->d_nlo, N * 8)); RC(dalloc(P->d_nhi, N * 8)); RC(dalloc(P->d_e0, (N + 1) * 8));
+  RC(dalloc(P->d_vd, NE * 8)); RC(dalloc(P->d_vlo, NE * 8)); RC(dalloc(P->d_vhi, NE * 8)); RC(dalloc(P->d_vb, NE));
+  RC(dalloc(P->d_k, NE * 8)); RC(dalloc(P->d_tgt, NE * 4)); RC(dalloc(P->d_D, NE * 8)); RC(dalloc(P->d_x, NE * 8));
+  RC(dalloc(P->d_mc, NE * 8)); RC(dalloc(P->d_lo, NE * 8)); RC(dalloc(P->d_low, NE * 8)); RC(dalloc(P->d_dq, NE * 8));
+  RC(dalloc(P->d_acc, NE * 8)); RC(dalloc(P->d_mmc, NE * 4)); RC(dalloc(P->d_dsp, NE * 8)); RC(dalloc(P->d_fin, NE * 8));
+  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_nlo.p, job->n_lo, N * 8, cudaMemcpyHostToDevice, st));
+  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_nhi.p, job->n_hi, N * 8, cudaMemcpyHostToDevice, st));
+  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_e0.p, P->e0.data(), (N + 1) * 8, cudaMemcpyHostToDevice, st));
+  {
+    ElemInitArgs a{P->d_nlo.as<u64>(), P->d_nhi.as<u64>(), P->d_e0.as<u64>(), N, u, NE,
+                   P->d_vd.as<double>(), P->d_vlo.as<u64>(), P->d_vhi.as<u64>(), P->d_vb.as<uint8_t>(), P->d_k.as<u64>(),
+                   P->d_tgt.as<uint32_t>(), P->d_D.as<u64>(), P->d_x.as<u64>(), P->d_mc.as<u64>(), P->d_lo.as<u64>()};
+    if (NE) k_elem_init<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(a);
+    P->launches++;
+    MT_CUDA_CHECK(cudaGetLastError());
+  }
+  std::vector<unsigned long long> tstat(3 * N, 0);
+  {
+    DevBuf d_ts;
+    RC(dalloc(d_ts, 3 * N * 8));
+    MT_CUDA_CHECK(cudaMemsetAsync(d_ts.p, 0, 3 * N * 8, st));
+    if (NE) k_elem_stats<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, P->d_tgt.as<uint32_t>(), P->d_mc.as<u64>(), P->d_x.as<u64>(), P->d_lo.as<u64>(), d_ts.as<unsigned long long>());
+    P->launches++;
+    MT_CUDA_CHECK(cudaMemcpyAsync(tstat.data(), d_ts.p, 3 * N * 8, cudaMemcpyDeviceToHost, st));
+    MT_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+  for (int i = 0; i < N; i++) {
+    P->Ymc = std::max<u64>(P->Ymc, tstat[3 * i]);
+    P->counted_items += tstat[3 * i + 1];
+    P->dense_items += tstat[3 * i + 2];
+  }
+
+  // ---- quotient tables: Q_t[j] = M(floor(n_t/j)), j in [jq0_t, jq1_t]
+  const u64 q_budget = job->q_budget_bytes ? job->q_budget_bytes : (48ull << 30);
+  P->J.assign(N, 0); P->jq0.assign(N, 0); P->jq1.assign(N, 0);
+  P->cap_c_lo = job->cap_c_lo; P->cap_c_hi = job->cap_c_hi;
+  for (int i = 0; i < N; i++) {
+    P->jq0[i] = (u64)(P->n[i] / ((u128)u + 1)) + 1;
+    P->J[i] = (u64)(P->n[i] / ((u128)P->Ymc + 1));
+  }
+  for (int it = 0; it < 64; it++) {  // cap the tables to the budget by scaling J down uniformly
+    u64 q_total = 0;
+    for (int i = 0; i < N; i++) {
+      u64 hi = P->J[i];
+      if (i == 0 && P->cap_c_hi >= P->cap_c_lo && P->cap_c_hi > hi) hi = P->cap_c_hi;
+      P->jq1[i] = hi;
+      if (hi >= P->jq0[i]) q_total += (hi - P->jq0[i] + 1);
+    }
+    if (q_total * 4 <= q_budget) break;
+    for (int i = 0; i < N; i++) P->J[i] = P->J[i] / 2;
+  }
+  for (int i = 0; i < N; i++)
+    if (P->J[i] < P->jq0[i]) P->J[i] = 0;  // no Q-gather for this target
+  P->d_Q.clear();
+  P->d_Q.reserve(N);
+  P->tdev.resize(N);
+  for (int i = 0; i < N; i++) {
+    P->d_Q.emplace_back();
+    u64 cnt = P->jq1[i] >= P->jq0[i] ? P->jq1[i] - P->jq0[i] + 1 : 0;
+    RC(dalloc(P->d_Q[i], cnt * 4));
+    P->tdev[i].Q = P->d_Q[i].as<int>();
+    P->tdev[i].jq0 = P->jq0[i];
+    if (cnt) {
+      CaptureTargetH c;
+      c.n_lo = job->n_lo[i]; c.n_hi = job->n_hi[i];
+      c.nd = job->n_hi[i] ? (double)job->n_hi[i] * 18446744073709551616.0 + (double)job->n_lo[i] : (double)job->n_lo[i];
+      c.nbits = 0;
+      for (u128 x = P->n[i]; x; x >>= 1) c.nbits++;
+      c.jq0 = P->jq0[i]; c.jq1 = P->jq1[i]; c.Q = P->tdev[i].Q;
+      P->caps.push_back(c);
     }
   }
-  MT_CUDA_CHECK(cudaEventRecord(ev[1], st));
-  // ---- tail
-  for (u64 s = 0; s < tail_segs; s++) {
-    const u64 Y0 = head_lim + s * Rt;
-    SieveSegment sg = make_seg(Y0, Rt, false);
-    RC(mt_launch_sieve_segment(sg, st));
-    launches += 5;
+  RC(dalloc(P->d_J, N * 8));
+  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_J.p, P->J.data(), N * 8, cudaMemcpyHostToDevice, st));
+  if (NE) k_elem_split<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, P->d_k.as<u64>(), P->d_tgt.as<uint32_t>(), P->d_J.as<u64>(), P->d_lo.as<u64>(), P->d_x.as<u64>(), P->d_low.as<u64>(), P->d_dq.as<u64>());
+  if (NE) k_elem_dsp<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, P->d_vd.as<double>(), P->d_dsp.as<u64>());
+  P->launches += 2;
+  // element groups for the window walk: consecutive k of one target, size clamp(k/8, 32, 1024)
+  for (int i = 0; i < N; i++) {
+    u64 k0 = 1;
+    while (k0 <= P->K[i]) {
+      P->gstart.push_back(P->e0[i] + k0 - 1);
+      k0 += std::min<u64>(1024, std::max<u64>(32, k0 / 8));
+    }
   }
-  MT_CUDA_CHECK(cudaEventRecord(ev[2], st));
-  // ---- Q-gather + resolve
-  RC(mt_update_qgather(uc, st));
-  RC(mt_update_finish(uc, st));
-  MT_CUDA_CHECK(cudaEventRecord(ev[3], st));
-  DevBuf d_fin;
-  RC(dalloc(d_fin, NE * 8));
-  for (int i = 0; i < N; i++)
-    RC(mt_finalize_dev(d_acc.as<u64>() + e0[i], d_D.as<u64>() + e0[i], K[i], d_fin.as<int64_t>() + e0[i], st));
-  MT_CUDA_CHECK(cudaEventRecord(ev[4], st));
-  if (out->finals && NE)
-    MT_CUDA_CHECK(cudaMemcpyAsync(out->finals, d_fin.p, NE * 8, cudaMemcpyDeviceToHost, st));
-  if (out->acc_out && NE)
-    MT_CUDA_CHECK(cudaMemcpyAsync(out->acc_out, d_acc.p, NE * 8, cudaMemcpyDeviceToHost, st));
+  const u64 ng = P->ng = P->gstart.size();
+  P->gstart.push_back(NE);
+  RC(dalloc(P->d_gs, (ng + 1) * 8)); RC(dalloc(P->d_gylo, ng * 8)); RC(dalloc(P->d_gyhi, ng * 8)); RC(dalloc(P->d_gw, ng));
+  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_gs.p, P->gstart.data(), (ng + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (ng) k_group_meta<<<(unsigned)ng, 256, 0, st>>>(P->d_gs.as<u64>(), ng, P->d_vlo.as<u64>(), P->d_vhi.as<u64>(), P->d_x.as<u64>(), P->d_low.as<u64>(), P->d_dsp.as<u64>(), P->d_gylo.as<u64>(), P->d_gyhi.as<u64>(), P->d_gw.as<uint8_t>());
+  P->launches++;
+  GroupDev grp{P->d_gs.as<u64>(), P->d_gylo.as<u64>(), P->d_gyhi.as<u64>(), P->d_gw.as<uint8_t>(), ng};
+  u64 head_end = P->Ymc;
+  {
+    DevBuf d_we;
+    RC(dalloc(d_we, 8));
+    MT_CUDA_CHECK(cudaMemsetAsync(d_we.p, 0, 8, st));
+    if (NE) k_window_extent<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, P->d_vlo.as<u64>(), P->d_vhi.as<u64>(), P->d_low.as<u64>(), P->d_x.as<u64>(), d_we.as<unsigned long long>());
+    P->launches++;
+    unsigned long long we = 0;
+    MT_CUDA_CHECK(cudaMemcpyAsync(&we, d_we.p, 8, cudaMemcpyDeviceToHost, st));
+    MT_CUDA_CHECK(cudaStreamSynchronize(st));
+    head_end = std::max<u64>(head_end, we);
+  }
+  P->cap_small = job->cap_small;
+  if (P->cap_small > head_end) head_end = P->cap_small;
+  if (head_end > u) head_end = u;
+  P->head_end = head_end;
+
+  // tiles metadata for the counted walk
+  const u64 ntiles = P->ntiles = (NE + MT_CT - 1) / MT_CT;
+  RC(dalloc(P->d_tmax, ntiles * 8)); RC(dalloc(P->d_tbits, ntiles));
+  if (ntiles) k_tile_meta<<<(unsigned)ntiles, MT_CT, 0, st>>>(NE, P->d_mc.as<u64>(), P->d_vb.as<uint8_t>(), P->d_tmax.as<u64>(), P->d_tbits.as<uint8_t>());
+  P->launches++;
+
+  // ---- segments
+  P->Rh = 1ull << (job->seg_log2_head ? job->seg_log2_head : 24);
+  P->Rt = 1ull << (job->seg_log2_tail ? job->seg_log2_tail : 27);
+  const u64 Rh = P->Rh, Rt = P->Rt;
+  if (Rh < MT_TILE || Rt < Rh || (Rt % Rh) || P->Rt > (1ull << 31)) { mt_set_error("bad segment sizes"); return MT_ERR_VALUE; }
+  P->head_segs = (head_end + 1 + Rh - 1) / Rh;
+  P->head_lim = P->head_segs * Rh;  // first y of the tail
+  P->tail_segs = 0;
+  if (u + 1 > P->head_lim) P->tail_segs = (u + 1 - P->head_lim + Rt - 1) / Rt;
+  P->y_last = P->head_lim + P->tail_segs * Rt - 1;
+  P->tseg0 = P->tail_segs * P->rank / P->world;
+  P->tseg1 = P->tail_segs * (P->rank + 1) / P->world;
+
+  build_primes(std::max<u64>(ceil_sqrt_u128(P->y_last) + 1, 2), P->pt);
+  uint8_t wheel[MT_WHEEL];
+  reference_wheel(wheel);
+  std::vector<uint32_t> w32;
+  build_wheel_words(wheel, w32);
+  const u64 np = P->pt.p.size();
+  RC(dalloc(P->d_p, np * 4)); RC(dalloc(P->d_rp, np * 8)); RC(dalloc(P->d_lg, np));
+  RC(dalloc(P->d_w32, w32.size() * 4));
+  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_p.p, P->pt.p.data(), np * 4, cudaMemcpyHostToDevice, st));
+  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_rp.p, P->pt.r.data(), np * 8, cudaMemcpyHostToDevice, st));
+  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_lg.p, P->pt.lg.data(), np, cudaMemcpyHostToDevice, st));
+  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_w32.p, w32.data(), w32.size() * 4, cudaMemcpyHostToDevice, st));
+  RC(dalloc(P->d_big, Rt)); RC(dalloc(P->d_mu, Rh)); RC(dalloc(P->d_m, Rh * 2));
+  RC(dalloc(P->d_half, (Rt / MT_TILE) * 4)); RC(dalloc(P->d_bk, (Rh / MT_BLK) * 8 + 8));
+  RC(dalloc(P->d_tsum, (Rt / MT_TILE) * 4)); RC(dalloc(P->d_tbase, (Rt / MT_TILE) * 8)); RC(dalloc(P->d_run, 8));
+  RC(dalloc(P->d_caps, P->caps.size() * sizeof(CaptureTargetH)));
+  if (!P->caps.empty())
+    MT_CUDA_CHECK(cudaMemcpyAsync(P->d_caps.p, P->caps.data(), P->caps.size() * sizeof(CaptureTargetH), cudaMemcpyHostToDevice, st));
+  P->nsmall = P->cap_small ? P->cap_small + 1 : 0;
+  RC(dalloc(P->d_small, P->nsmall * 8));
+
+  ElemDev E;
+  E.vd = P->d_vd.as<double>(); E.vlo = P->d_vlo.as<u64>(); E.vhi = P->d_vhi.as<u64>(); E.vbits = P->d_vb.as<uint8_t>();
+  E.k = P->d_k.as<u64>(); E.tgt = P->d_tgt.as<uint32_t>(); E.mcut = P->d_mc.as<u64>(); E.xcut = P->d_x.as<u64>();
+  E.lo = P->d_lo.as<u64>(); E.lo_w = P->d_low.as<u64>(); E.dq_hi = P->d_dq.as<u64>(); E.d_sp = P->d_dsp.as<u64>(); E.n = NE;
+  Shard sh;
+  sh.rank = P->rank; sh.world = P->world; sh.flags = P->flags;
+  RC(mt_update_create(&P->uc, E, P->d_acc.as<u64>(), P->d_mmc.as<int32_t>(), P->d_tmax.as<u64>(), P->d_tbits.as<uint8_t>(),
+                      ntiles, P->tdev.data(), N, grp, sh, &P->kt, st));
+  MT_CUDA_CHECK(cudaStreamSynchronize(st));
+  P->ms_setup = ms_since(T0);
+  return MT_OK;
+}
+
+extern "C" int mt_plan_create(const mt_job* job, mt_plan** out) {
+  g_err[0] = 0;
+  if (!out) { mt_set_error("null plan out"); return MT_ERR_VALUE; }
+  *out = nullptr;
+  mt_plan* P = new mt_plan();
+  int rc = plan_setup(P, job);
+  if (rc != MT_OK) { delete P; return rc; }
+  *out = P;
+  return MT_OK;
+}
+
+extern "C" void mt_plan_destroy(mt_plan* p) { delete p; }
+
+// phase 1: head (sieve + this rank's share of the updates) and this rank's tail segments
+extern "C" int mt_plan_sieve_update(mt_plan* P, int64_t* m_head, int64_t* tail_total) {
+  PLAN_DEV(P);
+  cudaStream_t st = P->st;
+  P->kt.reset();
+  MT_CUDA_CHECK(cudaMemsetAsync(P->d_acc.p, 0, P->NE * 8, st));
+  MT_CUDA_CHECK(cudaMemsetAsync(P->d_mmc.p, 0, P->NE * 4, st));
+  MT_CUDA_CHECK(cudaMemsetAsync(P->d_run.p, 0, 8, st));
+  MT_CUDA_CHECK(cudaEventRecord(P->ev[0], st));
+  for (u64 s = 0; s < P->head_segs; s++) {
+    const u64 Y0 = s * P->Rh;
+    SieveSegment sg = P->make_seg(Y0, P->Rh, true);
+    RC(mt_launch_sieve_segment(sg, st, &P->kt));
+    P->launches += 6;
+    RC(mt_update_head_segment(P->uc, Y0, P->Rh, P->d_mu.as<int8_t>(), P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), st));
+    if (P->nsmall && Y0 <= P->cap_small) {
+      k_copy_small<<<(unsigned)((P->Rh + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, P->Rh, P->cap_small, P->d_small.as<int64_t>());
+      P->launches++;
+    }
+  }
+  int64_t mh = 0, tt = 0;
+  MT_CUDA_CHECK(cudaMemcpyAsync(&mh, P->d_run.p, 8, cudaMemcpyDeviceToHost, st));
+  MT_CUDA_CHECK(cudaMemsetAsync(P->d_run.p, 0, 8, st));  // tail prefixes are rank-local
+  MT_CUDA_CHECK(cudaEventRecord(P->ev[1], st));
+  for (u64 s = P->tseg0; s < P->tseg1; s++) {
+    SieveSegment sg = P->make_seg(P->tail_y0(s), P->Rt, false);
+    RC(mt_launch_sieve_segment(sg, st, &P->kt));
+    P->launches += 5;
+  }
+  MT_CUDA_CHECK(cudaMemcpyAsync(&tt, P->d_run.p, 8, cudaMemcpyDeviceToHost, st));
+  MT_CUDA_CHECK(cudaEventRecord(P->ev[2], st));
+  MT_CUDA_CHECK(cudaStreamSynchronize(st));
+  MT_CUDA_CHECK(cudaGetLastError());
+  P->m_head = mh; P->tail_total = tt;
+  if (m_head) *m_head = mh;
+  if (tail_total) *tail_total = tt;
+  float f = 0;
+  cudaEventElapsedTime(&f, P->ev[0], P->ev[1]); P->ms_head = f;
+  cudaEventElapsedTime(&f, P->ev[1], P->ev[2]); P->ms_tail = f;
+  P->phase = 1;
+  return MT_OK;
+}
+
+// phase 2: absolute prefixes for this rank's tail captures: Q += M(Y_r - 1)
+extern "C" int mt_plan_tail_offset(mt_plan* P, int64_t offset) {
+  if (P->phase < 1) { mt_set_error("tail_offset before sieve_update"); return MT_ERR_CONTRACT; }
+  PLAN_DEV(P);
+  if (offset > INT32_MAX || offset < INT32_MIN) { mt_set_error("M offset beyond int32"); return MT_ERR_OVERFLOW; }
+  for (int t = 0; t < P->N; t++) {
+    u64 j0, j1;
+    P->q_slice(t, P->rank, j0, j1);
+    if (j0 > j1 || offset == 0) continue;
+    u64 cnt = j1 - j0 + 1;
+    k_q_offset<<<(unsigned)((cnt + 255) / 256), 256, 0, P->st>>>(P->tdev[t].Q + (j0 - P->jq0[t]), cnt, (int)offset);
+    P->launches++;
+    MT_CUDA_CHECK(cudaGetLastError());
+  }
+  MT_CUDA_CHECK(cudaStreamSynchronize(P->st));
+  P->phase = 2;
+  return MT_OK;
+}
+
+extern "C" int mt_plan_q_slice(mt_plan* P, uint32_t target, uint32_t rank, void** dptr, uint64_t* count) {
+  if ((int)target >= P->N || rank >= P->world) { mt_set_error("bad target/rank"); return MT_ERR_VALUE; }
+  u64 j0, j1;
+  P->q_slice((int)target, rank, j0, j1);
+  if (j0 > j1) { *dptr = nullptr; *count = 0; return MT_OK; }
+  *dptr = (void*)(P->tdev[target].Q + (j0 - P->jq0[target]));
+  *count = j1 - j0 + 1;
+  return MT_OK;
+}
+
+extern "C" int mt_plan_acc(mt_plan* P, void** dptr, uint64_t* count) {
+  *dptr = P->d_acc.p;
+  *count = P->NE;
+  return MT_OK;
+}
+
+// phase 3: dense items from the (complete) quotient tables; rank 0 also
+// applies the summation-by-parts correction -M(mcut)*xcut
+extern "C" int mt_plan_gather(mt_plan* P) {
+  if (P->phase < 2) { mt_set_error("gather before tail_offset"); return MT_ERR_CONTRACT; }
+  PLAN_DEV(P);
+  MT_CUDA_CHECK(cudaEventRecord(P->ev[3], P->st));
+  RC(mt_update_qgather(P->uc, P->st));
+  if (P->rank == 0) RC(mt_update_finish(P->uc, P->st));
+  MT_CUDA_CHECK(cudaEventRecord(P->ev[4], P->st));
+  MT_CUDA_CHECK(cudaStreamSynchronize(P->st));
+  float f = 0;
+  cudaEventElapsedTime(&f, P->ev[3], P->ev[4]); P->ms_gather = f;
+  P->phase = 3;
+  return MT_OK;
+}
+
+// phase 4: level-parallel resolve of every target (engine.py:394-402) and outputs
+extern "C" int mt_plan_resolve(mt_plan* P, mt_result* out) {
+  if (P->phase < 3) { mt_set_error("finalize before the harmonic array is complete"); return MT_ERR_CONTRACT; }
+  PLAN_DEV(P);
+  cudaStream_t st = P->st;
+  MT_CUDA_CHECK(cudaEventRecord(P->ev[4], st));
+  for (int i = 0; i < P->N; i++)
+    RC(mt_finalize_dev(P->d_acc.as<u64>() + P->e0[i], P->d_D.as<u64>() + P->e0[i], P->K[i], P->d_fin.as<int64_t>() + P->e0[i], st));
+  MT_CUDA_CHECK(cudaEventRecord(P->ev[5], st));
   DevBuf d_capm;
-  if (out->cap_m_out && job->cap_c_hi >= job->cap_c_lo) {
-    u64 cnt = job->cap_c_hi - job->cap_c_lo + 1;
-    if (job->cap_c_lo < jq0[0]) { mt_set_error("capture range below floor(n/(u+1))+1"); return MT_ERR_VALUE; }
+  if (out && out->finals && P->NE)
+    MT_CUDA_CHECK(cudaMemcpyAsync(out->finals, P->d_fin.p, P->NE * 8, cudaMemcpyDeviceToHost, st));
+  if (out && out->acc_out && P->NE)
+    MT_CUDA_CHECK(cudaMemcpyAsync(out->acc_out, P->d_acc.p, P->NE * 8, cudaMemcpyDeviceToHost, st));
+  if (out && out->cap_m_out && P->cap_c_hi >= P->cap_c_lo) {
+    u64 cnt = P->cap_c_hi - P->cap_c_lo + 1;
+    if (P->cap_c_lo < P->jq0[0]) { mt_set_error("capture range below floor(n/(u+1))+1"); return MT_ERR_VALUE; }
     RC(dalloc(d_capm, cnt * 8));
-    k_copy_caps<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(tdev[0].Q, jq0[0], job->cap_c_lo, cnt, d_capm.as<int64_t>());
+    k_copy_caps<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(P->tdev[0].Q, P->jq0[0], P->cap_c_lo, cnt, d_capm.as<int64_t>());
     MT_CUDA_CHECK(cudaMemcpyAsync(out->cap_m_out, d_capm.p, cnt * 8, cudaMemcpyDeviceToHost, st));
   }
-  if (nsmall) MT_CUDA_CHECK(cudaMemcpyAsync(out->small_m_out, d_small.p, nsmall * 8, cudaMemcpyDeviceToHost, st));
-  MT_CUDA_CHECK(cudaEventRecord(ev[5], st));
+  if (out && out->small_m_out && P->nsmall)
+    MT_CUDA_CHECK(cudaMemcpyAsync(out->small_m_out, P->d_small.p, P->nsmall * 8, cudaMemcpyDeviceToHost, st));
   MT_CUDA_CHECK(cudaStreamSynchronize(st));
-
+  MT_CUDA_CHECK(cudaGetLastError());
+  P->kt.drain();
+  float f = 0;
+  cudaEventElapsedTime(&f, P->ev[4], P->ev[5]); P->ms_fin = f;
+  if (!out) return MT_OK;
   // ---- stats (RunStats fields in closed form, engine.py:188-197)
   mt_stats& S = out->stats;
   memset(&S, 0, sizeof(S));
-  S.counted_items = counted_items;
-  S.dense_items = dense_items;
-  S.head_end = head_lim;
-  S.max_mcut = Ymc;
-  S.n_head_segments = head_segs;
-  S.n_tail_segments = tail_segs;
-  S.kernel_launches = launches + mt_update_launches(uc);
+  S.counted_items = P->counted_items;
+  S.dense_items = P->dense_items;
+  S.head_end = P->head_lim;
+  S.max_mcut = P->Ymc;
+  S.n_head_segments = P->head_segs;
+  S.n_tail_segments = P->tail_segs;
+  S.kernel_launches = P->launches + mt_update_launches(P->uc);
   u64 qe = 0;
-  for (int i = 0; i < N; i++) qe += jq1[i] >= jq0[i] ? jq1[i] - jq0[i] + 1 : 0;
+  for (int i = 0; i < P->N; i++) qe += P->jq1[i] >= P->jq0[i] ? P->jq1[i] - P->jq0[i] + 1 : 0;
   S.q_entries = qe;
-  float f;
-  cudaEventElapsedTime(&f, ev[0], ev[1]); S.ms_update_head = f;
-  cudaEventElapsedTime(&f, ev[1], ev[2]); S.ms_sieve_tail = f;
-  cudaEventElapsedTime(&f, ev[2], ev[3]); S.ms_qgather = f;
-  cudaEventElapsedTime(&f, ev[3], ev[4]); S.ms_finalize = f;
-  S.ms_total = ms_since(T0);
+  S.ms_update_head = P->ms_head;
+  S.ms_sieve_tail = P->ms_tail;
+  S.ms_qgather = P->ms_gather;
+  S.ms_finalize = P->ms_fin;
+  S.ms_total = P->ms_head + P->ms_tail + P->ms_gather + P->ms_fin;
+  S.ms_setup = P->ms_setup;
+  S.m_head = P->m_head;
+  S.tail_total = P->tail_total;
+  S.tail_seg_begin = P->tseg0;
+  S.tail_seg_end = P->tseg1;
+  for (int c = 0; c < KT_NCLASS && c < 8; c++) { S.kernel_ms[c] = P->kt.ms[c]; S.kernel_count[c] = P->kt.n[c]; }
+  S.ms_counted_kernel = P->kt.ms[KT_COUNTED];
+  S.ms_dense_kernel = P->kt.ms[KT_DWIN] + P->kt.ms[KT_DSPARSE] + P->kt.ms[KT_QGATHER];
+  return MT_OK;
+}
+
+extern "C" int mt_run(const mt_job* job, mt_result* out) {
+  auto T0 = std::chrono::steady_clock::now();
+  if (job && job->shard_world > 1) {
+    mt_set_error("mt_run is single-rank; use the plan API for shard_world > 1");
+    return MT_ERR_VALUE;
+  }
+  mt_plan* P = nullptr;
+  RC(mt_plan_create(job, &P));
+  struct G { mt_plan* p; ~G() { mt_plan_destroy(p); } } g{P};
+  int64_t mh = 0, tt = 0;
+  RC(mt_plan_sieve_update(P, &mh, &tt));
+  RC(mt_plan_tail_offset(P, mh));
+  RC(mt_plan_gather(P));
+  RC(mt_plan_resolve(P, out));
+  if (out) out->stats.ms_total = ms_since(T0);
   return MT_OK;
 }

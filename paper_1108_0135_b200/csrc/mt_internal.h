@@ -1,6 +1,7 @@
 // Internal (non-ABI) declarations shared by the engine's translation units.
 #pragma once
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "../../include/mertens_sm100.h"
@@ -51,7 +52,58 @@ struct SieveSegment {
   SieveTileArgs tile;
 };
 
-int mt_launch_sieve_segment(const SieveSegment& s, cudaStream_t st);
+// Per-kernel-class device timing (MT_FLAG_TIMING): CUDA events around every
+// launch of a class, on the launching stream, drained through a ring so that
+// a long job does not hold one event pair per launch.
+enum { KT_SIEVE_TILE = 0, KT_SIEVE_LARGE, KT_COUNTED, KT_DWIN, KT_DSPARSE, KT_QGATHER, KT_OTHER, KT_NCLASS };
+struct KTimer {
+  bool on = false;
+  static const int RING = 1024;
+  cudaEvent_t a[RING], b[RING];
+  int cls[RING];
+  bool busy[RING];
+  int next = 0, open = -1;
+  double ms[KT_NCLASS] = {0};
+  uint64_t n[KT_NCLASS] = {0};
+  void init(bool enable) {
+    on = enable;
+    if (!on) return;
+    for (int i = 0; i < RING; i++) {
+      cudaEventCreate(&a[i]); cudaEventCreate(&b[i]); busy[i] = false;
+    }
+  }
+  void reset() {
+    drain();
+    for (int i = 0; i < KT_NCLASS; i++) { ms[i] = 0; n[i] = 0; }
+  }
+  void retire(int i) {
+    if (!busy[i]) return;
+    cudaEventSynchronize(b[i]);
+    float f = 0.f;
+    cudaEventElapsedTime(&f, a[i], b[i]);
+    ms[cls[i]] += f; n[cls[i]]++;
+    busy[i] = false;
+  }
+  void begin(int c, cudaStream_t st) {
+    if (!on) return;
+    retire(next);
+    cls[next] = c; open = next;
+    cudaEventRecord(a[next], st);
+  }
+  void end(cudaStream_t st) {
+    if (!on || open < 0) return;
+    cudaEventRecord(b[open], st);
+    busy[open] = true; open = -1;
+    next = (next + 1) % RING;
+  }
+  void drain() { if (on) for (int i = 0; i < RING; i++) retire(i); }
+  ~KTimer() {
+    if (!on) return;
+    for (int i = 0; i < RING; i++) { cudaEventDestroy(a[i]); cudaEventDestroy(b[i]); }
+  }
+};
+
+int mt_launch_sieve_segment(const SieveSegment& s, cudaStream_t st, KTimer* kt = nullptr);
 
 // element arrays (device, SoA), one entry per harmonic-array element of every target
 struct ElemDev {
@@ -84,10 +136,15 @@ struct GroupDev {        // element groups for the shared-memory window walk
   const uint8_t* wide;   // [ng] 1 if some member has xcut >= 2^30 (64-bit walk)
   uint64_t ng;
 };
+// work sharding across ranks: rank r of w takes work units u with u % w == r
+struct Shard {
+  uint32_t rank = 0, world = 1;
+  uint32_t flags = 0;  // MT_FLAG_* (force-wide arithmetic paths for tests)
+};
 int mt_update_create(UpdateCtx** ctx, const ElemDev& E, uint64_t* acc, int32_t* Mmc,
                      const uint64_t* tile_mcut_max, const uint8_t* tile_vbits_max,
                      uint64_t ntiles, const TargetDev* tgts, int ntgt, const GroupDev& grp,
-                     cudaStream_t st);
+                     const Shard& sh, KTimer* kt, cudaStream_t st);
 void mt_update_destroy(UpdateCtx* ctx);
 int mt_update_head_segment(UpdateCtx* ctx, uint64_t Y0, uint64_t R, const int8_t* mu,
                            const int16_t* M16, const int64_t* bk, cudaStream_t st);

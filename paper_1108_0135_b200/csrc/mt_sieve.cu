@@ -322,15 +322,17 @@ __global__ void k_fixup_Q(SieveTileArgs a, const i64* __restrict__ tile_base) {
 }
 
 // ------------------------------------------------------------------ host side
-int mt_launch_sieve_segment(const SieveSegment& s, cudaStream_t st) {
+int mt_launch_sieve_segment(const SieveSegment& s, cudaStream_t st, KTimer* kt) {
   // 1. large primes into `big`
   if (s.big) {
     MT_CUDA_CHECK(cudaMemsetAsync(s.big, 0, s.R, st));
     if (s.p_large_end > s.p_large_begin) {
       u32 n = s.p_large_end - s.p_large_begin;
+      if (kt) kt->begin(KT_SIEVE_LARGE, st);
       k_sieve_large<<<(n + 255) / 256, 256, 0, st>>>(s.big, s.Y0, s.R, s.y2, s.primes, s.rprimes,
                                                      s.logs, s.p_large_begin, s.p_large_end,
                                                      s.do_logs_large);
+      if (kt) kt->end(st);
       MT_CUDA_CHECK(cudaGetLastError());
     }
   }
@@ -343,7 +345,9 @@ int mt_launch_sieve_segment(const SieveSegment& s, cudaStream_t st) {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
+  if (kt) kt->begin(KT_SIEVE_TILE, st);
   k_sieve_tile<MT_SIEVE_THREADS><<<ntiles, MT_SIEVE_THREADS, smem, st>>>(a);
+  if (kt) kt->end(st);
   MT_CUDA_CHECK(cudaGetLastError());
   if (s.running) {
     k_seg_scan<<<1, 1024, 0, st>>>(a.tile_sum, ntiles, s.running, s.tile_base, a.half_out, s.bk);

@@ -51,6 +51,8 @@ struct UpdateCtx {
   size_t cub_bytes;
   uint64_t launches;
   int nsm;
+  Shard sh;
+  KTimer* kt;
 };
 
 // ---------------------------------------------------------------- counted walk
@@ -89,6 +91,7 @@ struct CountedArgs {
   const int8_t* mu;     // segment mu
   u64 Y0;
   uint64_t* counter;
+  u32 rank, world, force_wide;
 };
 
 __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u64 total = a.off[a.ntiles];
   for (;;) {
-    if (tid == 0) s_unit = atomicAdd((unsigned long long*)a.counter, 1ull);
+    if (tid == 0) s_unit = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
     __syncthreads();
     const u64 unit = s_unit;
     if (unit >= total) break;
@@ -169,9 +172,9 @@ __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
         const double vd = a.E.vd[e];
         const u64 vlo = a.E.vlo[e];
         const int vb = a.tile_vbits_max[tau];
-        const bool ok = (vb <= 50) || (mlo >= (1ull << (vb - 50)));
+        const bool ok = !(a.force_wide & MT_FLAG_FORCE_SLOWDIV) && ((vb <= 50) || (mlo >= (1ull << (vb - 50))));
         u64 S;
-        if (ok && mhi <= (1ull << 31)) {
+        if (ok && mhi <= (1ull << 31) && !(a.force_wide & MT_FLAG_FORCE_WIDE)) {
           const u32 v32 = (u32)vlo;
           u64 ap = 0, an = 0;
           u32 cp = 0, cn = 0;
@@ -190,19 +193,21 @@ __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
           }
           S = (ap - (u64)bp_ * MT_EXP52 - cp) - (an - (u64)bn_ * MT_EXP52 - cn);
         } else if (ok) {
+          // 64-bit remainder: the estimate must be stripped of the exponent
+          // bits before it is multiplied by m (m >= 2^31 here)
           u64 ap = 0, an = 0, cp = 0, cn = 0;
           for (int i = 0; i < bp_; i++) {
-            u64 b = (u64)__double_as_longlong(fma(vd, rmL[i], MT_TWO52));
+            u64 b = (u64)__double_as_longlong(fma(vd, rmL[i], MT_TWO52)) - MT_EXP52;
             i64 t = (i64)(vlo - b * (mhw | mL[i]));
             ap += b; cp += (u64)t >> 63;
           }
           for (int i = 0; i < bn_; i++) {
             int idx = MT_CM - 1 - i;
-            u64 b = (u64)__double_as_longlong(fma(vd, rmL[idx], MT_TWO52));
+            u64 b = (u64)__double_as_longlong(fma(vd, rmL[idx], MT_TWO52)) - MT_EXP52;
             i64 t = (i64)(vlo - b * (mhw | mL[idx]));
             an += b; cn += (u64)t >> 63;
           }
-          S = (ap - (u64)bp_ * MT_EXP52 - cp) - (an - (u64)bn_ * MT_EXP52 - cn);
+          S = (ap - cp) - (an - cn);
         } else {  // exact slow path (small m with wide v)
           const u64 vhi = a.E.vhi[e];
           u64 sp = 0, sn = 0;
@@ -289,6 +294,7 @@ struct WinArgs {
   const int64_t* bk;
   u64 Y0;
   uint64_t* counter;
+  u32 rank, world, force_wide;
 };
 
 __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
@@ -298,7 +304,7 @@ __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
   const int tid = threadIdx.x;
   const u64 total = a.uoff[a.G.ng];
   for (;;) {
-    if (tid == 0) s_unit = atomicAdd((unsigned long long*)a.counter, 1ull);
+    if (tid == 0) s_unit = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
     __syncthreads();
     const u64 unit = s_unit;
     if (unit >= total) break;
@@ -310,7 +316,7 @@ __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
       for (int i = tid; i < (int)(MT_BLK / 8); i += 256) smem_win[i] = src[i];
     }
     const i64 base = a.bk[w];
-    const bool wide = a.G.wide[g];
+    const bool wide = a.G.wide[g] || a.force_wide;
     __syncthreads();
     const u64 e1 = a.G.start[g + 1];
     for (u64 e = a.G.start[g] + tid; e < e1; e += 256) {
@@ -373,6 +379,7 @@ struct SparseArgs {
   const int64_t* bk;
   u64 Y0;
   uint64_t* counter;
+  u32 rank, world;
 };
 
 __global__ void __launch_bounds__(256) k_dsparse(SparseArgs a) {
@@ -382,8 +389,8 @@ __global__ void __launch_bounds__(256) k_dsparse(SparseArgs a) {
     const int lane = threadIdx.x & 31;
     if (lane == 0) base_unit = atomicAdd((unsigned long long*)a.counter, 32ull);
     base_unit = __shfl_sync(0xffffffffu, base_unit, 0);
-    if (base_unit >= total) break;
-    const u64 unit = base_unit + lane;
+    if (base_unit * a.world + a.rank >= total) break;
+    const u64 unit = (base_unit + lane) * a.world + a.rank;
     if (unit >= total) continue;
     const u64 e = upper_idx(a.roff, a.E.n + 1, unit);
     const u64 j = unit - a.roff[e];
@@ -412,6 +419,7 @@ struct QArgs {
   uint64_t n;
   uint64_t* counter;
   const TargetDev* tgts;
+  u32 rank, world;
 };
 
 __global__ void __launch_bounds__(256) k_qitems(QArgs a) {
@@ -419,7 +427,7 @@ __global__ void __launch_bounds__(256) k_qitems(QArgs a) {
   const u64 total = a.off[a.n];
   for (;;) {
     u64 w = 0;
-    if (lane == 0) w = atomicAdd((unsigned long long*)a.counter, 1ull);
+    if (lane == 0) w = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
     w = __shfl_sync(0xffffffffu, w, 0);
     const u64 base = w * (32ull * IPT);
     if (base >= total) break;
@@ -486,8 +494,11 @@ static int scan_u64(UpdateCtx* c, const uint64_t* in, uint64_t* out, uint64_t n,
 
 int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* Mmc,
                      const uint64_t* tile_mcut_max, const uint8_t* tile_vbits_max, uint64_t ntiles,
-                     const TargetDev* tgts, int ntgt, const GroupDev& grp, cudaStream_t st) {
+                     const TargetDev* tgts, int ntgt, const GroupDev& grp, const Shard& sh,
+                     KTimer* kt, cudaStream_t st) {
   UpdateCtx* c = new UpdateCtx();
+  c->sh = sh;
+  c->kt = kt;
   c->G = grp;
   c->E = E; c->acc = acc; c->Mmc = Mmc;
   c->tile_mcut_max = tile_mcut_max; c->tile_vbits_max = tile_vbits_max; c->ntiles = ntiles;
@@ -536,8 +547,11 @@ int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const 
     int rc = scan_u64(c, units, off, c->ntiles + 1, st);
     if (rc) return rc;
     MT_CUDA_CHECK(cudaMemsetAsync(c->counter, 0, sizeof(uint64_t) * 4, st));
-    CountedArgs a{E, c->acc, c->tile_mcut_max, c->tile_vbits_max, off, c->ntiles, mu, Y0, c->counter};
+    CountedArgs a{E, c->acc, c->tile_mcut_max, c->tile_vbits_max, off, c->ntiles, mu, Y0, c->counter,
+                  c->sh.rank, c->sh.world, c->sh.flags};
+    c->kt->begin(KT_COUNTED, st);
     k_counted<<<c->nsm * 6, MT_CT, 0, st>>>(a);
+    c->kt->end(st);
     c->launches++;
     MT_CUDA_CHECK(cudaGetLastError());
   }
@@ -550,8 +564,11 @@ int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const 
     c->launches++;
     int rc = scan_u64(c, c->gunits, c->guoff, c->G.ng + 1, st);
     if (rc) return rc;
-    WinArgs a{E, c->acc, c->G, c->guoff, c->gwfirst, M16, bk, Y0, c->counter + 1};
+    WinArgs a{E, c->acc, c->G, c->guoff, c->gwfirst, M16, bk, Y0, c->counter + 1,
+              c->sh.rank, c->sh.world, (c->sh.flags & MT_FLAG_FORCE_WIDE) ? 1u : 0u};
+    c->kt->begin(KT_DWIN, st);
     k_dwin<<<c->nsm * 3, 256, MT_BLK * 2, st>>>(a);
+    c->kt->end(st);
     c->launches++;
     MT_CUDA_CHECK(cudaGetLastError());
   }
@@ -561,8 +578,10 @@ int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const 
     c->launches++;
     int rc = scan_u64(c, c->cnt, c->off, E.n + 1, st);
     if (rc) return rc;
-    SparseArgs a{E, c->acc, c->off, c->dtop, c->qoff, M16, bk, Y0, c->counter + 2};
+    SparseArgs a{E, c->acc, c->off, c->dtop, c->qoff, M16, bk, Y0, c->counter + 2, c->sh.rank, c->sh.world};
+    c->kt->begin(KT_DSPARSE, st);
     k_dsparse<<<c->nsm * 8, 256, 0, st>>>(a);
+    c->kt->end(st);
     c->launches++;
     MT_CUDA_CHECK(cudaGetLastError());
   }
@@ -576,8 +595,10 @@ int mt_update_qgather(UpdateCtx* c, cudaStream_t st) {
   int rc = scan_u64(c, c->qcnt, c->qoff, E.n + 1, st);
   if (rc) return rc;
   MT_CUDA_CHECK(cudaMemsetAsync(c->counter + 3, 0, sizeof(uint64_t), st));
-  QArgs a{E, c->acc, c->qoff, E.n, c->counter + 3, c->tgts};
+  QArgs a{E, c->acc, c->qoff, E.n, c->counter + 3, c->tgts, c->sh.rank, c->sh.world};
+  c->kt->begin(KT_QGATHER, st);
   k_qitems<<<c->nsm * 8, 256, 0, st>>>(a);
+  c->kt->end(st);
   c->launches++;
   MT_CUDA_CHECK(cudaGetLastError());
   return MT_OK;

@@ -82,6 +82,9 @@ class EngineConfig:
     q_budget_bytes: int = 0
     seg_log2_head: int = 0
     seg_log2_tail: int = 0
+    engine_flags: int = 0          # MT_FLAG_FORCE_WIDE / _FORCE_SLOWDIV (tests), MT_FLAG_TIMING
+    distributed: bool = True       # shard over the default torch.distributed group when one is up
+    stream: int | None = None      # cudaStream_t (int) to run on; None: the engine's own
 
     def effective_workers(self) -> int:
         return self.workers if self.workers > 0 else (os.cpu_count() or 1)
@@ -209,16 +212,14 @@ def _split_n(ns):
     return lo, hi
 
 
-def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None):
-    """One mt_run call; returns (finals per n, cap_m, small_m, raw stats)."""
-    L = _lib.require_device()
+def make_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, rank=0, world=1):
+    """The mt_job of one exact request (the arrays it points at are kept on the job)."""
     for n in ns:
         if n >= ENGINE_N_BOUND:
             raise ResourceLimitError(f"n={n} exceeds the engine range 2^75")
     n_lo, n_hi = _split_n(ns)
-    K = [n // u for n in ns]
-    finals = np.zeros(sum(K), dtype=np.int64)
     job = _lib.MtJob()
+    job._keep = (n_lo, n_hi)
     job.n_targets = len(ns)
     job.n_lo = n_lo.ctypes.data_as(_lib._pu64)
     job.n_hi = n_hi.ctypes.data_as(_lib._pu64)
@@ -227,28 +228,52 @@ def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None)
     job.q_budget_bytes = config.q_budget_bytes
     job.seg_log2_head = config.seg_log2_head
     job.seg_log2_tail = config.seg_log2_tail
+    job.flags = config.engine_flags
+    job.stream = config.stream
+    job.shard_rank, job.shard_world = rank, world
+    if cap_c is not None and cap_c[1] >= cap_c[0]:
+        job.cap_c_lo, job.cap_c_hi = cap_c
+    else:
+        job.cap_c_lo, job.cap_c_hi = 1, 0
+    job.cap_small = cap_small
+    return job
+
+
+def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None):
+    """One exact job (mt_run, or the plan phases over the process group when
+    one is up); returns (finals per n, cap_m, small_m, raw stats)."""
+    L = _lib.require_device()
+    from . import distributed
+
+    rank, world = distributed.world() if config.distributed else (0, 1)
+    job = make_job(ns, u, config, cap_c, cap_small, rank, world)
+    K = [n // u for n in ns]
+    finals = np.zeros(sum(K), dtype=np.int64)
     res = _lib.MtResult()
     res.finals = finals.ctypes.data_as(_lib._pi64)
     cap_m = small_m = None
     if cap_c is not None and cap_c[1] >= cap_c[0]:
-        job.cap_c_lo, job.cap_c_hi = cap_c
         cap_m = np.zeros(cap_c[1] - cap_c[0] + 1, dtype=np.int64)
         res.cap_m_out = cap_m.ctypes.data_as(_lib._pi64)
-    else:
-        job.cap_c_lo, job.cap_c_hi = 1, 0
     if cap_small:
-        job.cap_small = cap_small
         small_m = np.zeros(cap_small + 1, dtype=np.int64)
         res.small_m_out = small_m.ctypes.data_as(_lib._pi64)
     if acc_out is not None:
         res.acc_out = acc_out.ctypes.data_as(_lib._pu64)
-    _lib.check(L.mt_run(job, res))
+    if world > 1:
+        plan = distributed.DevicePlan(job)
+        try:
+            distributed.run_phases(plan, None, res)
+        finally:
+            plan.close()
+    else:
+        _lib.check(L.mt_run(job, res))
     out, o = [], 0
     for k in K:
         out.append(finals[o:o + k])
         o += k
-    st = res.stats
-    raw = {f: getattr(st, f) for f, _ in _lib.MtStats._fields_}
+    raw = _lib.stats_dict(res.stats)
+    raw["world"] = world
     return out, cap_m, small_m, raw
 
 

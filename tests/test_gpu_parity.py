@@ -193,3 +193,54 @@ def test_paper_1e16_and_quotients(engine, golden):
     assert r.value == J["paper"]["1e16"] == -3195437
     assert r.quotient(10) == J["reference_measured_survey"]["1e15"]
     assert r.quotient(1000) == J["reference_measured_survey"]["1e13"]
+
+
+@pytest.mark.parametrize("flags", [1, 2, 3])
+def test_forced_wide_paths(engine, golden, flags):
+    """The 64-bit remainder / 64-bit quotient-walk / exact-division code paths
+    (taken for real only when m or d pass 2^31, i.e. n >~ 1e18) forced on at
+    small n: identical finals."""
+    G, J = golden
+    r = engine.mertens_exact(10**10, engine.EngineConfig(engine_flags=flags))
+    assert np.array_equal(r._final, G["e10_final"]) and np.array_equal(r._cp_m, G["e10_cp_m"])
+    assert engine.mertens_exact(10**12, engine.EngineConfig(engine_flags=flags)).value == J["e12"]
+
+
+def test_plan_phases_reexecute(engine, golden):
+    """The plan API (mt_plan_*) at world size 1, executed twice on one plan."""
+    import ctypes
+
+    from paper_1108_0135_b200 import _lib
+    from paper_1108_0135_b200.engine import make_job
+
+    G, _ = golden
+    n = 10**10
+    job = make_job([n], engine.choose_u(n), engine.EngineConfig(engine_flags=_lib.MT_FLAG_TIMING))
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    _lib.check(L.mt_plan_create(ctypes.byref(job), ctypes.byref(h)))
+    try:
+        for _ in range(2):
+            res = _lib.MtResult()
+            fin = np.zeros(len(G["e10_final"]), np.int64)
+            res.finals = fin.ctypes.data_as(_lib._pi64)
+            mh, tt = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(L.mt_plan_sieve_update(h, ctypes.byref(mh), ctypes.byref(tt)))
+            _lib.check(L.mt_plan_tail_offset(h, mh.value))
+            _lib.check(L.mt_plan_gather(h))
+            _lib.check(L.mt_plan_resolve(h, ctypes.byref(res)))
+            assert np.array_equal(fin, G["e10_final"])
+            st = _lib.stats_dict(res.stats)
+            assert st["kernel_count"]["sieve_tile"] >= 1 and st["kernel_ms"]["counted"] > 0
+    finally:
+        L.mt_plan_destroy(h)
+
+
+@pytest.mark.slow
+def test_paper_1e19_and_quotients(engine, golden):
+    """C4: M(10^19) and, from the same run, M(10^18), M(10^17),
+    M(10^16) as quotients c = 10, 100, 1000."""
+    _, J = golden
+    r = engine.mertens_exact(10**19)
+    assert r.value == 899990187
+    assert (r.quotient(10), r.quotient(100), r.quotient(1000)) == (-46758740, -21830254, -3195437)

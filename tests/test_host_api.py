@@ -101,7 +101,7 @@ def test_library_exports_every_header_symbol():
     L = _lib.lib()
     for s in declared:
         assert hasattr(L, s)
-    assert L.mt_abi_version() == 1
+    assert L.mt_abi_version() == 2
 
 
 def test_no_gpu_fails_loudly():

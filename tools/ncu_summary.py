@@ -1,0 +1,64 @@
+"""Summarise ncu output for profiles/: a launch-list CSV (--metrics
+gpu__time_duration.sum) into per-kernel shares, and .ncu-rep captures into
+the metrics the roofline and DESIGN.md cite.
+
+  python tools/ncu_summary.py launches <launches.csv>
+  python tools/ncu_summary.py rep <file.ncu-rep> [...]
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "l1tex__throughput.avg.pct_of_peak_sustained_active",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
+        "smsp__inst_executed.sum"]
+
+
+def launches(path):
+    txt = open(path).read()
+    i = txt.find('"ID"')
+    rows = list(csv.DictReader(io.StringIO(txt[i:])))
+    tot = defaultdict(float)
+    cnt = defaultdict(int)
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r.get("Metric Unit", "")
+        v *= {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}.get(unit, 1.0)
+        k = r["Kernel Name"].split("(")[0]
+        tot[k] += v
+        cnt[k] += 1
+    s = sum(tot.values())
+    print(f"# {path}: {sum(cnt.values())} launches, {s:.3f} ms total (cold-cache, serialised)")
+    for k in sorted(tot, key=lambda k: -tot[k]):
+        print(f"{k:40s} {cnt[k]:7d} launches {tot[k]:10.3f} ms {100 * tot[k] / s:6.2f} %")
+
+
+def rep(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    for v in rows[2:]:
+        print(f"# {path}: {v[h.index('Kernel Name')][:60]}")
+        for w in WANT:
+            if w in h:
+                print(f"  {w:70s} {v[h.index(w)]:>16s} {units[h.index(w)]}")
+
+
+if __name__ == "__main__":
+    f = {"launches": launches, "rep": rep}[sys.argv[1]]
+    for p in sys.argv[2:]:
+        f(p)
