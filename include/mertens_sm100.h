@@ -88,6 +88,11 @@ int mt_mertens_range(uint64_t y1, uint64_t y2, int64_t* m_out);
  * [1, max pts].  Backs mertens_naive(n, checkpoints) (engine.py:553-603). */
 int mt_mertens_at(const uint64_t* pts, uint64_t npts, int64_t* m_out);
 
+/* the engine's production sieve (mt_sieve2.cu: presieve patterns, in-tile
+ * primes, bucketed large primes, look-back scan) over [y1, y2]: mu(y) into
+ * mu_out and, if m_out is non-null, M(y) into m_out (either may be null) */
+int mt_sieve_fast(uint64_t y1, uint64_t y2, int8_t* mu_out, int64_t* m_out);
+
 /* ---- 2. job-level production entry ----------------------------------------- */
 
 typedef struct {

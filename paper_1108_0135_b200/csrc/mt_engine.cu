@@ -308,6 +308,43 @@ extern "C" int mt_mertens_at(const uint64_t* pts, uint64_t npts, int64_t* m_out)
   return MT_OK;
 }
 
+// production sieve over [y1, y2] (parity tests of mt_sieve2.cu): mu and, when
+// m_out is given, M(y) (then sieving starts at 0 so prefixes are absolute)
+__global__ void k_m16_to_m(const int16_t* __restrict__ M16, const int64_t* __restrict__ bk, u64 n,
+                           int64_t* __restrict__ out) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = M16[i] + bk[i / MT_BLK];
+}
+
+extern "C" int mt_sieve_fast(uint64_t y1, uint64_t y2, int8_t* mu_out, int64_t* m_out) {
+  if (y2 < y1) { mt_set_error("bad range"); return MT_ERR_VALUE; }
+  const u64 T = MT_S2_TILE, NT = 256, R = T * NT;
+  u64 Y0 = m_out ? 0 : (y1 / T) * T;
+  const u64 y_last = ((y2 / R) + 1) * R + Y0;
+  Sieve2Host* h = nullptr;
+  struct G { Sieve2Host*& h; ~G() { mt_sieve2_destroy(h); } } g{h};
+  RC(mt_sieve2_create(&h, y_last, (uint32_t)NT, 0));
+  DevBuf d_mu, d_m, d_bk, d_run, d_mm;
+  RC(dalloc(d_mu, R)); RC(dalloc(d_m, R * 2)); RC(dalloc(d_bk, (R / MT_BLK) * 8)); RC(dalloc(d_run, 8));
+  RC(dalloc(d_mm, R * 8));
+  MT_CUDA_CHECK(cudaMemset(d_run.p, 0, 8));
+  for (; Y0 <= y2; Y0 += R) {
+    RC(mt_sieve2_run(h, Y0, (uint32_t)NT, d_run.as<int64_t>(), d_mu.as<int8_t>(), d_m.as<int16_t>(),
+                     d_bk.as<int64_t>(), nullptr, nullptr, 0, 0, nullptr));
+    if (Y0 + R - 1 < y1) continue;
+    const u64 a = std::max(Y0, y1), b = std::min(Y0 + R - 1, y2);
+    if (mu_out) MT_CUDA_CHECK(cudaMemcpy(mu_out + (a - y1), d_mu.as<int8_t>() + (a - Y0), b - a + 1, cudaMemcpyDeviceToHost));
+    if (m_out) {
+      k_m16_to_m<<<(unsigned)((R + 255) / 256), 256>>>(d_m.as<int16_t>(), d_bk.as<int64_t>(), R, d_mm.as<int64_t>());
+      MT_CUDA_CHECK(cudaGetLastError());
+      MT_CUDA_CHECK(cudaMemcpy(m_out + (a - y1), d_mm.as<int64_t>() + (a - Y0), (b - a + 1) * 8, cudaMemcpyDeviceToHost));
+    }
+  }
+  MT_CUDA_CHECK(cudaDeviceSynchronize());
+  if (mt_sieve2_overflows(h)) { /* recomputed exactly; reported only */ }
+  return MT_OK;
+}
+
 // ============================================================================
 // backend-protocol: apply_block / finalize / divisor arrays
 // ============================================================================
@@ -574,8 +611,8 @@ struct mt_plan {
   // segments
   u64 Rh = 0, Rt = 0, head_end = 0, head_segs = 0, head_lim = 0, tail_segs = 0, y_last = 0;
   u64 tseg0 = 0, tseg1 = 0;  // this rank's tail segments [tseg0, tseg1)
-  PrimeTable pt;
-  DevBuf d_p, d_rp, d_lg, d_w32, d_big, d_mu, d_m, d_half, d_bk, d_tsum, d_tbase, d_run, d_caps, d_small;
+  Sieve2Host* sv = nullptr;
+  DevBuf d_mu, d_m, d_bk, d_run, d_caps, d_small;
   u64 cap_c_lo = 1, cap_c_hi = 0, cap_small = 0, nsmall = 0;
   UpdateCtx* uc = nullptr;
   KTimer kt;
@@ -586,6 +623,7 @@ struct mt_plan {
   ~mt_plan() {
     if (device >= 0) cudaSetDevice(device);
     mt_update_destroy(uc);
+    mt_sieve2_destroy(sv);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     kt.drain();
     if (own_stream && st) cudaStreamDestroy(st);
@@ -604,30 +642,6 @@ struct mt_plan {
     if (hi > jq1[t]) hi = jq1[t];
     if (lo > hi) return;
     j0 = (u64)lo; j1 = (u64)hi;
-  }
-  SieveSegment make_seg(u64 Y0, u64 R, bool head) {
-    SieveSegment s{};
-    const u64 y2 = Y0 + R - 1;
-    PrimeCut c = prime_cut(pt.p, y2);
-    s.Y0 = Y0; s.R = R; s.y2 = y2;
-    s.big = d_big.as<uint32_t>();
-    s.primes = d_p.as<uint32_t>(); s.rprimes = d_rp.as<double>(); s.logs = d_lg.as<uint8_t>();
-    s.p_large_begin = c.small_end; s.p_large_end = c.large_end; s.do_logs_large = 1;
-    s.running = d_run.as<int64_t>(); s.tile_base = d_tbase.as<int64_t>();
-    s.bk = head ? d_bk.as<int64_t>() : nullptr;
-    SieveTileArgs& a = s.tile;
-    a.Y0 = Y0; a.y2 = y2; a.wheel32x = d_w32.as<uint32_t>(); a.big = s.big;
-    a.primes = s.primes; a.rprimes = s.rprimes; a.logs = s.logs;
-    a.p_first = c.first; a.p_warp_end = c.warp_end; a.p_small_end = c.small_end;
-    a.log_min = 11; a.do_logs = 1;
-    a.tile_sum = d_tsum.as<int>();
-    a.mu_out = head ? d_mu.as<int8_t>() : nullptr;
-    a.m_out = nullptr;
-    a.m16_out = head ? d_m.as<int16_t>() : nullptr;
-    a.half_out = d_half.as<int>();
-    a.states_out = nullptr;
-    a.caps = d_caps.p; a.n_cap = (int)caps.size();
-    return s;
   }
 };
 
@@ -780,11 +794,11 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   if (ntiles) k_tile_meta<<<(unsigned)ntiles, MT_CT, 0, st>>>(NE, P->d_mc.as<u64>(), P->d_vb.as<uint8_t>(), P->d_tmax.as<u64>(), P->d_tbits.as<uint8_t>());
   P->launches++;
 
-  // ---- segments
-  P->Rh = 1ull << (job->seg_log2_head ? job->seg_log2_head : 24);
-  P->Rt = 1ull << (job->seg_log2_tail ? job->seg_log2_tail : 27);
+  // ---- segments (production sieve tiles of 2^17 cells)
+  P->Rh = 1ull << (job->seg_log2_head ? job->seg_log2_head : 26);
+  P->Rt = 1ull << (job->seg_log2_tail ? job->seg_log2_tail : 26);
   const u64 Rh = P->Rh, Rt = P->Rt;
-  if (Rh < MT_TILE || Rt < Rh || (Rt % Rh) || P->Rt > (1ull << 31)) { mt_set_error("bad segment sizes"); return MT_ERR_VALUE; }
+  if (Rh < MT_S2_TILE || Rt < Rh || (Rt % Rh) || Rt > (1ull << 32)) { mt_set_error("bad segment sizes"); return MT_ERR_VALUE; }
   P->head_segs = (head_end + 1 + Rh - 1) / Rh;
   P->head_lim = P->head_segs * Rh;  // first y of the tail
   P->tail_segs = 0;
@@ -792,22 +806,9 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   P->y_last = P->head_lim + P->tail_segs * Rt - 1;
   P->tseg0 = P->tail_segs * P->rank / P->world;
   P->tseg1 = P->tail_segs * (P->rank + 1) / P->world;
-
-  build_primes(std::max<u64>(ceil_sqrt_u128(P->y_last) + 1, 2), P->pt);
-  uint8_t wheel[MT_WHEEL];
-  reference_wheel(wheel);
-  std::vector<uint32_t> w32;
-  build_wheel_words(wheel, w32);
-  const u64 np = P->pt.p.size();
-  RC(dalloc(P->d_p, np * 4)); RC(dalloc(P->d_rp, np * 8)); RC(dalloc(P->d_lg, np));
-  RC(dalloc(P->d_w32, w32.size() * 4));
-  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_p.p, P->pt.p.data(), np * 4, cudaMemcpyHostToDevice, st));
-  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_rp.p, P->pt.r.data(), np * 8, cudaMemcpyHostToDevice, st));
-  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_lg.p, P->pt.lg.data(), np, cudaMemcpyHostToDevice, st));
-  MT_CUDA_CHECK(cudaMemcpyAsync(P->d_w32.p, w32.data(), w32.size() * 4, cudaMemcpyHostToDevice, st));
-  RC(dalloc(P->d_big, Rt)); RC(dalloc(P->d_mu, Rh)); RC(dalloc(P->d_m, Rh * 2));
-  RC(dalloc(P->d_half, (Rt / MT_TILE) * 4)); RC(dalloc(P->d_bk, (Rh / MT_BLK) * 8 + 8));
-  RC(dalloc(P->d_tsum, (Rt / MT_TILE) * 4)); RC(dalloc(P->d_tbase, (Rt / MT_TILE) * 8)); RC(dalloc(P->d_run, 8));
+  RC(mt_sieve2_create(&P->sv, P->y_last, (uint32_t)(Rt / MT_S2_TILE), st));
+  RC(dalloc(P->d_mu, Rh)); RC(dalloc(P->d_m, Rh * 2)); RC(dalloc(P->d_bk, (Rh / MT_BLK) * 8 + 8));
+  RC(dalloc(P->d_run, 8));
   RC(dalloc(P->d_caps, P->caps.size() * sizeof(CaptureTargetH)));
   if (!P->caps.empty())
     MT_CUDA_CHECK(cudaMemcpyAsync(P->d_caps.p, P->caps.data(), P->caps.size() * sizeof(CaptureTargetH), cudaMemcpyHostToDevice, st));
@@ -851,9 +852,10 @@ extern "C" int mt_plan_sieve_update(mt_plan* P, int64_t* m_head, int64_t* tail_t
   MT_CUDA_CHECK(cudaEventRecord(P->ev[0], st));
   for (u64 s = 0; s < P->head_segs; s++) {
     const u64 Y0 = s * P->Rh;
-    SieveSegment sg = P->make_seg(Y0, P->Rh, true);
-    RC(mt_launch_sieve_segment(sg, st, &P->kt));
-    P->launches += 6;
+    RC(mt_sieve2_run(P->sv, Y0, (uint32_t)(P->Rh / MT_S2_TILE), P->d_run.as<int64_t>(), P->d_mu.as<int8_t>(),
+                     P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), nullptr,
+                     (const CaptureTarget2*)P->d_caps.p, (int)P->caps.size(), st, &P->kt));
+    P->launches += 2;
     RC(mt_update_head_segment(P->uc, Y0, P->Rh, P->d_mu.as<int8_t>(), P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), st));
     if (P->nsmall && Y0 <= P->cap_small) {
       k_copy_small<<<(unsigned)((P->Rh + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, P->Rh, P->cap_small, P->d_small.as<int64_t>());
@@ -865,9 +867,10 @@ extern "C" int mt_plan_sieve_update(mt_plan* P, int64_t* m_head, int64_t* tail_t
   MT_CUDA_CHECK(cudaMemsetAsync(P->d_run.p, 0, 8, st));  // tail prefixes are rank-local
   MT_CUDA_CHECK(cudaEventRecord(P->ev[1], st));
   for (u64 s = P->tseg0; s < P->tseg1; s++) {
-    SieveSegment sg = P->make_seg(P->tail_y0(s), P->Rt, false);
-    RC(mt_launch_sieve_segment(sg, st, &P->kt));
-    P->launches += 5;
+    RC(mt_sieve2_run(P->sv, P->tail_y0(s), (uint32_t)(P->Rt / MT_S2_TILE), P->d_run.as<int64_t>(), nullptr,
+                     nullptr, nullptr, nullptr, (const CaptureTarget2*)P->d_caps.p, (int)P->caps.size(), st,
+                     &P->kt));
+    P->launches += 2;
   }
   MT_CUDA_CHECK(cudaMemcpyAsync(&tt, P->d_run.p, 8, cudaMemcpyDeviceToHost, st));
   MT_CUDA_CHECK(cudaEventRecord(P->ev[2], st));

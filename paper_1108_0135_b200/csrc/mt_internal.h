@@ -105,6 +105,71 @@ struct KTimer {
 
 int mt_launch_sieve_segment(const SieveSegment& s, cudaStream_t st, KTimer* kt = nullptr);
 
+// ---- production sieve (mt_sieve2.cu)
+struct CaptureTarget2 {  // one exact target n for quotient captures (same layout as CaptureTarget)
+  uint64_t n_lo, n_hi;
+  double nd;
+  int nbits;
+  uint64_t jq0, jq1;  // capture j in [jq0, jq1]
+  int* Q;             // Q[j - jq0] = M(floor(n/j))
+};
+
+struct Bucket2Args {
+  uint64_t Y0;
+  uint32_t ntiles, cap, nprod_grid;
+  const uint32_t* primes;
+  const double* rprimes;
+  const uint8_t* logs;
+  uint32_t p_lo, p_hi;   // log marks of primes [p_lo, p_hi)  (p > 2^17)
+  uint32_t q_lo, q_hi;   // square flags of primes [q_lo, q_hi) (p^2 > 2^17)
+  uint32_t* buf;         // [nprod][ntiles][cap]
+  uint32_t* counts;      // [nprod][ntiles]
+};
+
+struct Sieve2Args {
+  uint64_t Y0;
+  uint32_t ntiles;
+  uint32_t* ticket;                 // tile order (zeroed per launch)
+  unsigned long long* tstate;       // look-back words [ntiles] (zeroed per launch)
+  int64_t* running;                 // M(Y0 - 1) in, M(Y0 + R - 1) out
+  const uint32_t *w1, *w2, *w3;     // presieve patterns (words)
+  uint64_t w1_period4, w2_period4, w3_period4;
+  const uint32_t* primes;
+  const double* rprimes;
+  const uint8_t* logs;
+  uint32_t p_first, p_warp_end, p_small_end;  // in-tile log primes
+  uint32_t sq_first, sq_end;                  // in-tile squares
+  uint32_t nprod, cap;                        // bucket lists (nprod = 0: none)
+  const uint32_t* counts;
+  const uint32_t* buf;
+  uint32_t p_lo, p_hi, q_lo, q_hi;            // bucket producers' prime ranges (overflow path)
+  unsigned long long* overflow;
+  uint8_t* states_out;                        // debug: raw states
+  int8_t* mu_out;                             // head: mu
+  int16_t* m16_out;                           // head: M(y) - M(32K block start - 1)
+  int64_t* bk;                                // head: M(32K block start - 1)
+  int* tile_sum;                              // optional
+  const CaptureTarget2* caps;
+  int n_cap;
+};
+
+struct Sieve2Segment {
+  Bucket2Args bucket;
+  Sieve2Args tile;
+};
+int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt);
+
+// host-side context of the production sieve: patterns, primes, bucket space
+struct Sieve2Host;
+int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cudaStream_t st);
+void mt_sieve2_destroy(Sieve2Host* h);
+// one segment [Y0, Y0 + ntiles*2^17): outputs as requested (null = skip)
+int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running, int8_t* mu_out,
+                  int16_t* m16_out, int64_t* bk, uint8_t* states_out, const CaptureTarget2* caps,
+                  int n_cap, cudaStream_t st, KTimer* kt);
+uint64_t mt_sieve2_overflows(Sieve2Host* h);
+#define MT_S2_TILE (1u << 17)
+
 // element arrays (device, SoA), one entry per harmonic-array element of every target
 struct ElemDev {
   const double* vd;      // double(v)

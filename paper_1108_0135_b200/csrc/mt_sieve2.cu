@@ -1,0 +1,623 @@
+// Production segmented Moebius sieve on sm_100a (the engine's head and tail).
+//
+// Replaces the CPU log-prime sieve the paper kept on the host (PAPER.md:87-115,
+// reference sieve.py:189-213 / _native.pyx:71-160).  mu(y) is decided by the
+// reference's rule (_native.pyx:143-159): with s = sum of l_p = ceil(log2 p)|1
+// over the primes p <= sqrt(y2) dividing y (0x80 if some p^2 | y),
+//   mu = 0 if s & 0x80, else (s > floor(log2 y) - 1 ? 1 - 2(s&1) : 2(s&1) - 1).
+// Marking more primes than the reference (the presieve patterns below include
+// 11..41 for every y) only moves y into the exact "fully factored" branch, so
+// mu is unchanged; raw states are NOT the reference's and the
+// instrumented logprime_states op keeps the reference kernel (mt_sieve.cu).
+//
+// Layout:
+//   tile     = 2^17 cells (one byte each, 128 KB of shared memory, 1 CTA/SM,
+//              1024 threads); tiles are 2^17-aligned, so every tile but the
+//              first lies in one binade and shares one classification threshold
+//   presieve = three L2-resident byte patterns added word-wise on load:
+//              W1 (2,3,5,7 logs; 0x80 at 4,9,25,49; period 485100),
+//              W2 (11,13,17,19,23; period 1062347), W3 (29,31,37,41; 1363783)
+//   in-tile  = primes 43 <= p <= 2^17 (warp per prime below 1024, thread per
+//              prime above) and squares p^2 for 11 <= p <= 362 (shared-memory
+//              byte adds / ORs on 32-bit words)
+//   buckets  = primes p > 2^17 and squares p^2 > 2^17: a producer kernel per
+//              segment enumerates every hit and appends (offset, value) to a
+//              producer-private list per tile (shared-memory cursors, no global
+//              atomics); the tile kernel applies its lists.  A list that would
+//              overflow its capacity is recomputed exactly by the tile (slow path)
+//   classify = SIMD within a word (4 cells), warp-parallel over words; 32-cell
+//              chunk sums -> block scan -> tile total
+//   scan     = decoupled look-back across the tiles of a launch (tile order from
+//              an atomic ticket), seeded with the running M before the segment,
+//              so captures M(floor(n/j)) are written absolute in the same pass
+#include <cstdio>
+
+#include "mt_common.cuh"
+#include "mt_internal.h"
+
+#define S2_T (1u << 17)          // cells per tile
+#define S2_W (S2_T / 4)          // words per tile
+#define S2_NT 1024               // threads per tile CTA
+#define S2_CH (S2_T / 32)        // 32-cell chunks per tile
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// look-back word: status in bits 62-63 (1 = aggregate, 2 = inclusive prefix), value in 0..61
+#define LB_AGG 1ull
+#define LB_INC 2ull
+__device__ __forceinline__ unsigned long long lb_pack(unsigned long long st, long long v) {
+  return (st << 62) | ((unsigned long long)v & ((1ull << 62) - 1));
+}
+__device__ __forceinline__ long long lb_val(unsigned long long w) {
+  return ((long long)(w << 2)) >> 2;
+}
+
+// (-Y) mod p for p < 2^32, Y < 2^53, with r = 1/p rounded (host: 1.0/p)
+__device__ __forceinline__ u32 neg_mod(u64 Y, double Yd, double r, u32 p) {
+  u64 q = qdiv64(Yd, r, Y, p);
+  u32 rem = (u32)(Y - q * p);
+  return rem ? p - rem : 0u;
+}
+
+// ----------------------------------------------------------------------------
+// bucket producer: every hit of a prime p > S2_T (log marks) and of p^2 > S2_T
+// (square flags) in the segment [Y0, Y0 + R), appended to the producer-private
+// list of its tile.  Entry = offset (17 bits) | value << 17 (value bit 7 = OR).
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_bucket_fill(Bucket2Args a) {
+  extern __shared__ u32 cnt[];  // [ntiles]
+  const int tid = threadIdx.x;
+  const u32 b = blockIdx.x, NP = gridDim.x;
+  for (u32 t = tid; t < a.ntiles; t += blockDim.x) cnt[t] = 0;
+  __syncthreads();
+  const u64 Y0 = a.Y0, R = (u64)a.ntiles * S2_T;
+  const double Yd = (double)Y0;
+  u32* __restrict__ out = a.buf + (u64)b * a.ntiles * a.cap;
+  // log marks of large primes: indices p_lo + b + k*NP
+  for (u64 i = (u64)a.p_lo + b + (u64)tid * NP; i < a.p_hi; i += (u64)blockDim.x * NP) {
+    const u32 p = a.primes[i];
+    const u32 lg = a.logs[i];
+    u64 pos = neg_mod(Y0, Yd, a.rprimes[i], p);
+    if (Y0 == 0 && pos == 0) pos = p;  // y = 0 is never marked
+    for (; pos < R; pos += p) {
+      const u32 t = (u32)(pos >> 17);
+      const u32 s = atomicAdd(&cnt[t], 1u);
+      if (s < a.cap) out[(u64)t * a.cap + s] = (u32)(pos & (S2_T - 1)) | (lg << 17);
+    }
+  }
+  // square flags of p^2 > S2_T: indices q_lo + b + k*NP
+  for (u64 i = (u64)a.q_lo + b + (u64)tid * NP; i < a.q_hi; i += (u64)blockDim.x * NP) {
+    const u64 p = a.primes[i];
+    const u64 q = p * p;
+    u64 qq = qdiv64(Yd, __drcp_rn((double)q), Y0, q);
+    u64 rem = Y0 - qq * q;
+    u64 pos = rem ? q - rem : (Y0 ? 0 : q);
+    for (; pos < R; pos += q) {
+      const u32 t = (u32)(pos >> 17);
+      const u32 s = atomicAdd(&cnt[t], 1u);
+      if (s < a.cap) out[(u64)t * a.cap + s] = (u32)(pos & (S2_T - 1)) | (0x80u << 17);
+    }
+  }
+  __syncthreads();
+  for (u32 t = tid; t < a.ntiles; t += blockDim.x) a.counts[(u64)b * a.ntiles + t] = cnt[t];
+}
+
+// ----------------------------------------------------------------------------
+// tile kernel
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void mark_add(u32* st, u32 j, u32 v) { atomicAdd(&st[j >> 2], v << ((j & 3) * 8)); }
+__device__ __forceinline__ void mark_or(u32* st, u32 j) { atomicOr(&st[j >> 2], 0x80u << ((j & 3) * 8)); }
+
+// mu of the 4 cells of a state word (uniform threshold thr): packed int8 and their sum
+__device__ __forceinline__ u32 mu_word(u32 w, u32 kthr, int& sum) {
+  const u32 nsq = ~w & 0x80808080u;                              // not square-flagged
+  const u32 g = ((w & 0x7f7f7f7fu) + kthr) & 0x80808080u;        // s > thr
+  const u32 x = g ^ ((w & 0x01010101u) << 7);                    // mu = +1 iff (s > thr) xor odd
+  const u32 pl = x & nsq, mi = ~x & nsq;
+  sum += __popc(pl) - __popc(mi);
+  const u32 p1 = pl >> 7, m1 = mi >> 7;
+  return p1 | (m1 * 255u);
+}
+
+__device__ __forceinline__ int mu_cell(u32 s, int thr) {
+  if (s & 0x80) return 0;
+  int par = s & 1;
+  return ((int)s > thr) ? 1 - 2 * par : 2 * par - 1;
+}
+
+__global__ void __launch_bounds__(S2_NT, 1) k_sieve2(Sieve2Args a) {
+  extern __shared__ u32 st[];                   // S2_W state / mu words
+  int* csum = (int*)(st + S2_W);                // S2_CH chunk sums -> exclusive chunk prefixes
+  __shared__ int wsum[32];
+  __shared__ u32 s_tile;
+  __shared__ long long s_excl;
+  __shared__ int s_total;
+  __shared__ u32 s_queue;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  if (tid == 0) { s_tile = atomicAdd(a.ticket, 1u); s_queue = 0; }
+  __syncthreads();
+  const u32 tile = s_tile;
+  const u64 Yt = a.Y0 + (u64)tile * S2_T;
+  const double Yd = (double)Yt;
+
+  // 1. presieve patterns
+  {
+    const u32* __restrict__ w1 = a.w1 + (u32)((Yt % a.w1_period4) >> 2);
+    const u32* __restrict__ w2 = a.w2 + (u32)((Yt % a.w2_period4) >> 2);
+    const u32* __restrict__ w3 = a.w3 + (u32)((Yt % a.w3_period4) >> 2);
+    for (int i = tid; i < (int)S2_W; i += S2_NT) st[i] = w1[i] + w2[i] + w3[i];
+  }
+  __syncthreads();
+
+  // 2.+3. marks, dealt to warps from a shared work queue (largest items first):
+  //   A  warp per prime, 43 <= p < 1024 (>= 128 multiples per tile)
+  //   B  32 consecutive primes 1024 <= p <= 2^17, lane per prime
+  //   C  warp per square p^2, 11 <= p <= 362
+  //   D  warp per bucket list (primes > 2^17, squares > 2^17)
+  {
+    const u32 nA = a.p_warp_end - a.p_first;
+    const u32 nB = (a.p_small_end - a.p_warp_end + 31) / 32;
+    const u32 nC = a.sq_end - a.sq_first;
+    const u32 nD = a.nprod;
+    const u32 total = nA + nB + nC + nD;
+    for (;;) {
+      u32 it = 0;
+      if (lane == 0) it = atomicAdd(&s_queue, 1u);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= total) break;
+      if (it < nA) {
+        const u32 i = a.p_first + it;
+        const u32 p = a.primes[i];
+        const u32 lg = a.logs[i];
+        u32 j0 = neg_mod(Yt, Yd, a.rprimes[i], p);
+        if (Yt == 0 && j0 == 0) j0 = p;
+        // step 32p keeps the byte lane: one shifted value, word index += 8p
+        const u32 j = j0 + lane * p;
+        const u32 v = lg << ((j & 3) * 8);
+        const u32 wstep = 8 * p;
+#pragma unroll 4
+        for (u32 w = j >> 2; w < S2_W; w += wstep) atomicAdd(&st[w], v);
+        continue;
+      }
+      it -= nA;
+      if (it < nB) {
+        const u32 i = a.p_warp_end + it * 32 + lane;
+        if (i < a.p_small_end) {
+          const u32 p = a.primes[i];
+          const u32 lg = a.logs[i];
+          u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
+          if (Yt == 0 && j == 0) j = p;
+          // four consecutive multiples cycle through the four byte lanes (p odd):
+          // their shifted values are loop-invariant and each word index steps by p
+          const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p;
+          const u32 v0 = lg << ((j & 3) * 8), v1 = lg << ((j1 & 3) * 8);
+          const u32 v2 = lg << ((j2 & 3) * 8), v3 = lg << ((j3 & 3) * 8);
+          u32 w0 = j >> 2, w1 = j1 >> 2, w2 = j2 >> 2, w3 = j3 >> 2;
+          for (; w3 < S2_W; w0 += p, w1 += p, w2 += p, w3 += p) {
+            atomicAdd(&st[w0], v0);
+            atomicAdd(&st[w1], v1);
+            atomicAdd(&st[w2], v2);
+            atomicAdd(&st[w3], v3);
+          }
+          if (w0 < S2_W) atomicAdd(&st[w0], v0);
+          if (w1 < S2_W) atomicAdd(&st[w1], v1);
+          if (w2 < S2_W) atomicAdd(&st[w2], v2);
+        }
+        __syncwarp();
+        continue;
+      }
+      it -= nB;
+      if (it < nC) {
+        const u32 i = a.sq_first + it;
+        const u32 p = a.primes[i];
+        const u32 q = p * p;
+        u32 j0 = neg_mod(Yt, Yd, __drcp_rn((double)q), q);
+        if (Yt == 0 && j0 == 0) j0 = q;
+        for (u32 j = j0 + lane * q; j < S2_T; j += 32 * q) mark_or(st, j);
+        continue;
+      }
+      const u32 b = it - nC;
+      const u32 n = a.counts[(u64)b * a.ntiles + tile];
+      const u32 m = n <= a.cap ? n : 0;  // an overflowed list is recomputed below instead
+      const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
+      for (u32 k = lane; k < m; k += 32) {
+        const u32 e = L[k];
+        const u32 j = e & (S2_T - 1), v = e >> 17;
+        if (v & 0x80u) mark_or(st, j); else mark_add(st, j, v);
+      }
+      if (n > a.cap) {  // overflowed list: this producer's hits on the tile, recomputed exactly
+        if (lane == 0) atomicAdd(a.overflow, 1ull);
+        for (u64 i = (u64)a.p_lo + b + (u64)lane * a.nprod; i < a.p_hi; i += 32ull * a.nprod) {
+          const u32 p = a.primes[i];
+          const u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
+          if (j < S2_T && !(Yt == 0 && j == 0)) mark_add(st, j, a.logs[i]);
+        }
+        for (u64 i = (u64)a.q_lo + b + (u64)lane * a.nprod; i < a.q_hi; i += 32ull * a.nprod) {
+          const u64 p = a.primes[i];
+          const u64 q = p * p;
+          const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Yt, q);
+          const u64 rem = Yt - qq * q;
+          const u64 j = rem ? q - rem : (Yt ? 0 : q);
+          if (j < S2_T) mark_or(st, (u32)j);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+
+  if (a.states_out) {  // instrumented export (debug)
+    u32* so = (u32*)(a.states_out + (u64)tile * S2_T);
+    for (int i = tid; i < (int)S2_W; i += S2_NT) so[i] = st[i];
+    __syncthreads();
+  }
+
+  // 4. classify: warp w owns words [w*1024, (w+1)*1024); per iteration lane l
+  //    takes the 4 words base + 4l .. 4l+3 (16 cells, half a 32-cell chunk)
+  {
+    const bool uniform = Yt >= S2_T;
+    const int thr_t = 62 - __clzll((long long)(Yt | 1));  // floor(log2 Yt) - 1
+    const u32 kthr = uniform ? (u32)(127 - thr_t) * 0x01010101u : 0u;
+    uint4* st4 = (uint4*)st;
+#pragma unroll 2
+    for (int it = 0; it < 8; it++) {
+      const int q = warp * 256 + it * 32 + lane;  // uint4 index
+      uint4 w = st4[q];
+      int s = 0;
+      if (uniform) {
+        w.x = mu_word(w.x, kthr, s);
+        w.y = mu_word(w.y, kthr, s);
+        w.z = mu_word(w.z, kthr, s);
+        w.w = mu_word(w.w, kthr, s);
+      } else {
+        u32* wv = (u32*)&w;
+        for (int k = 0; k < 4; k++) {
+          u32 mw = 0;
+          for (int bb = 0; bb < 4; bb++) {
+            const u64 y = Yt + (u64)(q * 4 + k) * 4 + bb;
+            const int thr = (y ? 63 - __clzll((long long)y) : 0) - 1;
+            const int m = mu_cell((wv[k] >> (8 * bb)) & 0xff, thr);
+            s += m;
+            mw |= ((u32)(m & 0xff)) << (8 * bb);
+          }
+          wv[k] = mw;
+        }
+      }
+      st4[q] = w;
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      if (!(lane & 1)) csum[q >> 1] = s;
+    }
+  }
+  __syncthreads();
+  // 5. block exclusive scan of the S2_CH = 4096 chunk sums (4 per thread)
+  {
+    int v0 = csum[tid * 4], v1 = csum[tid * 4 + 1], v2 = csum[tid * 4 + 2], v3 = csum[tid * 4 + 3];
+    int tsum = v0 + v1 + v2 + v3;
+    int incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int x = wsum[lane], ix = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, ix, o);
+        if (lane >= o) ix += t;
+      }
+      wsum[lane] = ix - x;
+      if (lane == 31) s_total = ix;
+    }
+    __syncthreads();
+    int e = wsum[warp] + incl - tsum;
+    csum[tid * 4] = e;
+    csum[tid * 4 + 1] = e + v0;
+    csum[tid * 4 + 2] = e + v0 + v1;
+    csum[tid * 4 + 3] = e + v0 + v1 + v2;
+  }
+  __syncthreads();
+
+  // 6. decoupled look-back: absolute M(Yt - 1)
+  if (warp == 0) {
+    const int total = s_total;
+    unsigned long long* ts = a.tstate;
+    long long excl = 0;
+    if (tile == 0) {
+      excl = *a.running;
+      if (lane == 0) st_release(&ts[0], lb_pack(LB_INC, excl + total));
+    } else {
+      if (lane == 0) st_release(&ts[tile], lb_pack(LB_AGG, total));
+      long long acc = 0;
+      long long look = (long long)tile - 1;
+      for (;;) {
+        const long long idx = look - lane;
+        unsigned long long w = idx >= 0 ? ld_acquire(&ts[idx]) : lb_pack(LB_INC, 0);
+        unsigned long long stt = w >> 62;
+        // wait until every lane's predecessor has published something
+        if (__any_sync(0xffffffffu, stt == 0)) continue;
+        const unsigned inc_mask = __ballot_sync(0xffffffffu, stt == LB_INC);
+        const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;  // nearest inclusive
+        long long v = (lane <= first_inc) ? lb_val(w) : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        acc += v;
+        if (inc_mask) break;
+        look -= 32;
+      }
+      excl = acc;
+      if (lane == 0) st_release(&ts[tile], lb_pack(LB_INC, excl + total));
+    }
+    if (lane == 0) {
+      s_excl = excl;
+      if (tile == a.ntiles - 1) *a.running = excl + total;
+      if (a.tile_sum) a.tile_sum[tile] = total;
+    }
+  }
+  __syncthreads();
+  const long long E = s_excl;
+
+  // 7. head outputs: mu bytes, M16 relative to each 32K block, block bases
+  if (a.mu_out) {
+    u32* mo = (u32*)(a.mu_out + (u64)tile * S2_T);
+    for (int i = tid; i < (int)S2_W; i += S2_NT) mo[i] = st[i];
+  }
+  if (a.m16_out) {
+    if (tid < 4) a.bk[(u64)tile * 4 + tid] = E + csum[tid * 1024];  // chunk 1024*q starts block q
+    // thread per chunk (4 chunks per thread): prefix within the chunk
+    int16_t* m16 = a.m16_out + (u64)tile * S2_T;
+    for (int c = tid; c < (int)S2_CH; c += S2_NT) {
+      const int bstart = csum[(c >> 10) << 10];
+      int run = csum[c] - bstart;
+      const u32* wp = st + c * 8;
+      uint4 o[4];
+      u32* ov = (u32*)o;
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const u32 w = wp[k];
+        const int c0 = run + (int)(int8_t)(w & 0xff);
+        const int c1 = c0 + (int)(int8_t)((w >> 8) & 0xff);
+        const int c2 = c1 + (int)(int8_t)((w >> 16) & 0xff);
+        const int c3 = c2 + (int)(int8_t)(w >> 24);
+        ov[2 * k] = (u32)(uint16_t)c0 | ((u32)(uint16_t)c1 << 16);
+        ov[2 * k + 1] = (u32)(uint16_t)c2 | ((u32)(uint16_t)c3 << 16);
+        run = c3;
+      }
+      uint4* dst = (uint4*)(m16 + (u64)c * 32);
+#pragma unroll
+      for (int k = 0; k < 4; k++) dst[k] = o[k];
+    }
+  }
+
+  // 8. quotient captures Q_t[j] = M(floor(n_t / j)) for floor(n_t/j) in this tile
+  for (int t = 0; t < a.n_cap; t++) {
+    const CaptureTarget2& ct = a.caps[t];
+    u64 jhi = Yt ? udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt) : ~0ull;
+    u64 jlo = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt + S2_T) + 1;
+    if (jlo < ct.jq0) jlo = ct.jq0;
+    if (jhi > ct.jq1) jhi = ct.jq1;
+    for (u64 j = jlo + tid; j <= jhi; j += S2_NT) {
+      const u64 y = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, j);
+      const u32 o = (u32)(y - Yt);
+      const int c = o >> 5;
+      const u32* wp = st + (c << 3);
+      int s = 0;
+      const u32 last = o & 31;
+      for (u32 k = 0; k <= (last >> 2); k++) {
+        u32 w = wp[k];
+        if (k == (last >> 2)) {
+          const u32 keep = (last & 3) + 1;
+          w = keep == 4 ? w : (w & ((1u << (8 * keep)) - 1));
+        }
+        s = __dp4a((int)w, 0x01010101, s);
+      }
+      ct.Q[j - ct.jq0] = (int)(E + csum[c] + s);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
+  const size_t smem = S2_T + S2_CH * sizeof(int);
+  Sieve2Args a = g.tile;
+  if (a.nprod) {
+    Bucket2Args b = g.bucket;
+    const size_t bs = (size_t)b.ntiles * sizeof(u32);
+    if (kt) kt->begin(KT_SIEVE_LARGE, st);
+    k_bucket_fill<<<b.nprod_grid, 512, bs, st>>>(b);
+    if (kt) kt->end(st);
+    MT_CUDA_CHECK(cudaGetLastError());
+  }
+  MT_CUDA_CHECK(cudaMemsetAsync(a.tstate, 0, sizeof(unsigned long long) * a.ntiles + sizeof(u32), st));
+  if (kt) kt->begin(KT_SIEVE_TILE, st);
+  k_sieve2<<<a.ntiles, S2_NT, smem, st>>>(a);
+  if (kt) kt->end(st);
+  MT_CUDA_CHECK(cudaGetLastError());
+  return MT_OK;
+}
+
+// ============================================================================
+// host context
+// ============================================================================
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+namespace {
+struct Buf {
+  void* p = nullptr;
+  ~Buf() { if (p) cudaFree(p); }
+};
+int balloc(Buf& b, size_t n) {
+  if (!n) n = 16;
+  cudaError_t e = cudaMalloc(&b.p, n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    mt_set_error("device allocation of %zu bytes failed: %s", n, cudaGetErrorString(e));
+    return MT_ERR_RESOURCE;
+  }
+  return MT_OK;
+}
+u64 isqrt64(u64 x) {
+  u64 s = (u64)std::sqrt((long double)x);
+  while (s * s > x) s--;
+  while ((s + 1) * (s + 1) <= x) s++;
+  return s;
+}
+uint8_t logp(u64 p) {  // ceil(log2 p) | 1  (sieve.py:111-121)
+  int bl = 0;
+  for (u64 x = p - 1; x; x >>= 1) bl++;
+  return (uint8_t)(bl | 1);
+}
+// byte pattern of period P replicated over 4P + T bytes, as words
+std::vector<uint32_t> pattern_words(u64 P, const std::vector<u32>& logp_primes, const std::vector<u32>& sq) {
+  std::vector<uint8_t> one(P, 0);
+  for (u32 p : logp_primes)
+    for (u64 j = 0; j < P; j += p) one[j] = (uint8_t)(one[j] + logp(p));
+  for (u32 q : sq)
+    for (u64 j = 0; j < P; j += q) one[j] |= 0x80;
+  const u64 nbytes = 4 * P + S2_T;
+  std::vector<uint32_t> w(nbytes / 4);
+  for (u64 i = 0; i < nbytes / 4; i++) {
+    u32 v = 0;
+    for (int b = 0; b < 4; b++) v |= (u32)one[(4 * i + b) % P] << (8 * b);
+    w[i] = v;
+  }
+  return w;
+}
+}  // namespace
+
+struct Sieve2Host {
+  Buf w1, w2, w3, prm, rp, lg, buf, counts, tstate, ovf;
+  u64 P1 = 485100, P2 = 1062347, P3 = 1363783;
+  std::vector<u32> p;
+  u32 nprod = 0, cap = 0, max_tiles = 0;
+  uint64_t overflows_host = 0;
+};
+
+int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cudaStream_t st) {
+  Sieve2Host* h = new Sieve2Host();
+  *out = h;
+  h->max_tiles = max_tiles;
+  // primes up to ceil(sqrt(y_last)) + 1
+  const u64 lim = isqrt64(y_last) + 2;
+  {
+    std::vector<uint8_t> f(lim + 1, 1);
+    f[0] = 0;
+    if (lim >= 1) f[1] = 0;
+    for (u64 i = 2; i * i <= lim; i++)
+      if (f[i]) for (u64 j = i * i; j <= lim; j += i) f[j] = 0;
+    for (u64 i = 2; i <= lim; i++) if (f[i]) h->p.push_back((u32)i);
+  }
+  const size_t np = h->p.size();
+  std::vector<double> r(np);
+  std::vector<uint8_t> l(np);
+  for (size_t i = 0; i < np; i++) { r[i] = 1.0 / (double)h->p[i]; l[i] = logp(h->p[i]); }
+  if (balloc(h->prm, np * 4) || balloc(h->rp, np * 8) || balloc(h->lg, np)) return MT_ERR_RESOURCE;
+  MT_CUDA_CHECK(cudaMemcpyAsync(h->prm.p, h->p.data(), np * 4, cudaMemcpyHostToDevice, st));
+  MT_CUDA_CHECK(cudaMemcpyAsync(h->rp.p, r.data(), np * 8, cudaMemcpyHostToDevice, st));
+  MT_CUDA_CHECK(cudaMemcpyAsync(h->lg.p, l.data(), np, cudaMemcpyHostToDevice, st));
+  // presieve patterns
+  auto up = [&](Buf& b, const std::vector<uint32_t>& w) -> int {
+    if (balloc(b, w.size() * 4)) return MT_ERR_RESOURCE;
+    MT_CUDA_CHECK(cudaMemcpyAsync(b.p, w.data(), w.size() * 4, cudaMemcpyHostToDevice, st));
+    MT_CUDA_CHECK(cudaStreamSynchronize(st));  // the host vector dies at return
+    return MT_OK;
+  };
+  if (up(h->w1, pattern_words(h->P1, {2, 3, 5, 7}, {4, 9, 25, 49}))) return MT_ERR_RESOURCE;
+  if (up(h->w2, pattern_words(h->P2, {11, 13, 17, 19, 23}, {}))) return MT_ERR_RESOURCE;
+  if (up(h->w3, pattern_words(h->P3, {29, 31, 37, 41}, {}))) return MT_ERR_RESOURCE;
+  // bucket space: producers = SMs; capacity from the expected hits per (producer, tile)
+  int dev, nsm;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  double e = 0;
+  for (size_t i = 0; i < np; i++) {
+    const double pp = h->p[i];
+    if (pp > S2_T) e += S2_T / pp;
+    if (pp > 362 && pp * pp <= (double)y_last * 1.0001) e += S2_T / (pp * pp);
+  }
+  const bool any = np && (h->p.back() > S2_T || (double)h->p.back() > 362.0);
+  if (any && e > 0) {
+    h->nprod = (u32)nsm;
+    const double m = e / h->nprod;
+    h->cap = (u32)std::ceil(m + 8.0 * std::sqrt(m) + 32.0);
+    h->cap = (h->cap + 31) & ~31u;
+    if (balloc(h->buf, (size_t)h->nprod * max_tiles * h->cap * 4) ||
+        balloc(h->counts, (size_t)h->nprod * max_tiles * 4))
+      return MT_ERR_RESOURCE;
+  }
+  if (balloc(h->tstate, ((size_t)max_tiles + 1) * 8) || balloc(h->ovf, 8)) return MT_ERR_RESOURCE;
+  MT_CUDA_CHECK(cudaMemsetAsync(h->ovf.p, 0, 8, st));
+  static bool attr = false;
+  if (!attr) {
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(S2_T + S2_CH * sizeof(int))));
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(max_tiles * 4)));
+    attr = true;
+  }
+  if (max_tiles * 4 > 200 * 1024) { mt_set_error("too many tiles per segment"); return MT_ERR_VALUE; }
+  MT_CUDA_CHECK(cudaStreamSynchronize(st));
+  return MT_OK;
+}
+
+void mt_sieve2_destroy(Sieve2Host* h) { delete h; }
+
+uint64_t mt_sieve2_overflows(Sieve2Host* h) {
+  unsigned long long v = 0;
+  cudaMemcpy(&v, h->ovf.p, 8, cudaMemcpyDeviceToHost);
+  return v;
+}
+
+int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running, int8_t* mu_out,
+                  int16_t* m16_out, int64_t* bk, uint8_t* states_out, const CaptureTarget2* caps,
+                  int n_cap, cudaStream_t st, KTimer* kt) {
+  if (ntiles == 0) return MT_OK;
+  if (ntiles > h->max_tiles || (Y0 % S2_T)) { mt_set_error("bad sieve segment"); return MT_ERR_VALUE; }
+  const u64 y2 = Y0 + (u64)ntiles * S2_T - 1;
+  const std::vector<u32>& p = h->p;
+  const u64 s = isqrt64(y2);  // p <= floor(sqrt(y2))  <=>  p*p <= y2
+  auto idx_gt = [&](u64 v) { return (u32)(std::upper_bound(p.begin(), p.end(), (u32)std::min<u64>(v, 0xFFFFFFFFull)) - p.begin()); };
+  const u32 end = idx_gt(s);
+  Sieve2Segment g{};
+  Sieve2Args& a = g.tile;
+  a.Y0 = Y0;
+  a.ntiles = ntiles;
+  a.tstate = (unsigned long long*)h->tstate.p;
+  a.ticket = (uint32_t*)((unsigned long long*)h->tstate.p + ntiles);
+  a.running = running;
+  a.w1 = (const u32*)h->w1.p; a.w2 = (const u32*)h->w2.p; a.w3 = (const u32*)h->w3.p;
+  a.w1_period4 = 4 * h->P1; a.w2_period4 = 4 * h->P2; a.w3_period4 = 4 * h->P3;
+  a.primes = (const u32*)h->prm.p; a.rprimes = (const double*)h->rp.p; a.logs = (const uint8_t*)h->lg.p;
+  a.p_first = std::min(idx_gt(42), end);
+  a.p_warp_end = std::max(a.p_first, std::min(idx_gt(1023), end));
+  a.p_small_end = std::max(a.p_warp_end, std::min(idx_gt(S2_T), end));
+  a.sq_first = std::min(idx_gt(10), end);
+  a.sq_end = std::max(a.sq_first, std::min(idx_gt(362), end));
+  a.p_lo = a.p_small_end; a.p_hi = end;
+  a.q_lo = std::max(a.sq_end, std::min(idx_gt(362), end)); a.q_hi = end;
+  a.nprod = (h->nprod && (a.p_hi > a.p_lo || a.q_hi > a.q_lo)) ? h->nprod : 0;
+  a.cap = h->cap;
+  a.counts = (const u32*)h->counts.p; a.buf = (const u32*)h->buf.p;
+  a.overflow = (unsigned long long*)h->ovf.p;
+  a.states_out = states_out; a.mu_out = mu_out; a.m16_out = m16_out; a.bk = bk;
+  a.tile_sum = nullptr;
+  a.caps = caps; a.n_cap = n_cap;
+  Bucket2Args& b = g.bucket;
+  b.Y0 = Y0; b.ntiles = ntiles; b.cap = h->cap; b.nprod_grid = a.nprod;
+  b.primes = a.primes; b.rprimes = a.rprimes; b.logs = a.logs;
+  b.p_lo = a.p_lo; b.p_hi = a.p_hi; b.q_lo = a.q_lo; b.q_hi = a.q_hi;
+  b.buf = (u32*)h->buf.p; b.counts = (u32*)h->counts.p;
+  return mt_sieve2_segment(g, st, kt);
+}

@@ -244,3 +244,27 @@ def test_paper_1e19_and_quotients(engine, golden):
     r = engine.mertens_exact(10**19)
     assert r.value == 899990187
     assert (r.quotient(10), r.quotient(100), r.quotient(1000)) == (-46758740, -21830254, -3195437)
+
+
+@pytest.mark.parametrize("y1,length", [(1, 3 << 20), (10**9 - 123457, 3 << 20), (2**32 - 70000, 300000),
+                                       (4_641_588_833_612 - 10**6, 2 * 10**6),
+                                       (82_036_050_574_571 - 10**6, 10**6), (464_158_883_361_277 - 10**6, 10**6)])
+def test_production_sieve_mu(engine, oracle, y1, length):
+    """The engine's production sieve (presieve patterns, buckets, look-back)
+    gives the reference's mu on ranges up to the 1e22 job's u."""
+    from paper_1108_0135_b200 import _lib
+
+    y2 = y1 + length - 1
+    mu = np.zeros(length, np.int8)
+    _lib.check(_lib.lib().mt_sieve_fast(y1, y2, _lib.ptr(mu), None))
+    ref = oracle.mu_range(oracle.get_kernels("c"), y1, y2)
+    assert np.array_equal(mu, ref), int((mu != ref).sum())
+
+
+def test_production_sieve_prefix(engine, oracle):
+    from paper_1108_0135_b200 import _lib
+
+    n = 5_000_000
+    m = np.zeros(n, np.int64)
+    _lib.check(_lib.lib().mt_sieve_fast(1, n, None, _lib.ptr(m)))
+    assert np.array_equal(m, oracle.mertens_table(n))
