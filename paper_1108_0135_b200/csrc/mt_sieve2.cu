@@ -59,6 +59,19 @@ __device__ __forceinline__ long long lb_val(unsigned long long w) {
   return ((long long)(w << 2)) >> 2;
 }
 
+__device__ __forceinline__ void red_add(u32 saddr, u32 v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_or(u32 saddr, u32 v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+// bucket entry: offset (17 bits) | value << 17; value bit 7 = square flag (OR)
+__device__ __forceinline__ void apply_entry(u32 sbase, u32 e) {
+  const u32 j = e & 0x1FFFFu, v = e >> 17, sh = (j & 3) * 8;
+  if (v & 0x80u) red_or(sbase + (j & ~3u), 0x80u << sh);
+  else red_add(sbase + (j & ~3u), v << sh);
+}
+
 // (-Y) mod p for p < 2^32, Y < 2^53, with r = 1/p rounded (host: 1.0/p)
 __device__ __forceinline__ u32 neg_mod(u64 Y, double Yd, double r, u32 p) {
   u64 q = qdiv64(Yd, r, Y, p);
@@ -71,38 +84,114 @@ __device__ __forceinline__ u32 neg_mod(u64 Y, double Yd, double r, u32 p) {
 // (square flags) in the segment [Y0, Y0 + R), appended to the producer-private
 // list of its tile.  Entry = offset (17 bits) | value << 17 (value bit 7 = OR).
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(512) k_bucket_fill(Bucket2Args a) {
+// Work is balanced by hits, not by primes: small primes hit the segment up
+// to 16x more often than large ones, so each round first computes every
+// prime's first hit and hit count (one prime per thread), then deals the hits
+// out in chunks of FCH consecutive multiples over all threads.
+#define FBATCH 2048  // primes per round
+#define FCH 8        // hits per chunk
+__global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
   extern __shared__ u32 cnt[];  // [ntiles]
-  const int tid = threadIdx.x;
+  __shared__ u64 s_q0[FBATCH];
+  __shared__ u32 s_step[FBATCH];
+  __shared__ u32 s_val[FBATCH];
+  __shared__ u32 s_off[FBATCH + 1];  // exclusive scan of chunk counts
+  __shared__ u32 s_wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 b = blockIdx.x, NP = gridDim.x;
   for (u32 t = tid; t < a.ntiles; t += blockDim.x) cnt[t] = 0;
-  __syncthreads();
   const u64 Y0 = a.Y0, R = (u64)a.ntiles * S2_T;
   const double Yd = (double)Y0;
   u32* __restrict__ out = a.buf + (u64)b * a.ntiles * a.cap;
-  // log marks of large primes: indices p_lo + b + k*NP
-  for (u64 i = (u64)a.p_lo + b + (u64)tid * NP; i < a.p_hi; i += (u64)blockDim.x * NP) {
-    const u32 p = a.primes[i];
-    const u32 lg = a.logs[i];
-    u64 pos = neg_mod(Y0, Yd, a.rprimes[i], p);
-    if (Y0 == 0 && pos == 0) pos = p;  // y = 0 is never marked
-    for (; pos < R; pos += p) {
-      const u32 t = (u32)(pos >> 17);
-      const u32 s = atomicAdd(&cnt[t], 1u);
-      if (s < a.cap) out[(u64)t * a.cap + s] = (u32)(pos & (S2_T - 1)) | (lg << 17);
+  const u32 cap = a.cap;
+  // this producer's items: log primes p_lo + b + k*NP, then squares q_lo + b + k*NP
+  const u32 nlog = a.p_hi > a.p_lo + b ? (a.p_hi - a.p_lo - b + NP - 1) / NP : 0;
+  const u32 nsq = a.q_hi > a.q_lo + b ? (a.q_hi - a.q_lo - b + NP - 1) / NP : 0;
+  const u32 nitems = nlog + nsq;
+  for (u32 base = 0; base < nitems; base += FBATCH) {
+    __syncthreads();
+    // phase 1: first hit, step, value and chunk count of 2 items per thread
+    u32 c[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const u32 k = base + tid * 2 + h;
+      c[h] = 0;
+      if (k >= nitems || tid * 2 + h >= FBATCH) continue;
+      u64 q0, step;
+      u32 val;
+      if (k < nlog) {
+        const u64 i = (u64)a.p_lo + b + (u64)k * NP;
+        const u32 p = a.primes[i];
+        q0 = neg_mod(Y0, Yd, a.rprimes[i], p);
+        if (Y0 == 0 && q0 == 0) q0 = p;  // y = 0 is never marked
+        step = p;
+        val = (u32)a.logs[i] << 17;
+      } else {
+        const u64 i = (u64)a.q_lo + b + (u64)(k - nlog) * NP;
+        const u64 p = a.primes[i];
+        const u64 q = p * p;
+        const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Y0, q);
+        const u64 rem = Y0 - qq * q;
+        q0 = rem ? q - rem : (Y0 ? 0 : q);
+        step = q;
+        val = 0x80u << 17;
+      }
+      const u64 hits = q0 < R ? (R - 1 - q0) / step + 1 : 0;
+      c[h] = (u32)((hits + FCH - 1) / FCH);
+      s_q0[tid * 2 + h] = q0;
+      s_step[tid * 2 + h] = step > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)step;  // R <= 2^31: one hit at most
+      s_val[tid * 2 + h] = val;
     }
-  }
-  // square flags of p^2 > S2_T: indices q_lo + b + k*NP
-  for (u64 i = (u64)a.q_lo + b + (u64)tid * NP; i < a.q_hi; i += (u64)blockDim.x * NP) {
-    const u64 p = a.primes[i];
-    const u64 q = p * p;
-    u64 qq = qdiv64(Yd, __drcp_rn((double)q), Y0, q);
-    u64 rem = Y0 - qq * q;
-    u64 pos = rem ? q - rem : (Y0 ? 0 : q);
-    for (; pos < R; pos += q) {
-      const u32 t = (u32)(pos >> 17);
-      const u32 s = atomicAdd(&cnt[t], 1u);
-      if (s < a.cap) out[(u64)t * a.cap + s] = (u32)(pos & (S2_T - 1)) | (0x80u << 17);
+    // block exclusive scan of chunk counts (2 per thread)
+    const u32 tsum = c[0] + c[1];
+    u32 incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const u32 x = s_wsum[lane];
+      u32 ix = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, ix, o);
+        if (lane >= o) ix += t;
+      }
+      s_wsum[lane] = ix - x;
+      if (lane == 31) s_off[FBATCH] = ix;
+    }
+    __syncthreads();
+    {
+      const u32 e = s_wsum[warp] + incl - tsum;
+      if (tid * 2 < FBATCH) s_off[tid * 2] = e;
+      if (tid * 2 + 1 < FBATCH) s_off[tid * 2 + 1] = e + c[0];
+    }
+    __syncthreads();
+    const u32 nb = min((u32)FBATCH, nitems - base);
+    const u32 total = s_off[FBATCH];
+    // phase 2: chunks of FCH hits over all threads
+    for (u32 g = tid; g < total; g += blockDim.x) {
+      u32 lo = 0, hi = nb;  // largest k with s_off[k] <= g
+      while (hi - lo > 1) {
+        const u32 mid = (lo + hi) >> 1;
+        if (s_off[mid] <= g) lo = mid; else hi = mid;
+      }
+      const u32 ci = g - s_off[lo];
+      const u64 step = s_step[lo];
+      const u32 val = s_val[lo];
+      u64 pos = s_q0[lo] + (u64)ci * FCH * step;
+#pragma unroll
+      for (int h = 0; h < FCH; h++) {
+        if (pos < R) {
+          const u32 t = (u32)(pos >> 17);
+          const u32 sl = atomicAdd(&cnt[t], 1u);
+          if (sl < cap) out[(u64)t * cap + sl] = (u32)(pos & (S2_T - 1)) | val;
+        }
+        pos += step;
+      }
     }
   }
   __syncthreads();
@@ -139,10 +228,9 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve2(Sieve2Args a) {
   __shared__ u32 s_tile;
   __shared__ long long s_excl;
   __shared__ int s_total;
-  __shared__ u32 s_queue;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  if (tid == 0) { s_tile = atomicAdd(a.ticket, 1u); s_queue = 0; }
+  if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
   __syncthreads();
   const u32 tile = s_tile;
   const u64 Yt = a.Y0 + (u64)tile * S2_T;
@@ -157,99 +245,100 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve2(Sieve2Args a) {
   }
   __syncthreads();
 
-  // 2.+3. marks, dealt to warps from a shared work queue (largest items first):
-  //   A  warp per prime, 43 <= p < 1024 (>= 128 multiples per tile)
-  //   B  32 consecutive primes 1024 <= p <= 2^17, lane per prime
+  // 2.+3. marks, statically dealt to the 32 warps (no queue):
+  //   A  warp per prime, 43 <= p < 1024, snake order (balances the large early primes)
+  //   B  32 consecutive primes 1024 <= p <= big_min, lane per prime, groups round-robin
   //   C  warp per square p^2, 11 <= p <= 362
-  //   D  warp per bucket list (primes > 2^17, squares > 2^17)
+  //   D  bucket lists (primes > big_min, squares > 2^17), round-robin
+  // Marks are shared-memory reductions (red.shared) on the 32-bit word of the cell.
   {
+    const u32 sbase = (u32)__cvta_generic_to_shared(st);
     const u32 nA = a.p_warp_end - a.p_first;
+    for (u32 r = 0; r * 32 < nA; r++) {
+      const u32 k = r * 32 + ((r & 1) ? 31 - warp : warp);
+      if (k >= nA) continue;
+      const u32 i = a.p_first + k;
+      const u32 p = a.primes[i];
+      const u32 lg = a.logs[i];
+      u32 j0 = neg_mod(Yt, Yd, a.rprimes[i], p);
+      if (Yt == 0 && j0 == 0) j0 = p;
+      // step 32p keeps the byte lane: one shifted value, word index += 8p
+      const u32 j = j0 + lane * p;
+      const u32 v = lg << ((j & 3) * 8);
+      const u32 astep = 32 * p;  // bytes
+#pragma unroll 4
+      for (u32 ad = sbase + (j & ~3u); ad < sbase + S2_T; ad += astep) red_add(ad, v);
+    }
     const u32 nB = (a.p_small_end - a.p_warp_end + 31) / 32;
-    const u32 nC = a.sq_end - a.sq_first;
-    const u32 nD = a.nprod;
-    const u32 total = nA + nB + nC + nD;
-    for (;;) {
-      u32 it = 0;
-      if (lane == 0) it = atomicAdd(&s_queue, 1u);
-      it = __shfl_sync(0xffffffffu, it, 0);
-      if (it >= total) break;
-      if (it < nA) {
-        const u32 i = a.p_first + it;
+    for (u32 g = warp; g < nB; g += 32) {
+      const u32 i = a.p_warp_end + g * 32 + lane;
+      if (i < a.p_small_end) {
         const u32 p = a.primes[i];
         const u32 lg = a.logs[i];
-        u32 j0 = neg_mod(Yt, Yd, a.rprimes[i], p);
-        if (Yt == 0 && j0 == 0) j0 = p;
-        // step 32p keeps the byte lane: one shifted value, word index += 8p
-        const u32 j = j0 + lane * p;
-        const u32 v = lg << ((j & 3) * 8);
-        const u32 wstep = 8 * p;
-#pragma unroll 4
-        for (u32 w = j >> 2; w < S2_W; w += wstep) atomicAdd(&st[w], v);
-        continue;
+        u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
+        if (Yt == 0 && j == 0) j = p;
+        // four consecutive multiples cycle through the four byte lanes (p odd):
+        // their shifted values are loop-invariant and each address steps by 4p
+        const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p;
+        const u32 v0 = lg << ((j & 3) * 8), v1 = lg << ((j1 & 3) * 8);
+        const u32 v2 = lg << ((j2 & 3) * 8), v3 = lg << ((j3 & 3) * 8);
+        const u32 end = sbase + S2_T, st4 = 4 * p;
+        u32 a0 = sbase + (j & ~3u), a1 = sbase + (j1 & ~3u), a2 = sbase + (j2 & ~3u), a3 = sbase + (j3 & ~3u);
+        for (; a0 < end; a0 += st4, a1 += st4, a2 += st4, a3 += st4) {
+          red_add(a0, v0);
+          if (a1 < end) red_add(a1, v1);
+          if (a2 < end) red_add(a2, v2);
+          if (a3 < end) red_add(a3, v3);
+        }
       }
-      it -= nA;
-      if (it < nB) {
-        const u32 i = a.p_warp_end + it * 32 + lane;
-        if (i < a.p_small_end) {
-          const u32 p = a.primes[i];
-          const u32 lg = a.logs[i];
-          u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
-          if (Yt == 0 && j == 0) j = p;
-          // four consecutive multiples cycle through the four byte lanes (p odd):
-          // their shifted values are loop-invariant and each word index steps by p
-          const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p;
-          const u32 v0 = lg << ((j & 3) * 8), v1 = lg << ((j1 & 3) * 8);
-          const u32 v2 = lg << ((j2 & 3) * 8), v3 = lg << ((j3 & 3) * 8);
-          u32 w0 = j >> 2, w1 = j1 >> 2, w2 = j2 >> 2, w3 = j3 >> 2;
-          for (; w3 < S2_W; w0 += p, w1 += p, w2 += p, w3 += p) {
-            atomicAdd(&st[w0], v0);
-            atomicAdd(&st[w1], v1);
-            atomicAdd(&st[w2], v2);
-            atomicAdd(&st[w3], v3);
+    }
+    for (u32 i = a.sq_first + warp; i < a.sq_end; i += 32) {
+      const u32 p = a.primes[i];
+      const u32 q = p * p;
+      u32 j0 = neg_mod(Yt, Yd, __drcp_rn((double)q), q);
+      if (Yt == 0 && j0 == 0) j0 = q;
+      for (u32 j = j0 + lane * q; j < S2_T; j += 32 * q) red_or(sbase + (j & ~3u), 0x80u << ((j & 3) * 8));
+    }
+    if (a.nprod) {
+      for (u32 b0 = 0; b0 < a.nprod; b0 += 32 * 32) {
+        // counts of this warp's next (up to) 32 lists: list b0 + warp + 32*l in lane l
+        const u32 bl = b0 + warp + 32 * lane;
+        const u32 nl = bl < a.nprod ? a.counts[(u64)bl * a.ntiles + tile] : 0u;
+        for (u32 l = 0; l < 32; l++) {
+          const u32 b = b0 + warp + 32 * l;
+          if (b >= a.nprod) break;
+          const u32 n = __shfl_sync(0xffffffffu, nl, l);
+          const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
+          if (n <= a.cap) {
+            for (u32 k = lane; k < n; k += 128) {
+              const u32 e0 = L[k];
+              const u32 e1 = k + 32 < n ? L[k + 32] : 0u;
+              const u32 e2 = k + 64 < n ? L[k + 64] : 0u;
+              const u32 e3 = k + 96 < n ? L[k + 96] : 0u;
+              apply_entry(sbase, e0);
+              apply_entry(sbase, e1);
+              apply_entry(sbase, e2);
+              apply_entry(sbase, e3);
+            }
+          } else {  // overflowed list: this producer's hits on the tile, recomputed exactly
+            if (lane == 0) atomicAdd(a.overflow, 1ull);
+            for (u64 i = (u64)a.p_lo + b + (u64)lane * a.nprod; i < a.p_hi; i += 32ull * a.nprod) {
+              const u32 p = a.primes[i];
+              u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
+              if (Yt == 0 && j == 0) j = p;
+              for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), (u32)a.logs[i] << ((j & 3) * 8));
+            }
+            for (u64 i = (u64)a.q_lo + b + (u64)lane * a.nprod; i < a.q_hi; i += 32ull * a.nprod) {
+              const u64 p = a.primes[i];
+              const u64 q = p * p;
+              const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Yt, q);
+              const u64 rem = Yt - qq * q;
+              const u64 j = rem ? q - rem : (Yt ? 0 : q);
+              if (j < S2_T) red_or(sbase + ((u32)j & ~3u), 0x80u << (((u32)j & 3) * 8));
+            }
           }
-          if (w0 < S2_W) atomicAdd(&st[w0], v0);
-          if (w1 < S2_W) atomicAdd(&st[w1], v1);
-          if (w2 < S2_W) atomicAdd(&st[w2], v2);
-        }
-        __syncwarp();
-        continue;
-      }
-      it -= nB;
-      if (it < nC) {
-        const u32 i = a.sq_first + it;
-        const u32 p = a.primes[i];
-        const u32 q = p * p;
-        u32 j0 = neg_mod(Yt, Yd, __drcp_rn((double)q), q);
-        if (Yt == 0 && j0 == 0) j0 = q;
-        for (u32 j = j0 + lane * q; j < S2_T; j += 32 * q) mark_or(st, j);
-        continue;
-      }
-      const u32 b = it - nC;
-      const u32 n = a.counts[(u64)b * a.ntiles + tile];
-      const u32 m = n <= a.cap ? n : 0;  // an overflowed list is recomputed below instead
-      const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
-      for (u32 k = lane; k < m; k += 32) {
-        const u32 e = L[k];
-        const u32 j = e & (S2_T - 1), v = e >> 17;
-        if (v & 0x80u) mark_or(st, j); else mark_add(st, j, v);
-      }
-      if (n > a.cap) {  // overflowed list: this producer's hits on the tile, recomputed exactly
-        if (lane == 0) atomicAdd(a.overflow, 1ull);
-        for (u64 i = (u64)a.p_lo + b + (u64)lane * a.nprod; i < a.p_hi; i += 32ull * a.nprod) {
-          const u32 p = a.primes[i];
-          const u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
-          if (j < S2_T && !(Yt == 0 && j == 0)) mark_add(st, j, a.logs[i]);
-        }
-        for (u64 i = (u64)a.q_lo + b + (u64)lane * a.nprod; i < a.q_hi; i += 32ull * a.nprod) {
-          const u64 p = a.primes[i];
-          const u64 q = p * p;
-          const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Yt, q);
-          const u64 rem = Yt - qq * q;
-          const u64 j = rem ? q - rem : (Yt ? 0 : q);
-          if (j < S2_T) mark_or(st, (u32)j);
         }
       }
-      __syncwarp();
     }
   }
   __syncthreads();
@@ -434,7 +523,7 @@ int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
     Bucket2Args b = g.bucket;
     const size_t bs = (size_t)b.ntiles * sizeof(u32);
     if (kt) kt->begin(KT_SIEVE_LARGE, st);
-    k_bucket_fill<<<b.nprod_grid, 512, bs, st>>>(b);
+    k_bucket_fill<<<b.nprod_grid, 1024, bs, st>>>(b);
     if (kt) kt->end(st);
     MT_CUDA_CHECK(cudaGetLastError());
   }
@@ -451,6 +540,7 @@ int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
 // ============================================================================
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 namespace {
@@ -502,6 +592,7 @@ struct Sieve2Host {
   u64 P1 = 485100, P2 = 1062347, P3 = 1363783;
   std::vector<u32> p;
   u32 nprod = 0, cap = 0, max_tiles = 0;
+  u32 big_min = S2_T;  // primes above this go to the bucket lists
   uint64_t overflows_host = 0;
 };
 
@@ -537,6 +628,7 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
   if (up(h->w1, pattern_words(h->P1, {2, 3, 5, 7}, {4, 9, 25, 49}))) return MT_ERR_RESOURCE;
   if (up(h->w2, pattern_words(h->P2, {11, 13, 17, 19, 23}, {}))) return MT_ERR_RESOURCE;
   if (up(h->w3, pattern_words(h->P3, {29, 31, 37, 41}, {}))) return MT_ERR_RESOURCE;
+  if (const char* e = getenv("MT_S2_BIG_LOG2")) h->big_min = 1u << atoi(e);
   // bucket space: producers = SMs; capacity from the expected hits per (producer, tile)
   int dev, nsm;
   cudaGetDevice(&dev);
@@ -544,10 +636,10 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
   double e = 0;
   for (size_t i = 0; i < np; i++) {
     const double pp = h->p[i];
-    if (pp > S2_T) e += S2_T / pp;
+    if (pp > h->big_min) e += S2_T / pp + 1.0 / 64;
     if (pp > 362 && pp * pp <= (double)y_last * 1.0001) e += S2_T / (pp * pp);
   }
-  const bool any = np && (h->p.back() > S2_T || (double)h->p.back() > 362.0);
+  const bool any = np && (h->p.back() > h->big_min || (double)h->p.back() > 362.0);
   if (any && e > 0) {
     h->nprod = (u32)nsm;
     const double m = e / h->nprod;
@@ -567,7 +659,7 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
                                        (int)(max_tiles * 4)));
     attr = true;
   }
-  if (max_tiles * 4 > 200 * 1024) { mt_set_error("too many tiles per segment"); return MT_ERR_VALUE; }
+  if (max_tiles > 16384) { mt_set_error("too many tiles per segment (max 2^31 cells)"); return MT_ERR_VALUE; }
   MT_CUDA_CHECK(cudaStreamSynchronize(st));
   return MT_OK;
 }
@@ -602,7 +694,7 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
   a.primes = (const u32*)h->prm.p; a.rprimes = (const double*)h->rp.p; a.logs = (const uint8_t*)h->lg.p;
   a.p_first = std::min(idx_gt(42), end);
   a.p_warp_end = std::max(a.p_first, std::min(idx_gt(1023), end));
-  a.p_small_end = std::max(a.p_warp_end, std::min(idx_gt(S2_T), end));
+  a.p_small_end = std::max(a.p_warp_end, std::min(idx_gt(h->big_min), end));
   a.sq_first = std::min(idx_gt(10), end);
   a.sq_end = std::max(a.sq_first, std::min(idx_gt(362), end));
   a.p_lo = a.p_small_end; a.p_hi = end;

@@ -1,0 +1,12 @@
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests -x -q -m gpu -k "production or e10 or reference_values or multi" 2>&1 | tail -2
+for big in 17 16; do
+echo "big_min 2^$big"
+for e in 1e17 1e19; do MT_TIMING=1 MT_S2_BIG_LOG2=$big timeout 300 python tools/prof_job.py $e 1 ; done 2>&1 | python -c "
+import sys,ast
+for l in sys.stdin:
+    p=l.split(' ',3)
+    if len(p)<4: print(l); continue
+    d=ast.literal_eval(p[3]); print(p[0],p[1],p[2],{k:d[k] for k in ('ms_total','ms_update_head','ms_sieve_tail','ms_qgather','ms_setup')}, {k:round(v,1) for k,v in d['kernel_ms'].items()})
+"
+done
