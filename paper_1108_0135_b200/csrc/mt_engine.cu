@@ -795,10 +795,17 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   P->launches++;
 
   // ---- segments (production sieve tiles of 2^17 cells)
-  P->Rh = 1ull << (job->seg_log2_head ? job->seg_log2_head : 26);
-  P->Rt = 1ull << (job->seg_log2_tail ? job->seg_log2_tail : 26);
+  // default segment = 4 tiles per SM (the persistent sieve CTAs each take 4 contiguous tiles)
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P->device);
+  const u64 seg_default = (u64)nsm * 4 * MT_S2_TILE;
+  P->Rh = job->seg_log2_head ? 1ull << job->seg_log2_head : seg_default;
+  P->Rt = job->seg_log2_tail ? 1ull << job->seg_log2_tail : seg_default;
   const u64 Rh = P->Rh, Rt = P->Rt;
-  if (Rh < MT_S2_TILE || Rt < Rh || (Rt % Rh) || Rt > (1ull << 32)) { mt_set_error("bad segment sizes"); return MT_ERR_VALUE; }
+  if (Rh < MT_S2_TILE || Rt < MT_S2_TILE || (Rh % MT_S2_TILE) || (Rt % MT_S2_TILE) || Rt > (1ull << 31) || Rh > (1ull << 31)) {
+    mt_set_error("bad segment sizes");
+    return MT_ERR_VALUE;
+  }
   P->head_segs = (head_end + 1 + Rh - 1) / Rh;
   P->head_lim = P->head_segs * Rh;  // first y of the tail
   P->tail_segs = 0;
@@ -806,7 +813,7 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   P->y_last = P->head_lim + P->tail_segs * Rt - 1;
   P->tseg0 = P->tail_segs * P->rank / P->world;
   P->tseg1 = P->tail_segs * (P->rank + 1) / P->world;
-  RC(mt_sieve2_create(&P->sv, P->y_last, (uint32_t)(Rt / MT_S2_TILE), st));
+  RC(mt_sieve2_create(&P->sv, P->y_last, (uint32_t)(std::max(Rh, Rt) / MT_S2_TILE), st));
   RC(dalloc(P->d_mu, Rh)); RC(dalloc(P->d_m, Rh * 2)); RC(dalloc(P->d_bk, (Rh / MT_BLK) * 8 + 8));
   RC(dalloc(P->d_run, 8));
   RC(dalloc(P->d_caps, P->caps.size() * sizeof(CaptureTargetH)));

@@ -148,7 +148,10 @@ struct Sieve2Args {
   int8_t* mu_out;                             // head: mu
   int16_t* m16_out;                           // head: M(y) - M(32K block start - 1)
   int64_t* bk;                                // head: M(32K block start - 1)
-  int* tile_sum;                              // optional
+  int* tile_sum;                              // [ntiles] tile totals
+  int64_t* tile_base;                         // [ntiles] M(tile start - 1)
+  int* bkrel;                                 // head: tile-relative 32K block starts [ntiles*4]
+  uint32_t tiles_per_cta;                     // persistent CTAs: contiguous tiles each
   const CaptureTarget2* caps;
   int n_cap;
 };

@@ -515,9 +515,361 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve2(Sieve2Args a) {
   }
 }
 
+// ----------------------------------------------------------------------------
+// k_sieve3: persistent tile kernel.  CTA c sieves the contiguous tiles
+// [c*m, c*m + m) of the segment; the first multiple of every in-tile prime
+// (and square) is computed once per CTA by division and then carried from
+// tile to tile in shared memory (no per-tile division).  Captures and head
+// outputs are tile-relative; k_s3_scan / k_s3_fixup make them absolute.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void red_add_if(u32 saddr, u32 v, u32 end) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.lt.u32 q, %0, %2;\n\t@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(saddr), "r"(v),
+               "r"(end)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
+  extern __shared__ u32 st[];                   // S2_W state / mu words
+  int* csum = (int*)(st + S2_W);                // S2_CH chunk sums -> exclusive chunk prefixes
+  const u32 nA = a.p_warp_end - a.p_first;
+  const u32 nBp = a.p_small_end - a.p_warp_end;
+  const u32 nC = a.sq_end - a.sq_first;
+  u32* offA = (u32*)(csum + S2_CH);             // first multiple of p (lane 0's mark), A primes
+  u32* tmA = offA + nA;                         // T mod p
+  u32* offB = tmA + nA;                         // first multiple, B primes
+  u32* offC = offB + nBp;                       // first multiple of p^2, small squares
+  u32* tmC = offC + nC;                         // T mod p^2
+  __shared__ int wsum[32];
+  __shared__ int s_total;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 m = a.tiles_per_cta;
+  const u32 tile0 = blockIdx.x * m;
+  if (tile0 >= a.ntiles) return;
+  const u32 tile_end = min(tile0 + m, a.ntiles);
+  const u32 sbase = (u32)__cvta_generic_to_shared(st);
+  const u32 send = sbase + S2_T;
+
+  // ---- first multiples at the CTA's first tile
+  {
+    const u64 Y = a.Y0 + (u64)tile0 * S2_T;
+    const double Yd = (double)Y;
+    for (u32 k = tid; k < nA; k += S2_NT) {
+      const u32 i = a.p_first + k, p = a.primes[i];
+      u32 j = neg_mod(Y, Yd, a.rprimes[i], p);
+      if (Y == 0 && j == 0) j = p;
+      offA[k] = j;
+      tmA[k] = S2_T % p;
+    }
+    for (u32 k = tid; k < nBp; k += S2_NT) {
+      const u32 i = a.p_warp_end + k, p = a.primes[i];
+      u32 j = neg_mod(Y, Yd, a.rprimes[i], p);
+      if (Y == 0 && j == 0) j = p;
+      offB[k] = j;
+    }
+    for (u32 k = tid; k < nC; k += S2_NT) {
+      const u32 p = a.primes[a.sq_first + k], q = p * p;
+      u32 j = neg_mod(Y, Yd, __drcp_rn((double)q), q);
+      if (Y == 0 && j == 0) j = q;
+      offC[k] = j;
+      tmC[k] = S2_T % q;
+    }
+  }
+
+  for (u32 tile = tile0; tile < tile_end; tile++) {
+    const u64 Yt = a.Y0 + (u64)tile * S2_T;
+    __syncthreads();  // offsets ready / previous tile's outputs done
+    // 1. presieve patterns
+    {
+      const u32* __restrict__ w1 = a.w1 + (u32)((Yt % a.w1_period4) >> 2);
+      const u32* __restrict__ w2 = a.w2 + (u32)((Yt % a.w2_period4) >> 2);
+      const u32* __restrict__ w3 = a.w3 + (u32)((Yt % a.w3_period4) >> 2);
+      for (int i = tid; i < (int)S2_W; i += S2_NT) st[i] = w1[i] + w2[i] + w3[i];
+    }
+    __syncthreads();
+    // 2. marks
+    // A: warp per prime, snake order over the warps
+    for (u32 r = 0; r * 32 < nA; r++) {
+      const u32 k = r * 32 + ((r & 1) ? 31 - warp : warp);
+      if (k >= nA) continue;
+      const u32 i = a.p_first + k;
+      const u32 p = a.primes[i];
+      const u32 lg = a.logs[i];
+      const u32 j0 = offA[k];
+      const u32 j = j0 + lane * p;
+      const u32 v = lg << ((j & 3) * 8);
+      const u32 astep = 32 * p;
+#pragma unroll 4
+      for (u32 ad = sbase + (j & ~3u); ad < send; ad += astep) red_add(ad, v);
+      __syncwarp();
+      if (lane == 0) { const u32 tm = tmA[k]; offA[k] = j0 >= tm ? j0 - tm : j0 + p - tm; }
+    }
+    // B: lane per prime, groups of 32 in snake order
+    {
+      const u32 nB = (nBp + 31) / 32;
+      for (u32 r = 0; r * 32 < nB; r++) {
+        const u32 g = r * 32 + ((r & 1) ? 31 - warp : warp);
+        if (g >= nB) continue;
+        const u32 k = g * 32 + lane;
+        if (k < nBp) {
+          const u32 i = a.p_warp_end + k;
+          const u32 p = a.primes[i];
+          const u32 lg = a.logs[i];
+          u32 j = offB[k];
+          const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p, p4 = 4 * p;
+          const u32 v0 = lg << ((j & 3) * 8), v1 = lg << ((j1 & 3) * 8);
+          const u32 v2 = lg << ((j2 & 3) * 8), v3 = lg << ((j3 & 3) * 8);
+          u32 a0 = sbase + (j & ~3u), a1 = sbase + (j1 & ~3u), a2 = sbase + (j2 & ~3u), a3 = sbase + (j3 & ~3u);
+          for (; a0 < send; a0 += p4, a1 += p4, a2 += p4, a3 += p4, j += p4) {
+            red_add(a0, v0);
+            red_add_if(a1, v1, send);
+            red_add_if(a2, v2, send);
+            red_add_if(a3, v3, send);
+          }
+          // first multiple beyond the tile: j (loop exit) minus the multiples past the end
+          while (j >= S2_T + p) j -= p;
+          offB[k] = j - S2_T;
+        }
+      }
+    }
+    // C: warp per small square
+    for (u32 k = warp; k < nC; k += 32) {
+      const u32 p = a.primes[a.sq_first + k], q = p * p;
+      const u32 j0 = offC[k];
+      for (u32 j = j0 + lane * q; j < S2_T; j += 32 * q) red_or(sbase + (j & ~3u), 0x80u << ((j & 3) * 8));
+      __syncwarp();
+      if (lane == 0) { const u32 tm = tmC[k]; offC[k] = j0 >= tm ? j0 - tm : j0 + q - tm; }
+    }
+    // D: bucket lists (primes > big_min, squares > 2^17)
+    if (a.nprod) {
+      const double Yd = (double)Yt;
+      for (u32 b0 = 0; b0 < a.nprod; b0 += 32 * 32) {
+        const u32 bl = b0 + warp + 32 * lane;
+        const u32 nl = bl < a.nprod ? a.counts[(u64)bl * a.ntiles + tile] : 0u;
+        for (u32 l = 0; l < 32; l++) {
+          const u32 b = b0 + warp + 32 * l;
+          if (b >= a.nprod) break;
+          const u32 n = __shfl_sync(0xffffffffu, nl, l);
+          const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
+          if (n <= a.cap) {
+            for (u32 k = lane; k < n; k += 128) {
+              const u32 e0 = L[k];
+              const u32 e1 = k + 32 < n ? L[k + 32] : 0u;
+              const u32 e2 = k + 64 < n ? L[k + 64] : 0u;
+              const u32 e3 = k + 96 < n ? L[k + 96] : 0u;
+              apply_entry(sbase, e0);
+              apply_entry(sbase, e1);
+              apply_entry(sbase, e2);
+              apply_entry(sbase, e3);
+            }
+          } else {  // overflowed list: this producer's hits on the tile, recomputed exactly
+            if (lane == 0) atomicAdd(a.overflow, 1ull);
+            for (u64 i = (u64)a.p_lo + b + (u64)lane * a.nprod; i < a.p_hi; i += 32ull * a.nprod) {
+              const u32 p = a.primes[i];
+              u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
+              if (Yt == 0 && j == 0) j = p;
+              for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), (u32)a.logs[i] << ((j & 3) * 8));
+            }
+            for (u64 i = (u64)a.q_lo + b + (u64)lane * a.nprod; i < a.q_hi; i += 32ull * a.nprod) {
+              const u64 p = a.primes[i];
+              const u64 q = p * p;
+              const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Yt, q);
+              const u64 rem = Yt - qq * q;
+              const u64 j = rem ? q - rem : (Yt ? 0 : q);
+              if (j < S2_T) red_or(sbase + ((u32)j & ~3u), 0x80u << (((u32)j & 3) * 8));
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (a.states_out) {  // instrumented export (debug)
+      u32* so = (u32*)(a.states_out + (u64)tile * S2_T);
+      for (int i = tid; i < (int)S2_W; i += S2_NT) so[i] = st[i];
+      __syncthreads();
+    }
+    // 3. classify (warp w: words [w*1024, (w+1)*1024), lane l: 4 words per step)
+    {
+      const bool uniform = Yt >= S2_T;
+      const int thr_t = 62 - __clzll((long long)(Yt | 1));
+      const u32 kthr = uniform ? (u32)(127 - thr_t) * 0x01010101u : 0u;
+      uint4* st4 = (uint4*)st;
+#pragma unroll 2
+      for (int it = 0; it < 8; it++) {
+        const int q = warp * 256 + it * 32 + lane;
+        uint4 w = st4[q];
+        int s = 0;
+        if (uniform) {
+          w.x = mu_word(w.x, kthr, s);
+          w.y = mu_word(w.y, kthr, s);
+          w.z = mu_word(w.z, kthr, s);
+          w.w = mu_word(w.w, kthr, s);
+        } else {
+          u32* wv = (u32*)&w;
+          for (int k = 0; k < 4; k++) {
+            u32 mw = 0;
+            for (int bb = 0; bb < 4; bb++) {
+              const u64 y = Yt + (u64)(q * 4 + k) * 4 + bb;
+              const int thr = (y ? 63 - __clzll((long long)y) : 0) - 1;
+              const int mm = mu_cell((wv[k] >> (8 * bb)) & 0xff, thr);
+              s += mm;
+              mw |= ((u32)(mm & 0xff)) << (8 * bb);
+            }
+            wv[k] = mw;
+          }
+        }
+        st4[q] = w;
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        if (!(lane & 1)) csum[q >> 1] = s;
+      }
+    }
+    __syncthreads();
+    // 4. exclusive scan of the 4096 chunk sums (tile-relative)
+    {
+      int v0 = csum[tid * 4], v1 = csum[tid * 4 + 1], v2 = csum[tid * 4 + 2], v3 = csum[tid * 4 + 3];
+      int tsum = v0 + v1 + v2 + v3;
+      int incl = tsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) wsum[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        int x = wsum[lane], ix = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int t = __shfl_up_sync(0xffffffffu, ix, o);
+          if (lane >= o) ix += t;
+        }
+        wsum[lane] = ix - x;
+        if (lane == 31) s_total = ix;
+      }
+      __syncthreads();
+      int e = wsum[warp] + incl - tsum;
+      csum[tid * 4] = e;
+      csum[tid * 4 + 1] = e + v0;
+      csum[tid * 4 + 2] = e + v0 + v1;
+      csum[tid * 4 + 3] = e + v0 + v1 + v2;
+    }
+    __syncthreads();
+    if (tid == 0) a.tile_sum[tile] = s_total;
+    // 5. head outputs (tile-relative block starts; k_s3_scan makes bk absolute)
+    if (a.mu_out) {
+      u32* mo = (u32*)(a.mu_out + (u64)tile * S2_T);
+      for (int i = tid; i < (int)S2_W; i += S2_NT) mo[i] = st[i];
+    }
+    if (a.m16_out) {
+      if (tid < 4) a.bkrel[(u64)tile * 4 + tid] = csum[tid * 1024];
+      int16_t* m16 = a.m16_out + (u64)tile * S2_T;
+      for (int c = tid; c < (int)S2_CH; c += S2_NT) {
+        const int bstart = csum[(c >> 10) << 10];
+        int run = csum[c] - bstart;
+        const u32* wp = st + c * 8;
+        uint4 o[4];
+        u32* ov = (u32*)o;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const u32 w = wp[k];
+          const int c0 = run + (int)(int8_t)(w & 0xff);
+          const int c1 = c0 + (int)(int8_t)((w >> 8) & 0xff);
+          const int c2 = c1 + (int)(int8_t)((w >> 16) & 0xff);
+          const int c3 = c2 + (int)(int8_t)(w >> 24);
+          ov[2 * k] = (u32)(uint16_t)c0 | ((u32)(uint16_t)c1 << 16);
+          ov[2 * k + 1] = (u32)(uint16_t)c2 | ((u32)(uint16_t)c3 << 16);
+          run = c3;
+        }
+        uint4* dst = (uint4*)(m16 + (u64)c * 32);
+#pragma unroll
+        for (int k = 0; k < 4; k++) dst[k] = o[k];
+      }
+    }
+    // 6. captures, tile-relative: Q_t[j] = M(floor(n_t/j)) - M(Yt - 1)
+    for (int t = 0; t < a.n_cap; t++) {
+      const CaptureTarget2& ct = a.caps[t];
+      u64 jhi = Yt ? udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt) : ~0ull;
+      u64 jlo = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt + S2_T) + 1;
+      if (jlo < ct.jq0) jlo = ct.jq0;
+      if (jhi > ct.jq1) jhi = ct.jq1;
+      for (u64 j = jlo + tid; j <= jhi; j += S2_NT) {
+        const u64 y = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, j);
+        const u32 o = (u32)(y - Yt);
+        const int c = o >> 5;
+        const u32* wp = st + (c << 3);
+        int s = 0;
+        const u32 last = o & 31;
+        for (u32 k = 0; k <= (last >> 2); k++) {
+          u32 w = wp[k];
+          if (k == (last >> 2)) {
+            const u32 keep = (last & 3) + 1;
+            w = keep == 4 ? w : (w & ((1u << (8 * keep)) - 1));
+          }
+          s = __dp4a((int)w, 0x01010101, s);
+        }
+        ct.Q[j - ct.jq0] = csum[c] + s;
+      }
+    }
+  }
+}
+
+// exclusive tile bases for one segment, seeded with the running M; absolute
+// 32K block bases for the head
+__global__ void k_s3_scan(const int* __restrict__ tile_sum, u32 ntiles, i64* __restrict__ running,
+                          i64* __restrict__ tile_base, const int* __restrict__ bkrel, i64* __restrict__ bk) {
+  __shared__ i64 wsum[32];
+  __shared__ i64 carry;
+  const int tid = threadIdx.x;
+  if (tid == 0) carry = *running;
+  __syncthreads();
+  for (u32 base = 0; base < ntiles; base += 1024) {
+    const u32 i = base + tid;
+    const i64 v = i < ntiles ? tile_sum[i] : 0;
+    i64 incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      i64 t = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((tid & 31) >= o) incl += t;
+    }
+    if ((tid & 31) == 31) wsum[tid >> 5] = incl;
+    __syncthreads();
+    if (tid < 32) {
+      i64 x = wsum[tid], ix = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        i64 t = __shfl_up_sync(0xffffffffu, ix, o);
+        if (tid >= o) ix += t;
+      }
+      wsum[tid] = ix - x;
+    }
+    __syncthreads();
+    const i64 excl = carry + wsum[tid >> 5] + incl - v;
+    if (i < ntiles) {
+      tile_base[i] = excl;
+      if (bk)
+        for (int q = 0; q < 4; q++) bk[(u64)i * 4 + q] = excl + bkrel[(u64)i * 4 + q];
+    }
+    __syncthreads();
+    if (tid == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (tid == 0) *running = carry;
+}
+
+// Q[j] += M(Yt - 1) for the captures of each tile (one block per tile)
+__global__ void k_s3_fixup(const CaptureTarget2* __restrict__ caps, int n_cap, u64 Y0,
+                           const i64* __restrict__ tile_base) {
+  const u64 Yt = Y0 + (u64)blockIdx.x * S2_T;
+  const int b = (int)tile_base[blockIdx.x];
+  for (int t = 0; t < n_cap; t++) {
+    const CaptureTarget2& ct = caps[t];
+    u64 jhi = Yt ? udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt) : ~0ull;
+    u64 jlo = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt + S2_T) + 1;
+    if (jlo < ct.jq0) jlo = ct.jq0;
+    if (jhi > ct.jq1) jhi = ct.jq1;
+    for (u64 j = jlo + threadIdx.x; j <= jhi; j += blockDim.x) ct.Q[j - ct.jq0] += b;
+  }
+}
+
 // ------------------------------------------------------------------ host side
 int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
-  const size_t smem = S2_T + S2_CH * sizeof(int);
   Sieve2Args a = g.tile;
   if (a.nprod) {
     Bucket2Args b = g.bucket;
@@ -527,9 +879,16 @@ int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
     if (kt) kt->end(st);
     MT_CUDA_CHECK(cudaGetLastError());
   }
-  MT_CUDA_CHECK(cudaMemsetAsync(a.tstate, 0, sizeof(unsigned long long) * a.ntiles + sizeof(u32), st));
+  const u32 nA = a.p_warp_end - a.p_first, nBp = a.p_small_end - a.p_warp_end, nC = a.sq_end - a.sq_first;
+  const size_t smem = S2_T + S2_CH * sizeof(int) + (size_t)(2 * nA + nBp + 2 * nC) * 4;
+  const u32 grid = (a.ntiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
   if (kt) kt->begin(KT_SIEVE_TILE, st);
-  k_sieve2<<<a.ntiles, S2_NT, smem, st>>>(a);
+  k_sieve3<<<grid, S2_NT, smem, st>>>(a);
+  if (kt) kt->end(st);
+  MT_CUDA_CHECK(cudaGetLastError());
+  if (kt) kt->begin(KT_OTHER, st);
+  k_s3_scan<<<1, 1024, 0, st>>>(a.tile_sum, a.ntiles, a.running, a.tile_base, a.bkrel, a.bk);
+  if (a.n_cap) k_s3_fixup<<<a.ntiles, 256, 0, st>>>(a.caps, a.n_cap, a.Y0, a.tile_base);
   if (kt) kt->end(st);
   MT_CUDA_CHECK(cudaGetLastError());
   return MT_OK;
@@ -588,7 +947,8 @@ std::vector<uint32_t> pattern_words(u64 P, const std::vector<u32>& logp_primes, 
 }  // namespace
 
 struct Sieve2Host {
-  Buf w1, w2, w3, prm, rp, lg, buf, counts, tstate, ovf;
+  Buf w1, w2, w3, prm, rp, lg, buf, counts, tstate, ovf, tsum, tbase, bkrel;
+  int nsm = 148;
   u64 P1 = 485100, P2 = 1062347, P3 = 1363783;
   std::vector<u32> p;
   u32 nprod = 0, cap = 0, max_tiles = 0;
@@ -649,15 +1009,21 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
         balloc(h->counts, (size_t)h->nprod * max_tiles * 4))
       return MT_ERR_RESOURCE;
   }
-  if (balloc(h->tstate, ((size_t)max_tiles + 1) * 8) || balloc(h->ovf, 8)) return MT_ERR_RESOURCE;
+  h->nsm = nsm;
+  if (balloc(h->tstate, ((size_t)max_tiles + 1) * 8) || balloc(h->ovf, 8) || balloc(h->tsum, (size_t)max_tiles * 4) ||
+      balloc(h->tbase, (size_t)max_tiles * 8) || balloc(h->bkrel, (size_t)max_tiles * 16))
+    return MT_ERR_RESOURCE;
   MT_CUDA_CHECK(cudaMemsetAsync(h->ovf.p, 0, 8, st));
-  static bool attr = false;
-  if (!attr) {
-    MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(S2_T + S2_CH * sizeof(int))));
+  {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_sieve3));
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       optin - (int)fa.sharedSizeBytes));
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_bucket_fill));
     MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(max_tiles * 4)));
-    attr = true;
+                                       optin - (int)fa.sharedSizeBytes));
   }
   if (max_tiles > 16384) { mt_set_error("too many tiles per segment (max 2^31 cells)"); return MT_ERR_VALUE; }
   MT_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -704,7 +1070,10 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
   a.counts = (const u32*)h->counts.p; a.buf = (const u32*)h->buf.p;
   a.overflow = (unsigned long long*)h->ovf.p;
   a.states_out = states_out; a.mu_out = mu_out; a.m16_out = m16_out; a.bk = bk;
-  a.tile_sum = nullptr;
+  a.tile_sum = (int*)h->tsum.p;
+  a.tile_base = (int64_t*)h->tbase.p;
+  a.bkrel = (int*)h->bkrel.p;
+  a.tiles_per_cta = (ntiles + h->nsm - 1) / h->nsm;
   a.caps = caps; a.n_cap = n_cap;
   Bucket2Args& b = g.bucket;
   b.Y0 = Y0; b.ntiles = ntiles; b.cap = h->cap; b.nprod_grid = a.nprod;
