@@ -93,6 +93,12 @@ int mt_mertens_at(const uint64_t* pts, uint64_t npts, int64_t* m_out);
  * mu_out and, if m_out is non-null, M(y) into m_out (either may be null) */
 int mt_sieve_fast(uint64_t y1, uint64_t y2, int8_t* mu_out, int64_t* m_out);
 
+/* profiling entry (tools/sieve_bench.py): the production sieve in tail mode
+ * over nseg default-size segments from Y0 (a multiple of 2^17) with the primes
+ * of y_last; summed CUDA-event ms per kernel class into ms_out[7]
+ * (sieve_tile, bucket_fill, -, -, -, -, scan+fixup) */
+int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, double* ms_out);
+
 /* ---- 2. job-level production entry ----------------------------------------- */
 
 typedef struct {

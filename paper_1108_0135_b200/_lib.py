@@ -16,7 +16,7 @@ import numpy as np
 from .errors import ContractViolationError, DeviceError, ResourceLimitError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmertens_sm100.so")
+LIB_PATH = os.environ.get("MT_LIB") or os.path.join(HERE, "libmertens_sm100.so")
 
 MT_OK, MT_ERR_RESOURCE, MT_ERR_CONTRACT, MT_ERR_CUDA, MT_ERR_VALUE, MT_ERR_OVERFLOW = range(6)
 
@@ -99,6 +99,7 @@ def lib():
         "mt_mertens_range": [_u64, _u64, vp],
         "mt_mertens_at": [vp, _u64, vp],
         "mt_sieve_fast": [_u64, _u64, vp, vp],
+        "mt_sieve_bench": [_u64, _u64, _u64, vp],
         "mt_run": [ctypes.POINTER(MtJob), ctypes.POINTER(MtResult)],
         "mt_plan_create": [ctypes.POINTER(MtJob), ctypes.POINTER(ctypes.c_void_p)],
         "mt_plan_sieve_update": [vp, _pi64, _pi64],
@@ -150,7 +151,7 @@ def ptr(a: np.ndarray):
 EXPORTED_SYMBOLS = (
     "mt_last_error", "mt_abi_version", "mt_device_count", "mt_set_device",
     "mt_sieve_logprime", "mt_logprime_states", "mt_sieve_naive", "mt_apply_block",
-    "mt_finalize", "mt_build_divisor_arrays", "mt_mertens_range", "mt_mertens_at", "mt_sieve_fast", "mt_run",
+    "mt_finalize", "mt_build_divisor_arrays", "mt_mertens_range", "mt_mertens_at", "mt_sieve_fast", "mt_sieve_bench", "mt_run",
     "mt_plan_create", "mt_plan_sieve_update", "mt_plan_tail_offset", "mt_plan_q_slice", "mt_plan_acc",
     "mt_plan_gather", "mt_plan_resolve", "mt_plan_destroy",
 )

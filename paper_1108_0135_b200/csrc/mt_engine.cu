@@ -345,6 +345,33 @@ extern "C" int mt_sieve_fast(uint64_t y1, uint64_t y2, int8_t* mu_out, int64_t* 
   return MT_OK;
 }
 
+// profiling entry: the production sieve in tail mode (sums only, no outputs)
+// over nseg segments of the default size from Y0 (multiple of 2^17), with
+// primes for y_last; per-kernel-class CUDA-event ms into ms_out[KT_NCLASS]
+extern "C" int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, double* ms_out) {
+  if (Y0 % MT_S2_TILE) { mt_set_error("Y0 must be a multiple of 2^17"); return MT_ERR_VALUE; }
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t NT = (uint32_t)nsm * 4;
+  const u64 R = (u64)NT * MT_S2_TILE;
+  if (y_last < Y0 + nseg * R) y_last = Y0 + nseg * R;
+  Sieve2Host* h = nullptr;
+  struct G { Sieve2Host*& h; ~G() { mt_sieve2_destroy(h); } } g{h};
+  RC(mt_sieve2_create(&h, y_last, NT, 0));
+  DevBuf d_run;
+  RC(dalloc(d_run, 8));
+  MT_CUDA_CHECK(cudaMemset(d_run.p, 0, 8));
+  KTimer kt;
+  kt.init(true);
+  for (u64 s = 0; s < nseg; s++)
+    RC(mt_sieve2_run(h, Y0 + s * R, NT, d_run.as<int64_t>(), nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, &kt));
+  MT_CUDA_CHECK(cudaDeviceSynchronize());
+  kt.drain();
+  for (int c = 0; c < KT_NCLASS; c++) ms_out[c] = kt.ms[c];
+  return MT_OK;
+}
+
 // ============================================================================
 // backend-protocol: apply_block / finalize / divisor arrays
 // ============================================================================

@@ -17,19 +17,23 @@
 //   presieve = three L2-resident byte patterns added word-wise on load:
 //              W1 (2,3,5,7 logs; 0x80 at 4,9,25,49; period 485100),
 //              W2 (11,13,17,19,23; period 1062347), W3 (29,31,37,41; 1363783)
-//   in-tile  = primes 43 <= p <= 2^17 (warp per prime below 1024, thread per
+//   in-tile  = primes 43 <= p <= 2^17 (warp per prime below 1024, lane per
 //              prime above) and squares p^2 for 11 <= p <= 362 (shared-memory
-//              byte adds / ORs on 32-bit words)
+//              byte reductions, red.shared.add / .or, on the cell's 32-bit word)
 //   buckets  = primes p > 2^17 and squares p^2 > 2^17: a producer kernel per
-//              segment enumerates every hit and appends (offset, value) to a
-//              producer-private list per tile (shared-memory cursors, no global
+//              segment enumerates every hit (balanced in chunks of hits) and
+//              appends (offset, log) to a producer-private list per tile, square
+//              flags from the list's back (shared-memory cursors, no global
 //              atomics); the tile kernel applies its lists.  A list that would
 //              overflow its capacity is recomputed exactly by the tile (slow path)
 //   classify = SIMD within a word (4 cells), warp-parallel over words; 32-cell
 //              chunk sums -> block scan -> tile total
-//   scan     = decoupled look-back across the tiles of a launch (tile order from
-//              an atomic ticket), seeded with the running M before the segment,
-//              so captures M(floor(n/j)) are written absolute in the same pass
+//   CTAs     = persistent: CTA c sieves 4 contiguous tiles of the segment and
+//              carries every in-tile prime's next multiple from tile to tile in
+//              shared memory, so a prime costs one division per CTA, not per tile
+//   scan     = tile sums -> one-block scan seeded with the running M; captures
+//              M(floor(n/j)) and the head's 32K block bases are written
+//              tile-relative and made absolute by a fixup pass (k_s3_fixup)
 #include <cstdio>
 
 #include "mt_common.cuh"
@@ -39,25 +43,9 @@
 #define S2_W (S2_T / 4)          // words per tile
 #define S2_NT 1024               // threads per tile CTA
 #define S2_CH (S2_T / 32)        // 32-cell chunks per tile
-
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// look-back word: status in bits 62-63 (1 = aggregate, 2 = inclusive prefix), value in 0..61
-#define LB_AGG 1ull
-#define LB_INC 2ull
-__device__ __forceinline__ unsigned long long lb_pack(unsigned long long st, long long v) {
-  return (st << 62) | ((unsigned long long)v & ((1ull << 62) - 1));
-}
-__device__ __forceinline__ long long lb_val(unsigned long long w) {
-  return ((long long)(w << 2)) >> 2;
-}
+#ifndef S2_BSPLIT
+#define S2_BSPLIT 0              // lane-per-prime loops: 1 = split at 2^14, 0 = one loop
+#endif
 
 __device__ __forceinline__ void red_add(u32 saddr, u32 v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
@@ -65,13 +53,6 @@ __device__ __forceinline__ void red_add(u32 saddr, u32 v) {
 __device__ __forceinline__ void red_or(u32 saddr, u32 v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
-// bucket entry: offset (17 bits) | value << 17; value bit 7 = square flag (OR)
-__device__ __forceinline__ void apply_entry(u32 sbase, u32 e) {
-  const u32 j = e & 0x1FFFFu, v = e >> 17, sh = (j & 3) * 8;
-  if (v & 0x80u) red_or(sbase + (j & ~3u), 0x80u << sh);
-  else red_add(sbase + (j & ~3u), v << sh);
-}
-
 // (-Y) mod p for p < 2^32, Y < 2^53, with r = 1/p rounded (host: 1.0/p)
 __device__ __forceinline__ u32 neg_mod(u64 Y, double Yd, double r, u32 p) {
   u64 q = qdiv64(Yd, r, Y, p);
@@ -85,66 +66,71 @@ __device__ __forceinline__ u32 neg_mod(u64 Y, double Yd, double r, u32 p) {
 // list of its tile.  Entry = offset (17 bits) | value << 17 (value bit 7 = OR).
 // ----------------------------------------------------------------------------
 // Work is balanced by hits, not by primes: small primes hit the segment up
-// to 16x more often than large ones, so each round first computes every
-// prime's first hit and hit count (one prime per thread), then deals the hits
-// out in chunks of FCH consecutive multiples over all threads.
-#define FBATCH 2048  // primes per round
-#define FCH 8        // hits per chunk
+// to 16x more often than large ones.  Each round takes FBATCH of this
+// producer's primes, computes every prime's first hit and hit count (one
+// prime per thread), cuts the hit runs into items of at most FITEM
+// consecutive multiples, lists the items in shared memory, and lets the warps
+// take 32 items at a time (lane per item).  Slots in a tile's list come from
+// shared-memory counters (returning atomics run at ~9 lanes/clk/SM on B200).
+#define FBATCH 1024  // primes per round
+#define FITEM 64     // hits per item
+#define FMAXIT 8192  // items per round (shared-memory list)
 __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
-  extern __shared__ u32 cnt[];  // [ntiles]
-  __shared__ u64 s_q0[FBATCH];
+  extern __shared__ u32 cnt[];  // [ntiles] log entries (front), then [ntiles] squares (back)
+  u32* cnt2 = cnt + a.ntiles;
+  __shared__ u32 s_q0[FBATCH];
   __shared__ u32 s_step[FBATCH];
   __shared__ u32 s_val[FBATCH];
-  __shared__ u32 s_off[FBATCH + 1];  // exclusive scan of chunk counts
+  __shared__ u32 s_item[FMAXIT];  // k | chunk << 16
   __shared__ u32 s_wsum[32];
+  __shared__ u32 s_nitems, s_next;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 b = blockIdx.x, NP = gridDim.x;
-  for (u32 t = tid; t < a.ntiles; t += blockDim.x) cnt[t] = 0;
-  const u64 Y0 = a.Y0, R = (u64)a.ntiles * S2_T;
+  for (u32 t = tid; t < 2 * a.ntiles; t += blockDim.x) cnt[t] = 0;
+  const u64 Y0 = a.Y0;
+  const u32 R = a.ntiles * S2_T;  // <= 2^31
   const double Yd = (double)Y0;
   u32* __restrict__ out = a.buf + (u64)b * a.ntiles * a.cap;
   const u32 cap = a.cap;
-  // this producer's items: log primes p_lo + b + k*NP, then squares q_lo + b + k*NP
+  // this producer's primes: log marks p_lo + b + k*NP, then squares q_lo + b + k*NP
   const u32 nlog = a.p_hi > a.p_lo + b ? (a.p_hi - a.p_lo - b + NP - 1) / NP : 0;
   const u32 nsq = a.q_hi > a.q_lo + b ? (a.q_hi - a.q_lo - b + NP - 1) / NP : 0;
-  const u32 nitems = nlog + nsq;
-  for (u32 base = 0; base < nitems; base += FBATCH) {
+  const u32 nprim = nlog + nsq;
+  for (u32 base = 0; base < nprim; base += FBATCH) {
     __syncthreads();
-    // phase 1: first hit, step, value and chunk count of 2 items per thread
-    u32 c[2];
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const u32 k = base + tid * 2 + h;
-      c[h] = 0;
-      if (k >= nitems || tid * 2 + h >= FBATCH) continue;
-      u64 q0, step;
-      u32 val;
-      if (k < nlog) {
-        const u64 i = (u64)a.p_lo + b + (u64)k * NP;
-        const u32 p = a.primes[i];
-        q0 = neg_mod(Y0, Yd, a.rprimes[i], p);
-        if (Y0 == 0 && q0 == 0) q0 = p;  // y = 0 is never marked
-        step = p;
-        val = (u32)a.logs[i] << 17;
-      } else {
-        const u64 i = (u64)a.q_lo + b + (u64)(k - nlog) * NP;
-        const u64 p = a.primes[i];
-        const u64 q = p * p;
-        const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Y0, q);
-        const u64 rem = Y0 - qq * q;
-        q0 = rem ? q - rem : (Y0 ? 0 : q);
-        step = q;
-        val = 0x80u << 17;
+    // phase 1: first hit, step, value, item count of one prime per thread
+    u32 c = 0;
+    {
+      const u32 k = base + tid;
+      if (k < nprim && tid < FBATCH) {
+        u32 q0 = R, step = 1, val = 0;
+        if (k < nlog) {
+          const u64 i = (u64)a.p_lo + b + (u64)k * NP;
+          const u32 p = a.primes[i];
+          q0 = neg_mod(Y0, Yd, a.rprimes[i], p);
+          if (Y0 == 0 && q0 == 0) q0 = p;  // y = 0 is never marked
+          step = p;
+          val = (u32)a.logs[i] << 17;
+        } else {
+          const u64 i = (u64)a.q_lo + b + (u64)(k - nlog) * NP;
+          const u64 p = a.primes[i];
+          const u64 q = p * p;
+          const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Y0, q);
+          const u64 rem = Y0 - qq * q;
+          const u64 f = rem ? q - rem : (Y0 ? 0 : q);
+          q0 = f < R ? (u32)f : R;
+          step = q < R ? (u32)q : R;  // one hit at most when q >= R
+          val = 0x80u << 17;
+        }
+        const u32 hits = q0 < R ? (R - 1 - q0) / step + 1 : 0;
+        c = (hits + FITEM - 1) / FITEM;
+        s_q0[tid] = q0;
+        s_step[tid] = step;
+        s_val[tid] = val;
       }
-      const u64 hits = q0 < R ? (R - 1 - q0) / step + 1 : 0;
-      c[h] = (u32)((hits + FCH - 1) / FCH);
-      s_q0[tid * 2 + h] = q0;
-      s_step[tid * 2 + h] = step > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)step;  // R <= 2^31: one hit at most
-      s_val[tid * 2 + h] = val;
     }
-    // block exclusive scan of chunk counts (2 per thread)
-    const u32 tsum = c[0] + c[1];
-    u32 incl = tsum;
+    // block exclusive scan of item counts
+    u32 incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
@@ -161,48 +147,75 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
         if (lane >= o) ix += t;
       }
       s_wsum[lane] = ix - x;
-      if (lane == 31) s_off[FBATCH] = ix;
+      if (lane == 31) { s_nitems = ix; s_next = 0; }
     }
     __syncthreads();
     {
-      const u32 e = s_wsum[warp] + incl - tsum;
-      if (tid * 2 < FBATCH) s_off[tid * 2] = e;
-      if (tid * 2 + 1 < FBATCH) s_off[tid * 2 + 1] = e + c[0];
+      const u32 e = s_wsum[warp] + incl - c;
+      for (u32 q = 0; q < c && e + q < FMAXIT; q++) s_item[e + q] = tid | (q << 16);
     }
     __syncthreads();
-    const u32 nb = min((u32)FBATCH, nitems - base);
-    const u32 total = s_off[FBATCH];
-    // phase 2: chunks of FCH hits over all threads
-    for (u32 g = tid; g < total; g += blockDim.x) {
-      u32 lo = 0, hi = nb;  // largest k with s_off[k] <= g
-      while (hi - lo > 1) {
-        const u32 mid = (lo + hi) >> 1;
-        if (s_off[mid] <= g) lo = mid; else hi = mid;
-      }
-      const u32 ci = g - s_off[lo];
-      const u64 step = s_step[lo];
-      const u32 val = s_val[lo];
-      u64 pos = s_q0[lo] + (u64)ci * FCH * step;
-#pragma unroll
-      for (int h = 0; h < FCH; h++) {
-        if (pos < R) {
-          const u32 t = (u32)(pos >> 17);
-          const u32 sl = atomicAdd(&cnt[t], 1u);
-          if (sl < cap) out[(u64)t * cap + sl] = (u32)(pos & (S2_T - 1)) | val;
+    const u32 nit = s_nitems;
+    // items beyond the shared list (only if a batch has > FMAXIT items) are
+    // processed by their owner thread after the shared list
+    for (;;) {
+      u32 i0 = 0;
+      if (lane == 0) i0 = atomicAdd(&s_next, 32u);
+      i0 = __shfl_sync(0xffffffffu, i0, 0);
+      if (i0 >= min(nit, (u32)FMAXIT)) break;
+      const u32 it = i0 + lane;
+      if (it < min(nit, (u32)FMAXIT)) {
+        const u32 w = s_item[it];
+        const u32 k = w & 0xFFFF, ci = w >> 16;
+        const u32 step = s_step[k], val = s_val[k];
+        u32 pos = s_q0[k] + ci * FITEM * step;
+        const u32 end = (u32)min((u64)R, (u64)pos + (u64)FITEM * step);
+        if (!(val & (0x80u << 17))) {
+          for (; pos < end; pos += step) {
+            const u32 t = pos >> 17;
+            const u32 sl = atomicAdd(&cnt[t], 1u);
+            if (sl < cap) out[t * cap + sl] = (pos & (S2_T - 1)) | val;
+          }
+        } else {  // square flags fill each list from the back
+          for (; pos < end; pos += step) {
+            const u32 t = pos >> 17;
+            const u32 sl = atomicAdd(&cnt2[t], 1u);
+            if (sl < cap) out[t * cap + (cap - 1 - sl)] = pos & (S2_T - 1);
+          }
         }
-        pos += step;
+      }
+    }
+    if (nit > FMAXIT) {  // overflowed item list: owners finish their own remaining items
+      const u32 e = s_wsum[warp] + incl - c;
+      for (u32 q = 0; q < c; q++) {
+        if (e + q < FMAXIT) continue;
+        const u32 step = s_step[tid], val = s_val[tid];
+        u32 pos = s_q0[tid] + q * FITEM * step;
+        const u32 end = (u32)min((u64)R, (u64)pos + (u64)FITEM * step);
+        for (; pos < end; pos += step) {
+          const u32 t = pos >> 17;
+          if (!(val & (0x80u << 17))) {
+            const u32 sl = atomicAdd(&cnt[t], 1u);
+            if (sl < cap) out[t * cap + sl] = (pos & (S2_T - 1)) | val;
+          } else {
+            const u32 sl = atomicAdd(&cnt2[t], 1u);
+            if (sl < cap) out[t * cap + (cap - 1 - sl)] = pos & (S2_T - 1);
+          }
+        }
       }
     }
   }
   __syncthreads();
-  for (u32 t = tid; t < a.ntiles; t += blockDim.x) a.counts[(u64)b * a.ntiles + t] = cnt[t];
+  for (u32 t = tid; t < a.ntiles; t += blockDim.x) {
+    const u32 nl = cnt[t], ns = cnt2[t];
+    // overflow (nl + ns > cap) is flagged by an all-ones count
+    a.counts[(u64)b * a.ntiles + t] = (nl + ns > cap || nl > 0xFFFF || ns > 0xFFFF) ? 0xFFFFFFFFu : (nl | (ns << 16));
+  }
 }
 
 // ----------------------------------------------------------------------------
 // tile kernel
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ void mark_add(u32* st, u32 j, u32 v) { atomicAdd(&st[j >> 2], v << ((j & 3) * 8)); }
-__device__ __forceinline__ void mark_or(u32* st, u32 j) { atomicOr(&st[j >> 2], 0x80u << ((j & 3) * 8)); }
 
 // mu of the 4 cells of a state word (uniform threshold thr): packed int8 and their sum
 __device__ __forceinline__ u32 mu_word(u32 w, u32 kthr, int& sum) {
@@ -219,300 +232,6 @@ __device__ __forceinline__ int mu_cell(u32 s, int thr) {
   if (s & 0x80) return 0;
   int par = s & 1;
   return ((int)s > thr) ? 1 - 2 * par : 2 * par - 1;
-}
-
-__global__ void __launch_bounds__(S2_NT, 1) k_sieve2(Sieve2Args a) {
-  extern __shared__ u32 st[];                   // S2_W state / mu words
-  int* csum = (int*)(st + S2_W);                // S2_CH chunk sums -> exclusive chunk prefixes
-  __shared__ int wsum[32];
-  __shared__ u32 s_tile;
-  __shared__ long long s_excl;
-  __shared__ int s_total;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
-  __syncthreads();
-  const u32 tile = s_tile;
-  const u64 Yt = a.Y0 + (u64)tile * S2_T;
-  const double Yd = (double)Yt;
-
-  // 1. presieve patterns
-  {
-    const u32* __restrict__ w1 = a.w1 + (u32)((Yt % a.w1_period4) >> 2);
-    const u32* __restrict__ w2 = a.w2 + (u32)((Yt % a.w2_period4) >> 2);
-    const u32* __restrict__ w3 = a.w3 + (u32)((Yt % a.w3_period4) >> 2);
-    for (int i = tid; i < (int)S2_W; i += S2_NT) st[i] = w1[i] + w2[i] + w3[i];
-  }
-  __syncthreads();
-
-  // 2.+3. marks, statically dealt to the 32 warps (no queue):
-  //   A  warp per prime, 43 <= p < 1024, snake order (balances the large early primes)
-  //   B  32 consecutive primes 1024 <= p <= big_min, lane per prime, groups round-robin
-  //   C  warp per square p^2, 11 <= p <= 362
-  //   D  bucket lists (primes > big_min, squares > 2^17), round-robin
-  // Marks are shared-memory reductions (red.shared) on the 32-bit word of the cell.
-  {
-    const u32 sbase = (u32)__cvta_generic_to_shared(st);
-    const u32 nA = a.p_warp_end - a.p_first;
-    for (u32 r = 0; r * 32 < nA; r++) {
-      const u32 k = r * 32 + ((r & 1) ? 31 - warp : warp);
-      if (k >= nA) continue;
-      const u32 i = a.p_first + k;
-      const u32 p = a.primes[i];
-      const u32 lg = a.logs[i];
-      u32 j0 = neg_mod(Yt, Yd, a.rprimes[i], p);
-      if (Yt == 0 && j0 == 0) j0 = p;
-      // step 32p keeps the byte lane: one shifted value, word index += 8p
-      const u32 j = j0 + lane * p;
-      const u32 v = lg << ((j & 3) * 8);
-      const u32 astep = 32 * p;  // bytes
-#pragma unroll 4
-      for (u32 ad = sbase + (j & ~3u); ad < sbase + S2_T; ad += astep) red_add(ad, v);
-    }
-    const u32 nB = (a.p_small_end - a.p_warp_end + 31) / 32;
-    for (u32 g = warp; g < nB; g += 32) {
-      const u32 i = a.p_warp_end + g * 32 + lane;
-      if (i < a.p_small_end) {
-        const u32 p = a.primes[i];
-        const u32 lg = a.logs[i];
-        u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
-        if (Yt == 0 && j == 0) j = p;
-        // four consecutive multiples cycle through the four byte lanes (p odd):
-        // their shifted values are loop-invariant and each address steps by 4p
-        const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p;
-        const u32 v0 = lg << ((j & 3) * 8), v1 = lg << ((j1 & 3) * 8);
-        const u32 v2 = lg << ((j2 & 3) * 8), v3 = lg << ((j3 & 3) * 8);
-        const u32 end = sbase + S2_T, st4 = 4 * p;
-        u32 a0 = sbase + (j & ~3u), a1 = sbase + (j1 & ~3u), a2 = sbase + (j2 & ~3u), a3 = sbase + (j3 & ~3u);
-        for (; a0 < end; a0 += st4, a1 += st4, a2 += st4, a3 += st4) {
-          red_add(a0, v0);
-          if (a1 < end) red_add(a1, v1);
-          if (a2 < end) red_add(a2, v2);
-          if (a3 < end) red_add(a3, v3);
-        }
-      }
-    }
-    for (u32 i = a.sq_first + warp; i < a.sq_end; i += 32) {
-      const u32 p = a.primes[i];
-      const u32 q = p * p;
-      u32 j0 = neg_mod(Yt, Yd, __drcp_rn((double)q), q);
-      if (Yt == 0 && j0 == 0) j0 = q;
-      for (u32 j = j0 + lane * q; j < S2_T; j += 32 * q) red_or(sbase + (j & ~3u), 0x80u << ((j & 3) * 8));
-    }
-    if (a.nprod) {
-      for (u32 b0 = 0; b0 < a.nprod; b0 += 32 * 32) {
-        // counts of this warp's next (up to) 32 lists: list b0 + warp + 32*l in lane l
-        const u32 bl = b0 + warp + 32 * lane;
-        const u32 nl = bl < a.nprod ? a.counts[(u64)bl * a.ntiles + tile] : 0u;
-        for (u32 l = 0; l < 32; l++) {
-          const u32 b = b0 + warp + 32 * l;
-          if (b >= a.nprod) break;
-          const u32 n = __shfl_sync(0xffffffffu, nl, l);
-          const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
-          if (n <= a.cap) {
-            for (u32 k = lane; k < n; k += 128) {
-              const u32 e0 = L[k];
-              const u32 e1 = k + 32 < n ? L[k + 32] : 0u;
-              const u32 e2 = k + 64 < n ? L[k + 64] : 0u;
-              const u32 e3 = k + 96 < n ? L[k + 96] : 0u;
-              apply_entry(sbase, e0);
-              apply_entry(sbase, e1);
-              apply_entry(sbase, e2);
-              apply_entry(sbase, e3);
-            }
-          } else {  // overflowed list: this producer's hits on the tile, recomputed exactly
-            if (lane == 0) atomicAdd(a.overflow, 1ull);
-            for (u64 i = (u64)a.p_lo + b + (u64)lane * a.nprod; i < a.p_hi; i += 32ull * a.nprod) {
-              const u32 p = a.primes[i];
-              u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
-              if (Yt == 0 && j == 0) j = p;
-              for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), (u32)a.logs[i] << ((j & 3) * 8));
-            }
-            for (u64 i = (u64)a.q_lo + b + (u64)lane * a.nprod; i < a.q_hi; i += 32ull * a.nprod) {
-              const u64 p = a.primes[i];
-              const u64 q = p * p;
-              const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Yt, q);
-              const u64 rem = Yt - qq * q;
-              const u64 j = rem ? q - rem : (Yt ? 0 : q);
-              if (j < S2_T) red_or(sbase + ((u32)j & ~3u), 0x80u << (((u32)j & 3) * 8));
-            }
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-
-  if (a.states_out) {  // instrumented export (debug)
-    u32* so = (u32*)(a.states_out + (u64)tile * S2_T);
-    for (int i = tid; i < (int)S2_W; i += S2_NT) so[i] = st[i];
-    __syncthreads();
-  }
-
-  // 4. classify: warp w owns words [w*1024, (w+1)*1024); per iteration lane l
-  //    takes the 4 words base + 4l .. 4l+3 (16 cells, half a 32-cell chunk)
-  {
-    const bool uniform = Yt >= S2_T;
-    const int thr_t = 62 - __clzll((long long)(Yt | 1));  // floor(log2 Yt) - 1
-    const u32 kthr = uniform ? (u32)(127 - thr_t) * 0x01010101u : 0u;
-    uint4* st4 = (uint4*)st;
-#pragma unroll 2
-    for (int it = 0; it < 8; it++) {
-      const int q = warp * 256 + it * 32 + lane;  // uint4 index
-      uint4 w = st4[q];
-      int s = 0;
-      if (uniform) {
-        w.x = mu_word(w.x, kthr, s);
-        w.y = mu_word(w.y, kthr, s);
-        w.z = mu_word(w.z, kthr, s);
-        w.w = mu_word(w.w, kthr, s);
-      } else {
-        u32* wv = (u32*)&w;
-        for (int k = 0; k < 4; k++) {
-          u32 mw = 0;
-          for (int bb = 0; bb < 4; bb++) {
-            const u64 y = Yt + (u64)(q * 4 + k) * 4 + bb;
-            const int thr = (y ? 63 - __clzll((long long)y) : 0) - 1;
-            const int m = mu_cell((wv[k] >> (8 * bb)) & 0xff, thr);
-            s += m;
-            mw |= ((u32)(m & 0xff)) << (8 * bb);
-          }
-          wv[k] = mw;
-        }
-      }
-      st4[q] = w;
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      if (!(lane & 1)) csum[q >> 1] = s;
-    }
-  }
-  __syncthreads();
-  // 5. block exclusive scan of the S2_CH = 4096 chunk sums (4 per thread)
-  {
-    int v0 = csum[tid * 4], v1 = csum[tid * 4 + 1], v2 = csum[tid * 4 + 2], v3 = csum[tid * 4 + 3];
-    int tsum = v0 + v1 + v2 + v3;
-    int incl = tsum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      int x = wsum[lane], ix = x;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(0xffffffffu, ix, o);
-        if (lane >= o) ix += t;
-      }
-      wsum[lane] = ix - x;
-      if (lane == 31) s_total = ix;
-    }
-    __syncthreads();
-    int e = wsum[warp] + incl - tsum;
-    csum[tid * 4] = e;
-    csum[tid * 4 + 1] = e + v0;
-    csum[tid * 4 + 2] = e + v0 + v1;
-    csum[tid * 4 + 3] = e + v0 + v1 + v2;
-  }
-  __syncthreads();
-
-  // 6. decoupled look-back: absolute M(Yt - 1)
-  if (warp == 0) {
-    const int total = s_total;
-    unsigned long long* ts = a.tstate;
-    long long excl = 0;
-    if (tile == 0) {
-      excl = *a.running;
-      if (lane == 0) st_release(&ts[0], lb_pack(LB_INC, excl + total));
-    } else {
-      if (lane == 0) st_release(&ts[tile], lb_pack(LB_AGG, total));
-      long long acc = 0;
-      long long look = (long long)tile - 1;
-      for (;;) {
-        const long long idx = look - lane;
-        unsigned long long w = idx >= 0 ? ld_acquire(&ts[idx]) : lb_pack(LB_INC, 0);
-        unsigned long long stt = w >> 62;
-        // wait until every lane's predecessor has published something
-        if (__any_sync(0xffffffffu, stt == 0)) continue;
-        const unsigned inc_mask = __ballot_sync(0xffffffffu, stt == LB_INC);
-        const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;  // nearest inclusive
-        long long v = (lane <= first_inc) ? lb_val(w) : 0;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        acc += v;
-        if (inc_mask) break;
-        look -= 32;
-      }
-      excl = acc;
-      if (lane == 0) st_release(&ts[tile], lb_pack(LB_INC, excl + total));
-    }
-    if (lane == 0) {
-      s_excl = excl;
-      if (tile == a.ntiles - 1) *a.running = excl + total;
-      if (a.tile_sum) a.tile_sum[tile] = total;
-    }
-  }
-  __syncthreads();
-  const long long E = s_excl;
-
-  // 7. head outputs: mu bytes, M16 relative to each 32K block, block bases
-  if (a.mu_out) {
-    u32* mo = (u32*)(a.mu_out + (u64)tile * S2_T);
-    for (int i = tid; i < (int)S2_W; i += S2_NT) mo[i] = st[i];
-  }
-  if (a.m16_out) {
-    if (tid < 4) a.bk[(u64)tile * 4 + tid] = E + csum[tid * 1024];  // chunk 1024*q starts block q
-    // thread per chunk (4 chunks per thread): prefix within the chunk
-    int16_t* m16 = a.m16_out + (u64)tile * S2_T;
-    for (int c = tid; c < (int)S2_CH; c += S2_NT) {
-      const int bstart = csum[(c >> 10) << 10];
-      int run = csum[c] - bstart;
-      const u32* wp = st + c * 8;
-      uint4 o[4];
-      u32* ov = (u32*)o;
-#pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const u32 w = wp[k];
-        const int c0 = run + (int)(int8_t)(w & 0xff);
-        const int c1 = c0 + (int)(int8_t)((w >> 8) & 0xff);
-        const int c2 = c1 + (int)(int8_t)((w >> 16) & 0xff);
-        const int c3 = c2 + (int)(int8_t)(w >> 24);
-        ov[2 * k] = (u32)(uint16_t)c0 | ((u32)(uint16_t)c1 << 16);
-        ov[2 * k + 1] = (u32)(uint16_t)c2 | ((u32)(uint16_t)c3 << 16);
-        run = c3;
-      }
-      uint4* dst = (uint4*)(m16 + (u64)c * 32);
-#pragma unroll
-      for (int k = 0; k < 4; k++) dst[k] = o[k];
-    }
-  }
-
-  // 8. quotient captures Q_t[j] = M(floor(n_t / j)) for floor(n_t/j) in this tile
-  for (int t = 0; t < a.n_cap; t++) {
-    const CaptureTarget2& ct = a.caps[t];
-    u64 jhi = Yt ? udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt) : ~0ull;
-    u64 jlo = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt + S2_T) + 1;
-    if (jlo < ct.jq0) jlo = ct.jq0;
-    if (jhi > ct.jq1) jhi = ct.jq1;
-    for (u64 j = jlo + tid; j <= jhi; j += S2_NT) {
-      const u64 y = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, j);
-      const u32 o = (u32)(y - Yt);
-      const int c = o >> 5;
-      const u32* wp = st + (c << 3);
-      int s = 0;
-      const u32 last = o & 31;
-      for (u32 k = 0; k <= (last >> 2); k++) {
-        u32 w = wp[k];
-        if (k == (last >> 2)) {
-          const u32 keep = (last & 3) + 1;
-          w = keep == 4 ? w : (w & ((1u << (8 * keep)) - 1));
-        }
-        s = __dp4a((int)w, 0x01010101, s);
-      }
-      ct.Q[j - ct.jq0] = (int)(E + csum[c] + s);
-    }
-  }
 }
 
 // ----------------------------------------------------------------------------
@@ -603,17 +322,17 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
       __syncwarp();
       if (lane == 0) { const u32 tm = tmA[k]; offA[k] = j0 >= tm ? j0 - tm : j0 + p - tm; }
     }
-    // B: lane per prime, groups of 32 in snake order
+#if S2_BSPLIT == 0
+    // B: lane per prime, groups of 32 in snake order (single loop, predicated tail)
     {
-      const u32 nB = (nBp + 31) / 32;
-      for (u32 r = 0; r * 32 < nB; r++) {
+      const u32 nG = (nBp + 31) / 32;
+      for (u32 r = 0; r * 32 < nG; r++) {
         const u32 g = r * 32 + ((r & 1) ? 31 - warp : warp);
-        if (g >= nB) continue;
+        if (g >= nG) continue;
         const u32 k = g * 32 + lane;
         if (k < nBp) {
-          const u32 i = a.p_warp_end + k;
-          const u32 p = a.primes[i];
-          const u32 lg = a.logs[i];
+          const u32 p = a.primes[a.p_warp_end + k];
+          const u32 lg = (32 - __clz(p - 1)) | 1;
           u32 j = offB[k];
           const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p, p4 = 4 * p;
           const u32 v0 = lg << ((j & 3) * 8), v1 = lg << ((j1 & 3) * 8);
@@ -625,12 +344,59 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
             red_add_if(a2, v2, send);
             red_add_if(a3, v3, send);
           }
-          // first multiple beyond the tile: j (loop exit) minus the multiples past the end
           while (j >= S2_T + p) j -= p;
           offB[k] = j - S2_T;
         }
       }
     }
+#else
+    // B1: lane per prime (p < 2^14, >= 8 marks), four multiples per step; groups
+    //     of 32 consecutive primes in snake order over the warps
+    const u32 nB1 = a.p_mid - a.p_warp_end;
+    {
+      const u32 nG = (nB1 + 31) / 32;
+      for (u32 r = 0; r * 32 < nG; r++) {
+        const u32 g = r * 32 + ((r & 1) ? 31 - warp : warp);
+        if (g >= nG) continue;
+        const u32 k = g * 32 + lane;
+        if (k < nB1) {
+          const u32 p = a.primes[a.p_warp_end + k];
+          const u32 lg = (32 - __clz(p - 1)) | 1;  // ceil(log2 p) | 1
+          u32 j = offB[k];
+          const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p, p4 = 4 * p;
+          const u32 v0 = lg << ((j & 3) * 8), v1 = lg << ((j1 & 3) * 8);
+          const u32 v2 = lg << ((j2 & 3) * 8), v3 = lg << ((j3 & 3) * 8);
+          u32 a0 = sbase + (j & ~3u), a1 = sbase + (j1 & ~3u), a2 = sbase + (j2 & ~3u), a3 = sbase + (j3 & ~3u);
+          // full groups of four, then the (at most three) remaining multiples
+          for (; a3 < send; a0 += p4, a1 += p4, a2 += p4, a3 += p4, j += p4) {
+            red_add(a0, v0);
+            red_add(a1, v1);
+            red_add(a2, v2);
+            red_add(a3, v3);
+          }
+          for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), lg << ((j & 3) * 8));
+          offB[k] = j - S2_T;
+        }
+      }
+    }
+    // B2: lane per prime (2^14 <= p <= big_min, <= 8 marks), plain loop
+    {
+      const u32 nB2 = a.p_small_end - a.p_mid;
+      const u32 nG = (nB2 + 31) / 32;
+      for (u32 r = 0; r * 32 < nG; r++) {
+        const u32 g = r * 32 + ((r & 1) ? 31 - warp : warp);
+        if (g >= nG) continue;
+        const u32 k = g * 32 + lane;
+        if (k < nB2) {
+          const u32 p = a.primes[a.p_mid + k];
+          const u32 lg = (32 - __clz(p - 1)) | 1;
+          u32 j = offB[nB1 + k];
+          for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), lg << ((j & 3) * 8));
+          offB[nB1 + k] = j - S2_T;
+        }
+      }
+    }
+#endif
     // C: warp per small square
     for (u32 k = warp; k < nC; k += 32) {
       const u32 p = a.primes[a.sq_first + k], q = p * p;
@@ -648,18 +414,23 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         for (u32 l = 0; l < 32; l++) {
           const u32 b = b0 + warp + 32 * l;
           if (b >= a.nprod) break;
-          const u32 n = __shfl_sync(0xffffffffu, nl, l);
+          const u32 cw = __shfl_sync(0xffffffffu, nl, l);
           const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
-          if (n <= a.cap) {
-            for (u32 k = lane; k < n; k += 128) {
+          if (cw != 0xFFFFFFFFu) {
+            const u32 n = cw & 0xFFFF, nsq = cw >> 16;
+            for (u32 k = lane; k < n; k += 128) {  // log entries (front)
               const u32 e0 = L[k];
               const u32 e1 = k + 32 < n ? L[k + 32] : 0u;
               const u32 e2 = k + 64 < n ? L[k + 64] : 0u;
               const u32 e3 = k + 96 < n ? L[k + 96] : 0u;
-              apply_entry(sbase, e0);
-              apply_entry(sbase, e1);
-              apply_entry(sbase, e2);
-              apply_entry(sbase, e3);
+              red_add(sbase + (e0 & 0x1FFFCu), (e0 >> 17) << ((e0 & 3) * 8));
+              red_add(sbase + (e1 & 0x1FFFCu), (e1 >> 17) << ((e1 & 3) * 8));
+              red_add(sbase + (e2 & 0x1FFFCu), (e2 >> 17) << ((e2 & 3) * 8));
+              red_add(sbase + (e3 & 0x1FFFCu), (e3 >> 17) << ((e3 & 3) * 8));
+            }
+            for (u32 k = lane; k < nsq; k += 32) {  // square flags (back)
+              const u32 e = L[a.cap - 1 - k];
+              red_or(sbase + (e & 0x1FFFCu), 0x80u << ((e & 3) * 8));
             }
           } else {  // overflowed list: this producer's hits on the tile, recomputed exactly
             if (lane == 0) atomicAdd(a.overflow, 1ull);
@@ -873,7 +644,7 @@ int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
   Sieve2Args a = g.tile;
   if (a.nprod) {
     Bucket2Args b = g.bucket;
-    const size_t bs = (size_t)b.ntiles * sizeof(u32);
+    const size_t bs = 2 * (size_t)b.ntiles * sizeof(u32);
     if (kt) kt->begin(KT_SIEVE_LARGE, st);
     k_bucket_fill<<<b.nprod_grid, 1024, bs, st>>>(b);
     if (kt) kt->end(st);
@@ -1061,6 +832,7 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
   a.p_first = std::min(idx_gt(42), end);
   a.p_warp_end = std::max(a.p_first, std::min(idx_gt(1023), end));
   a.p_small_end = std::max(a.p_warp_end, std::min(idx_gt(h->big_min), end));
+  a.p_mid = std::max(a.p_warp_end, std::min(idx_gt(16383), a.p_small_end));
   a.sq_first = std::min(idx_gt(10), end);
   a.sq_end = std::max(a.sq_first, std::min(idx_gt(362), end));
   a.p_lo = a.p_small_end; a.p_hi = end;

@@ -72,6 +72,38 @@ __global__ void k_lrand(int words, int n, uint32_t* out) {
   atomicAdd(out, s);
 }
 
+// returning smem atomics vs match.any-based warp aggregation (slot allocation)
+__global__ void k_atoms_ret(int n, uint32_t* out) {
+  __shared__ uint32_t cnt[1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  uint32_t x = blockIdx.x * 1315423911u + threadIdx.x * 2654435761u, acc = 0;
+  for (int i = 0; i < n; i++) {
+    x = x * 1664525u + 1013904223u;
+    acc += atomicAdd(&cnt[(x >> 8) % 592], 1u);
+  }
+  if (acc == 0x12345678) out[0] = acc;
+}
+__global__ void k_match(int n, uint32_t* out) {
+  __shared__ uint16_t cnt[32][600];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = lane; i < 600; i += 32) cnt[w][i] = 0;
+  __syncwarp();
+  uint32_t x = blockIdx.x * 1315423911u + threadIdx.x * 2654435761u, acc = 0;
+  for (int i = 0; i < n; i++) {
+    x = x * 1664525u + 1013904223u;
+    const uint32_t t = (x >> 8) % 592;
+    const uint32_t m = __match_any_sync(0xffffffffu, t);
+    const uint32_t rank = __popc(m & ((1u << lane) - 1));
+    const uint32_t base = cnt[w][t];
+    __syncwarp();
+    if (rank == __popc(m) - 1) cnt[w][t] = (uint16_t)(base + __popc(m));
+    __syncwarp();
+    acc += base + rank;
+  }
+  if (acc == 0x12345678) out[0] = acc;
+}
+
 int main() {
   int dev = 0, nsm, clk;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -128,6 +160,25 @@ int main() {
     cudaEventElapsedTime(&ms, a, b);
     double tot = (double)nsm * threads * n;
     printf("local random atomics: %.3f ops/clk/SM %s\n", tot / (ms * 1e-3) / nsm / (ghz * 1e9), cudaGetErrorString(cudaGetLastError()));
+  }
+  {
+    int n = 4096, threads = 1024;
+    k_atoms_ret<<<nsm, threads>>>(n, d_out);
+    cudaEventRecord(a);
+    k_atoms_ret<<<nsm, threads>>>(n, d_out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("returning smem atomics: %.3f lanes/clk/SM\n", (double)nsm * threads * n / (ms * 1e-3) / nsm / (ghz * 1e9));
+    k_match<<<nsm, threads>>>(n, d_out);
+    cudaEventRecord(a);
+    k_match<<<nsm, threads>>>(n, d_out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    printf("match.any slot allocation: %.3f lanes/clk/SM %s\n", (double)nsm * threads * n / (ms * 1e-3) / nsm / (ghz * 1e9),
+           cudaGetErrorString(cudaGetLastError()));
   }
   for (int C : {2, 4, 8, 16}) {
     for (int ro = 0; ro < 2; ro++) {
