@@ -76,8 +76,8 @@ __device__ __forceinline__ u32 neg_mod(u64 Y, double Yd, double r, u32 p) {
 #define FITEM 64     // hits per item
 #define FMAXIT 8192  // items per round (shared-memory list)
 __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
-  extern __shared__ u32 cnt[];  // [ntiles] log entries (front), then [ntiles] squares (back)
-  u32* cnt2 = cnt + a.ntiles;
+  extern __shared__ u32 cnt[];  // [ntiles + 1] log entries (front; + dummy), then [ntiles] squares (back)
+  u32* cnt2 = cnt + a.ntiles + 1;
   __shared__ u32 s_q0[FBATCH];
   __shared__ u32 s_step[FBATCH];
   __shared__ u32 s_val[FBATCH];
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
   __shared__ u32 s_nitems, s_next;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 b = blockIdx.x, NP = gridDim.x;
-  for (u32 t = tid; t < 2 * a.ntiles; t += blockDim.x) cnt[t] = 0;
+  for (u32 t = tid; t < 2 * a.ntiles + 1; t += blockDim.x) cnt[t] = 0;
   const u64 Y0 = a.Y0;
   const u32 R = a.ntiles * S2_T;  // <= 2^31
   const double Yd = (double)Y0;
@@ -171,10 +171,20 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
         u32 pos = s_q0[k] + ci * FITEM * step;
         const u32 end = (u32)min((u64)R, (u64)pos + (u64)FITEM * step);
         if (!(val & (0x80u << 17))) {
-          for (; pos < end; pos += step) {
-            const u32 t = pos >> 17;
-            const u32 sl = atomicAdd(&cnt[t], 1u);
-            if (sl < cap) out[t * cap + sl] = (pos & (S2_T - 1)) | val;
+          // four independent slot allocations in flight; hits past `end` count
+          // into the dummy counter cnt[ntiles]
+          for (; pos < end; pos += 4 * step) {
+            u32 t[4], sl[4];
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+              const u32 ph = pos + h * step;
+              t[h] = ph < end ? ph >> 17 : a.ntiles;
+            }
+#pragma unroll
+            for (int h = 0; h < 4; h++) sl[h] = atomicAdd(&cnt[t[h]], 1u);
+#pragma unroll
+            for (int h = 0; h < 4; h++)
+              if (t[h] < a.ntiles && sl[h] < cap) out[t[h] * cap + sl[h]] = ((pos + h * step) & (S2_T - 1)) | val;
           }
         } else {  // square flags fill each list from the back
           for (; pos < end; pos += step) {
@@ -644,7 +654,7 @@ int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
   Sieve2Args a = g.tile;
   if (a.nprod) {
     Bucket2Args b = g.bucket;
-    const size_t bs = 2 * (size_t)b.ntiles * sizeof(u32);
+    const size_t bs = (2 * (size_t)b.ntiles + 1) * sizeof(u32);
     if (kt) kt->begin(KT_SIEVE_LARGE, st);
     k_bucket_fill<<<b.nprod_grid, 1024, bs, st>>>(b);
     if (kt) kt->end(st);
