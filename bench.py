@@ -317,30 +317,40 @@ def main():
     dom = max(kms, key=lambda k: kms[k])
     avg_ms = kms[dom] / max(1, kcnt[dom])
     roof = {"kernel": dom}
-    seg_tail = 1 << 27
+    nsm = torch.cuda.get_device_properties(local).multi_processor_count
+    seg = nsm * 4 * (1 << 17)  # default segment: 4 tiles of 2^17 cells per SM (mt_engine.cu)
     if dom in ("sieve_tile", "sieve_large"):
         # 10 algorithmic bytes per y-value (state write+read 2 B, M(y) 8 B)
-        ys_per_launch = (stats_last["n_tail_segments"] * seg_tail + stats_last["n_head_segments"] * (1 << 24)) \
+        ys_per_launch = (stats_last["n_tail_segments"] + stats_last["n_head_segments"]) * seg \
             / max(1, kcnt[dom] / args.steps)
         A = 10 * ys_per_launch / (avg_ms * 1e-3) / 1e9
         P_ = pk.get("hbm_gbs", 6650.0)
+        tr = _ncu_traffic(dom)
         roof |= {"bound": "hbm", "achieved": A, "peak": P_, "unit": "GB/s", "frac": A / P_,
-                 "traffic": _ncu_traffic(dom), "per_unit": "10 B per y-value (SURVEY.md §8(d))",
+                 "traffic": tr, "per_unit": "10 B per y-value (SURVEY.md §8(d))",
                  "units_per_launch": ys_per_launch, "avg_launch_ms": avg_ms,
-                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"}
+                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in pk else "fallback",
+                 "note": ("the sieve keeps its state in shared memory: measured DRAM traffic per launch (ncu, "
+                          "profiles/traffic.json) is far below the 10 B/y accounting, so frac > 1; the kernel is "
+                          "bound by shared-memory reductions and issue (profiles/)")}
     else:
         ops = 7 * stats_last["counted_items"] + 4 * stats_last["dense_items"]
         A = ops / (kms[dom] / args.steps * 1e-3) / 1e12
         roof |= {"bound": "int", "achieved": A, "peak": 18.56, "unit": "Tops/s", "frac": A / 18.56,
                  "traffic": None}
-    # the update kernel against the INT-pipe roofline (7 IMAD/counted pair)
+    # the counted walk against its issue roofline: one exact division per squarefree m
+    # (6/pi^2 of the reference's counted pairs); peak = the microbenchmarked inner loop
+    # (14.15 items/clk/SM, profiles/r01_microbench.txt) x SMs x max clock
     upd_ms = kms.get("counted", 0.0) / args.steps
     upd = None
     if upd_ms > 0:
-        A = 7 * stats_last["counted_items"] / (upd_ms * 1e-3) / 1e12
-        upd = {"kernel": "counted", "bound": "int", "achieved": A, "peak": 18.56, "unit": "T IMAD-op/s",
-               "frac": A / 18.56, "per_unit": "7 IMAD-pipe ops per counted pair (SURVEY.md §8(d))",
-               "peak_source": "profiles/r01_microbench.txt (32-bit IMAD chains, 148 SMs @ 1965 MHz)"}
+        items = 6 / 3.141592653589793 ** 2 * stats_last["counted_items"]
+        A = items / (upd_ms * 1e-3) / 1e12
+        Pk = 14.15 * nsm * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        upd = {"kernel": "counted", "bound": "issue", "achieved": A, "peak": Pk, "unit": "T items/s",
+               "frac": A / Pk, "per_unit": "one fp64-reciprocal exact division + 64-bit accumulate per squarefree m",
+               "reference_count_rate": stats_last["counted_items"] / (upd_ms * 1e-3),
+               "peak_source": "profiles/r01_microbench.txt 'counted' loop (14.15 items/clk/SM) x SMs x sm_max_mhz"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:

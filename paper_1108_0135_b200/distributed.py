@@ -130,6 +130,18 @@ def tail_offsets(m_head: int, totals) -> list[int]:
     return out
 
 
+def _staged(t, fn, group):
+    """Run collective `fn` on `t`; gloo (the CPU tests' backend) gets a host copy."""
+    import torch.distributed as dist
+
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        c = t.cpu()
+        fn(c)
+        t.copy_(c)
+    else:
+        fn(t)
+
+
 def run_phases(plan, group=None, res=None):
     """Drive one job through the plan's phases with the three exchanges.
     `plan` is a DevicePlan (or the CPU stand-in of the tests) of THIS rank."""
@@ -137,7 +149,8 @@ def run_phases(plan, group=None, res=None):
     import torch.distributed as dist
 
     rank, size = dist.get_rank(group), dist.get_world_size(group)
-    dev = getattr(plan, "device", torch.device("cpu"))
+    gloo = dist.get_backend(group) == "gloo"
+    dev = torch.device("cpu") if gloo else getattr(plan, "device", torch.device("cpu"))
     m_head, t_local = plan.sieve_update()
     tot = torch.tensor([t_local], dtype=torch.int64, device=dev)
     allt = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(size)]
@@ -148,12 +161,13 @@ def run_phases(plan, group=None, res=None):
         for r in range(size):
             view = plan.q_slice(t, r)
             if view is not None:
-                dist.broadcast(view, src=dist.get_global_rank(group, r) if group is not None else r, group=group)
+                src = dist.get_global_rank(group, r) if group is not None else r
+                _staged(view, lambda x: dist.broadcast(x, src=src, group=group), group)
     plan.sync()
     plan.gather()
     acc = plan.acc()
     if acc is not None:
-        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+        _staged(acc, lambda x: dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group), group)
     plan.sync()
     plan.resolve(res)
     return offs

@@ -268,3 +268,96 @@ def test_production_sieve_prefix(engine, oracle):
     m = np.zeros(n, np.int64)
     _lib.check(_lib.lib().mt_sieve_fast(1, n, None, _lib.ptr(m)))
     assert np.array_equal(m, oracle.mertens_table(n))
+
+
+def _two_rank_worker(rank, world, port, n, q):
+    import os as _os
+    import sys as _sys
+
+    _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
+    import numpy as _np
+    import torch
+    import torch.distributed as dist
+
+    _os.environ["MASTER_ADDR"] = "127.0.0.1"
+    _os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_1108_0135_b200 as P
+        from paper_1108_0135_b200 import _lib, distributed
+        from paper_1108_0135_b200.engine import make_job
+
+        u = P.choose_u(n)
+        cfg = P.EngineConfig(device=0, seg_log2_head=20, seg_log2_tail=20)
+        job = make_job([n], u, cfg, rank=rank, world=world)
+        plan = distributed.DevicePlan(job)
+        res = _lib.MtResult()
+        fin = _np.zeros(n // u, _np.int64)
+        res.finals = fin.ctypes.data_as(_lib._pi64)
+        distributed.run_phases(plan, None, res)
+        st = _lib.stats_dict(res.stats)
+        plan.close()
+        q.put((rank, fin.tolist(), st["tail_seg_begin"], st["tail_seg_end"]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_ranks_on_one_gpu(engine, golden, world):
+    """The multi-GPU path (plan API + run_phases: interleaved head units, split
+    tail, offsets, Q-slice broadcasts, int64 allreduce) with `world` ranks sharing
+    cuda:0 over gloo: finals identical to the single-rank job."""
+    import socket
+    import time
+
+    import torch.multiprocessing as mp
+
+    n = 10**12
+    ref = engine.mertens_exact(n)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_two_rank_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out, t0 = [], time.time()
+    while len(out) < world:
+        try:
+            out.append(q.get(timeout=5))
+        except Exception:
+            assert all(p.is_alive() or p.exitcode == 0 for p in ps), "a rank died"
+            assert time.time() - t0 < 600
+    for p in ps:
+        p.join(timeout=60)
+    segs = sorted((o[2], o[3]) for o in out)
+    assert segs[0][0] == 0 and all(segs[i][1] == segs[i + 1][0] for i in range(world - 1)) and segs[0][1] > 0
+    for rank, fin, _, _ in out:
+        assert np.array_equal(np.array(fin, np.int64), ref._final), rank
+
+
+@pytest.mark.slow
+def test_paper_1e20_128bit(engine):
+    """n >= 2^64: elements k <= 5 carry 128-bit v.  M(10^20) and,
+    from the same run, M(10^19) = quotient(10) and M(10^18) = quotient(100)."""
+    r = engine.mertens_exact(10**20)
+    assert r.value == 461113106
+    assert (r.quotient(10), r.quotient(100)) == (899990187, -46758740)
+
+
+@pytest.mark.slow
+def test_batch_extreme_1161e19(engine):
+    """C3 (reduced to 8 targets): one shared sieve for close x around the
+    paper's extreme M(11609864264058592345) = -1995900927 (PAPER.md:217-219);
+    every target agrees with its own single-target run's value relation."""
+    x = 11609864264058592345
+    ns = [x + j * 10**10 for j in range(-4, 4)]
+    mm = engine.mertens_exact_multi(ns)
+    assert mm[x].value == -1995900927
+    assert round(mm[x].ratio, 9) == -0.585767684
+    # u-invariance: a different shared sieve (4 targets) gives the same values
+    sub = engine.mertens_exact_multi(ns[2:6])
+    assert all(sub[n].value == mm[n].value for n in ns[2:6])
