@@ -268,8 +268,10 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
   u32* offB = tmA + nA;                         // first multiple, B primes
   u32* offC = offB + nBp;                       // first multiple of p^2, small squares
   u32* tmC = offC + nC;                         // T mod p^2
+  uint16_t* pB = (uint16_t*)(tmC + nC);         // B primes as (p - 1) / 2
   __shared__ int wsum[32];
   __shared__ int s_total;
+  __shared__ u32 s_dnext;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 m = a.tiles_per_cta;
   const u32 tile0 = blockIdx.x * m;
@@ -294,6 +296,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
       u32 j = neg_mod(Y, Yd, a.rprimes[i], p);
       if (Y == 0 && j == 0) j = p;
       offB[k] = j;
+      pB[k] = (uint16_t)((p - 1) >> 1);
     }
     for (u32 k = tid; k < nC; k += S2_NT) {
       const u32 p = a.primes[a.sq_first + k], q = p * p;
@@ -307,6 +310,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
   for (u32 tile = tile0; tile < tile_end; tile++) {
     const u64 Yt = a.Y0 + (u64)tile * S2_T;
     __syncthreads();  // offsets ready / previous tile's outputs done
+    if (tid == 0) s_dnext = 0;
     // 1. presieve patterns
     {
       const u32* __restrict__ w1 = a.w1 + (u32)((Yt % a.w1_period4) >> 2);
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         if (g >= nG) continue;
         const u32 k = g * 32 + lane;
         if (k < nBp) {
-          const u32 p = a.primes[a.p_warp_end + k];
+          const u32 p = 2u * pB[k] + 1u;
           const u32 lg = (32 - __clz(p - 1)) | 1;
           u32 j = offB[k];
           const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p, p4 = 4 * p;
@@ -370,7 +374,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         if (g >= nG) continue;
         const u32 k = g * 32 + lane;
         if (k < nB1) {
-          const u32 p = a.primes[a.p_warp_end + k];
+          const u32 p = 2u * pB[k] + 1u;
           const u32 lg = (32 - __clz(p - 1)) | 1;  // ceil(log2 p) | 1
           u32 j = offB[k];
           const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p, p4 = 4 * p;
@@ -415,49 +419,45 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
       __syncwarp();
       if (lane == 0) { const u32 tm = tmC[k]; offC[k] = j0 >= tm ? j0 - tm : j0 + q - tm; }
     }
-    // D: bucket lists (primes > big_min, squares > 2^17)
+    // D: bucket lists (primes > big_min, squares > 2^17), dealt to warps from a
+    //    shared counter so warps that finished A-C early take more lists
     if (a.nprod) {
       const double Yd = (double)Yt;
-      for (u32 b0 = 0; b0 < a.nprod; b0 += 32 * 32) {
-        const u32 bl = b0 + warp + 32 * lane;
-        const u32 nl = bl < a.nprod ? a.counts[(u64)bl * a.ntiles + tile] : 0u;
-        for (u32 l = 0; l < 32; l++) {
-          const u32 b = b0 + warp + 32 * l;
-          if (b >= a.nprod) break;
-          const u32 cw = __shfl_sync(0xffffffffu, nl, l);
-          const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
-          if (cw != 0xFFFFFFFFu) {
-            const u32 n = cw & 0xFFFF, nsq = cw >> 16;
-            for (u32 k = lane; k < n; k += 128) {  // log entries (front)
-              const u32 e0 = L[k];
-              const u32 e1 = k + 32 < n ? L[k + 32] : 0u;
-              const u32 e2 = k + 64 < n ? L[k + 64] : 0u;
-              const u32 e3 = k + 96 < n ? L[k + 96] : 0u;
-              red_add(sbase + (e0 & 0x1FFFCu), (e0 >> 17) << ((e0 & 3) * 8));
-              red_add(sbase + (e1 & 0x1FFFCu), (e1 >> 17) << ((e1 & 3) * 8));
-              red_add(sbase + (e2 & 0x1FFFCu), (e2 >> 17) << ((e2 & 3) * 8));
-              red_add(sbase + (e3 & 0x1FFFCu), (e3 >> 17) << ((e3 & 3) * 8));
-            }
-            for (u32 k = lane; k < nsq; k += 32) {  // square flags (back)
-              const u32 e = L[a.cap - 1 - k];
-              red_or(sbase + (e & 0x1FFFCu), 0x80u << ((e & 3) * 8));
-            }
-          } else {  // overflowed list: this producer's hits on the tile, recomputed exactly
-            if (lane == 0) atomicAdd(a.overflow, 1ull);
-            for (u64 i = (u64)a.p_lo + b + (u64)lane * a.nprod; i < a.p_hi; i += 32ull * a.nprod) {
-              const u32 p = a.primes[i];
-              u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
-              if (Yt == 0 && j == 0) j = p;
-              for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), (u32)a.logs[i] << ((j & 3) * 8));
-            }
-            for (u64 i = (u64)a.q_lo + b + (u64)lane * a.nprod; i < a.q_hi; i += 32ull * a.nprod) {
-              const u64 p = a.primes[i];
-              const u64 q = p * p;
-              const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Yt, q);
-              const u64 rem = Yt - qq * q;
-              const u64 j = rem ? q - rem : (Yt ? 0 : q);
-              if (j < S2_T) red_or(sbase + ((u32)j & ~3u), 0x80u << (((u32)j & 3) * 8));
-            }
+      for (;;) {
+        u32 b = 0;
+        if (lane == 0) b = atomicAdd(&s_dnext, 1u);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (b >= a.nprod) break;
+        const u32 cw = a.counts[(u64)b * a.ntiles + tile];
+        const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
+        if (cw != 0xFFFFFFFFu) {
+          const u32 n = cw & 0xFFFF, nsq = cw >> 16;
+          for (u32 k = lane; k < n; k += 256) {  // log entries (front), 8 loads in flight
+            u32 e[8];
+#pragma unroll
+            for (int h = 0; h < 8; h++) e[h] = k + 32 * h < n ? L[k + 32 * h] : 0u;
+#pragma unroll
+            for (int h = 0; h < 8; h++) red_add(sbase + (e[h] & 0x1FFFCu), (e[h] >> 17) << ((e[h] & 3) * 8));
+          }
+          for (u32 k = lane; k < nsq; k += 32) {  // square flags (back)
+            const u32 e = L[a.cap - 1 - k];
+            red_or(sbase + (e & 0x1FFFCu), 0x80u << ((e & 3) * 8));
+          }
+        } else {  // overflowed list: this producer's hits on the tile, recomputed exactly
+          if (lane == 0) atomicAdd(a.overflow, 1ull);
+          for (u64 i = (u64)a.p_lo + b + (u64)lane * a.nprod; i < a.p_hi; i += 32ull * a.nprod) {
+            const u32 p = a.primes[i];
+            u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
+            if (Yt == 0 && j == 0) j = p;
+            for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), (u32)a.logs[i] << ((j & 3) * 8));
+          }
+          for (u64 i = (u64)a.q_lo + b + (u64)lane * a.nprod; i < a.q_hi; i += 32ull * a.nprod) {
+            const u64 p = a.primes[i];
+            const u64 q = p * p;
+            const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Yt, q);
+            const u64 rem = Yt - qq * q;
+            const u64 j = rem ? q - rem : (Yt ? 0 : q);
+            if (j < S2_T) red_or(sbase + ((u32)j & ~3u), 0x80u << (((u32)j & 3) * 8));
           }
         }
       }
@@ -661,7 +661,7 @@ int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
     MT_CUDA_CHECK(cudaGetLastError());
   }
   const u32 nA = a.p_warp_end - a.p_first, nBp = a.p_small_end - a.p_warp_end, nC = a.sq_end - a.sq_first;
-  const size_t smem = S2_T + S2_CH * sizeof(int) + (size_t)(2 * nA + nBp + 2 * nC) * 4;
+  const size_t smem = S2_T + S2_CH * sizeof(int) + (size_t)(2 * nA + nBp + 2 * nC) * 4 + (size_t)nBp * 2 + 16;
   const u32 grid = (a.ntiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
   if (kt) kt->begin(KT_SIEVE_TILE, st);
   k_sieve3<<<grid, S2_NT, smem, st>>>(a);

@@ -318,8 +318,14 @@ __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
     const i64 base = a.bk[w];
     const bool wide = a.G.wide[g] || a.force_wide;
     __syncthreads();
-    const u64 e1 = a.G.start[g + 1];
-    for (u64 e = a.G.start[g] + tid; e < e1; e += 256) {
+    const u64 e0g = a.G.start[g], e1 = a.G.start[g + 1];
+    // groups smaller than the CTA: S = 256/A threads per element, each walking a
+    // contiguous slice of the element's d-range in this window
+    const u32 A = (u32)(e1 - e0g);
+    const u32 S = A < 256 ? 256 / A : 1;
+    const u32 slice = A < 256 ? tid / A : 0;
+    const u64 efirst = A < 256 ? e0g + tid % A : e0g + tid;
+    for (u64 e = efirst; e < e1 && slice < S; e += (A < 256 ? e1 : 256)) {
       const u64 xc = a.E.xcut[e];
       u64 lw = a.E.lo_w[e];
       const u64 sp = a.E.d_sp[e];
@@ -328,10 +334,18 @@ __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
       const u64 vlo = a.E.vlo[e], vhi = a.E.vhi[e];
       const double vd = a.E.vd[e];
       const int vb = a.E.vbits[e];
-      const u64 dh = W0 ? div_clamp(vlo, vhi, vd, vb, W0, xc) : xc;
+      u64 dh = W0 ? div_clamp(vlo, vhi, vd, vb, W0, xc) : xc;
       u64 dl = div_clamp(vlo, vhi, vd, vb, W1, xc) + 1;
       if (dl < lw) dl = lw;
       if (dh < dl) continue;
+      if (S > 1) {  // this thread's slice of [dl, dh], counted from the top
+        const u64 len = dh - dl + 1, piece = (len + S - 1) / S;
+        if ((u64)slice * piece >= len) continue;
+        const u64 top = dh - (u64)slice * piece;
+        const u64 bot = top + 1 >= piece ? top - piece + 1 : 0;
+        dh = top;
+        if (bot > dl) dl = bot;
+      }
       int s = 0;
       auto f = [&](u64 y) { s += sw[(u32)(y - W0)]; };
       if (wide) walk_quotients<true>(vlo, vhi, vd, vb, dh, dl, f);
