@@ -43,6 +43,16 @@
 #define S2_W (S2_T / 4)          // words per tile
 #define S2_NT 1024               // threads per tile CTA
 #define S2_CH (S2_T / 32)        // 32-cell chunks per tile
+#define S2_MAXPROD 512           // bucket producers whose counts are staged in shared memory
+#ifndef S2_DLOADS
+#define S2_DLOADS 2              // bucket entries in flight per lane (measured: 2 > 4 > 8)
+#endif
+#ifndef S2_DYN_D
+#define S2_DYN_D 1               // bucket lists dealt dynamically (1) or round-robin (0)
+#endif
+#ifndef S2_PB_SMEM
+#define S2_PB_SMEM 1             // B primes read from shared memory (1) or global (0)
+#endif
 #ifndef S2_BSPLIT
 #define S2_BSPLIT 0              // lane-per-prime loops: 1 = split at 2^14, 0 = one loop
 #endif
@@ -272,6 +282,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
   __shared__ int wsum[32];
   __shared__ int s_total;
   __shared__ u32 s_dnext;
+  __shared__ u32 s_cnt[S2_MAXPROD];  // this tile's bucket-list counts
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 m = a.tiles_per_cta;
   const u32 tile0 = blockIdx.x * m;
@@ -318,6 +329,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
       const u32* __restrict__ w3 = a.w3 + (u32)((Yt % a.w3_period4) >> 2);
       for (int i = tid; i < (int)S2_W; i += S2_NT) st[i] = w1[i] + w2[i] + w3[i];
     }
+    for (u32 b = tid; b < a.nprod && b < S2_MAXPROD; b += S2_NT) s_cnt[b] = a.counts[(u64)b * a.ntiles + tile];
     __syncthreads();
     // 2. marks
     // A: warp per prime, snake order over the warps
@@ -345,7 +357,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         if (g >= nG) continue;
         const u32 k = g * 32 + lane;
         if (k < nBp) {
-          const u32 p = 2u * pB[k] + 1u;
+          const u32 p = S2_PB_SMEM ? 2u * pB[k] + 1u : a.primes[a.p_warp_end + k];
           const u32 lg = (32 - __clz(p - 1)) | 1;
           u32 j = offB[k];
           const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p, p4 = 4 * p;
@@ -374,7 +386,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         if (g >= nG) continue;
         const u32 k = g * 32 + lane;
         if (k < nB1) {
-          const u32 p = 2u * pB[k] + 1u;
+          const u32 p = S2_PB_SMEM ? 2u * pB[k] + 1u : a.primes[a.p_warp_end + k];
           const u32 lg = (32 - __clz(p - 1)) | 1;  // ceil(log2 p) | 1
           u32 j = offB[k];
           const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p, p4 = 4 * p;
@@ -423,21 +435,25 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
     //    shared counter so warps that finished A-C early take more lists
     if (a.nprod) {
       const double Yd = (double)Yt;
-      for (;;) {
+      for (u32 rr = 0;; rr++) {
         u32 b = 0;
+#if S2_DYN_D
         if (lane == 0) b = atomicAdd(&s_dnext, 1u);
         b = __shfl_sync(0xffffffffu, b, 0);
+#else
+        b = warp + 32 * rr;  // round-robin: list warp + 32 i
+#endif
         if (b >= a.nprod) break;
-        const u32 cw = a.counts[(u64)b * a.ntiles + tile];
+        const u32 cw = b < S2_MAXPROD ? s_cnt[b] : a.counts[(u64)b * a.ntiles + tile];
         const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
         if (cw != 0xFFFFFFFFu) {
           const u32 n = cw & 0xFFFF, nsq = cw >> 16;
-          for (u32 k = lane; k < n; k += 256) {  // log entries (front), 8 loads in flight
-            u32 e[8];
+          for (u32 k = lane; k < n; k += 32 * S2_DLOADS) {  // log entries (front), S2_DLOADS loads in flight
+            u32 e[S2_DLOADS];
 #pragma unroll
-            for (int h = 0; h < 8; h++) e[h] = k + 32 * h < n ? L[k + 32 * h] : 0u;
+            for (int h = 0; h < S2_DLOADS; h++) e[h] = k + 32 * h < n ? L[k + 32 * h] : 0u;
 #pragma unroll
-            for (int h = 0; h < 8; h++) red_add(sbase + (e[h] & 0x1FFFCu), (e[h] >> 17) << ((e[h] & 3) * 8));
+            for (int h = 0; h < S2_DLOADS; h++) red_add(sbase + (e[h] & 0x1FFFCu), (e[h] >> 17) << ((e[h] & 3) * 8));
           }
           for (u32 k = lane; k < nsq; k += 32) {  // square flags (back)
             const u32 e = L[a.cap - 1 - k];

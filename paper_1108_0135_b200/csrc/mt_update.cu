@@ -96,7 +96,7 @@ struct CountedArgs {
 
 __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
   __shared__ double rmL[MT_CM];
-  __shared__ u32 mL[MT_CM];
+  __shared__ u32 mL[MT_CM];  // low word of m, stored NEGATED: the 32-bit remainder is one IMAD (v + q * (-m))
   __shared__ u64 s_unit;
   __shared__ int wp[MT_CT / 32], wn[MT_CT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -148,8 +148,8 @@ __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
       u64 m = m0 + b;
       if (m < mhi && mu != 0) {
         double r = __drcp_rn((double)m);
-        if (mu > 0) { rmL[op] = r; mL[op] = (u32)m; op++; }
-        else { int idx = MT_CM - 1 - on; rmL[idx] = r; mL[idx] = (u32)m; on++; }  // low word; chunks never straddle 2^32
+        if (mu > 0) { rmL[op] = r; mL[op] = 0u - (u32)m; op++; }
+        else { int idx = MT_CM - 1 - on; rmL[idx] = r; mL[idx] = 0u - (u32)m; on++; }  // low word; chunks never straddle 2^32
       }
     }
     __syncthreads();
@@ -163,10 +163,10 @@ __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
         int bp_ = totp, bn_ = totn;
         if (mc + 1 < mhi) {  // partial: count entries with m <= mc (lists ascending in m)
           int lo = 0, hi = totp;
-          while (lo < hi) { int mid = (lo + hi) >> 1; if ((mhw | mL[mid]) <= mc) lo = mid + 1; else hi = mid; }
+          while (lo < hi) { int mid = (lo + hi) >> 1; if ((mhw | (0u - mL[mid])) <= mc) lo = mid + 1; else hi = mid; }
           bp_ = lo;
           lo = 0; hi = totn;
-          while (lo < hi) { int mid = (lo + hi) >> 1; if ((mhw | mL[MT_CM - 1 - mid]) <= mc) lo = mid + 1; else hi = mid; }
+          while (lo < hi) { int mid = (lo + hi) >> 1; if ((mhw | (0u - mL[MT_CM - 1 - mid])) <= mc) lo = mid + 1; else hi = mid; }
           bn_ = lo;
         }
         const double vd = a.E.vd[e];
@@ -181,14 +181,14 @@ __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
 #pragma unroll 8
           for (int i = 0; i < bp_; i++) {
             u64 b = (u64)__double_as_longlong(fma(vd, rmL[i], MT_TWO52));
-            int t = (int)(v32 - (u32)b * mL[i]);
+            int t = (int)(v32 + (u32)b * mL[i]);
             ap += b; cp += (u32)t >> 31;
           }
 #pragma unroll 8
           for (int i = 0; i < bn_; i++) {
             int idx = MT_CM - 1 - i;
             u64 b = (u64)__double_as_longlong(fma(vd, rmL[idx], MT_TWO52));
-            int t = (int)(v32 - (u32)b * mL[idx]);
+            int t = (int)(v32 + (u32)b * mL[idx]);
             an += b; cn += (u32)t >> 31;
           }
           S = (ap - (u64)bp_ * MT_EXP52 - cp) - (an - (u64)bn_ * MT_EXP52 - cn);
@@ -198,21 +198,21 @@ __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
           u64 ap = 0, an = 0, cp = 0, cn = 0;
           for (int i = 0; i < bp_; i++) {
             u64 b = (u64)__double_as_longlong(fma(vd, rmL[i], MT_TWO52)) - MT_EXP52;
-            i64 t = (i64)(vlo - b * (mhw | mL[i]));
+            i64 t = (i64)(vlo - b * (mhw | (0u - mL[i])));
             ap += b; cp += (u64)t >> 63;
           }
           for (int i = 0; i < bn_; i++) {
             int idx = MT_CM - 1 - i;
             u64 b = (u64)__double_as_longlong(fma(vd, rmL[idx], MT_TWO52)) - MT_EXP52;
-            i64 t = (i64)(vlo - b * (mhw | mL[idx]));
+            i64 t = (i64)(vlo - b * (mhw | (0u - mL[idx])));
             an += b; cn += (u64)t >> 63;
           }
           S = (ap - cp) - (an - cn);
         } else {  // exact slow path (small m with wide v)
           const u64 vhi = a.E.vhi[e];
           u64 sp = 0, sn = 0;
-          for (int i = 0; i < bp_; i++) sp += (u64)udiv128(vlo, vhi, mhw | mL[i]);
-          for (int i = 0; i < bn_; i++) sn += (u64)udiv128(vlo, vhi, mhw | mL[MT_CM - 1 - i]);
+          for (int i = 0; i < bp_; i++) sp += (u64)udiv128(vlo, vhi, mhw | (0u - mL[i]));
+          for (int i = 0; i < bn_; i++) sn += (u64)udiv128(vlo, vhi, mhw | (0u - mL[MT_CM - 1 - i]));
           S = sp - sn;
         }
         if (bp_ + bn_) atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)S);
