@@ -783,12 +783,16 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   if (NE) k_elem_split<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, P->d_k.as<u64>(), P->d_tgt.as<uint32_t>(), P->d_J.as<u64>(), P->d_lo.as<u64>(), P->d_x.as<u64>(), P->d_low.as<u64>(), P->d_dq.as<u64>());
   if (NE) k_elem_dsp<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, P->d_vd.as<double>(), P->d_dsp.as<u64>());
   P->launches += 2;
-  // element groups for the window walk: consecutive k of one target, size clamp(k/8, 32, 1024)
+  // element groups for the window walk: consecutive k of one target, size ~clamp(k/8, 32, 1024)
   for (int i = 0; i < N; i++) {
     u64 k0 = 1;
     while (k0 <= P->K[i]) {
       P->gstart.push_back(P->e0[i] + k0 - 1);
-      k0 += std::min<u64>(1024, std::max<u64>(32, k0 / 8));
+      // power-of-two sizes: below 256 the window walk splits each element over
+      // 256/size threads, above it each thread takes size/256 elements
+      u64 gs = 32;
+      while (gs * 2 <= std::min<u64>(1024, k0 / 8)) gs *= 2;
+      k0 += gs;
     }
   }
   const u64 ng = P->ng = P->gstart.size();
