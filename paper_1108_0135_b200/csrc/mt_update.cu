@@ -260,6 +260,45 @@ __device__ __forceinline__ void walk_quotients(u64 vlo, u64 vhi, double vd, int 
   }
 }
 
+// The window walk for d < 2^30 in 32-bit registers: d, the offset of y = v/d
+// inside the window, the remainder r and the increment delta = y(d) - y(d+1)
+// all fit (y < W0 + 2^15, delta <= y/d <= 2^12 in the window-walk region).
+// The split d_sp keeps y/d^2 <= 1, so one correction of delta per step is
+// exact; a second is never needed (a rare-path loop guards it anyway).
+__device__ __forceinline__ int walk_window32(u64 vlo, u64 vhi, double vd, int vb, u64 dh64, u64 dl64, u64 W0,
+                                             u32 swbase) {
+  const double rd = __drcp_rn((double)dh64);
+  const u64 y0 = qdiv_ok(vb, dh64) ? qdiv64(vd, rd, vlo, dh64) : (u64)udiv128(vlo, vhi, dh64);
+  u32 delta = (u32)((double)y0 * rd);
+  u32 d = (u32)dh64;
+  const u32 dl = (u32)dl64;
+  u32 r = (u32)vlo - (u32)y0 * d;
+  u32 yo = (u32)(y0 - W0);  // offset in the window
+  int s = 0;
+  u32 swb = swbase;
+  for (;;) {
+    asm volatile("" : "+r"(swb));  // keep the window base live (no per-item rematerialisation)
+    short m16;
+    asm volatile("ld.shared.s16 %0, [%1];" : "=h"(m16) : "r"(swb + 2 * yo));
+    s += m16;
+    if (d == dl) break;
+    --d;
+    const int ts = (int)(r + (yo + (u32)W0) - delta * d);  // (y + r) - delta*d in (-d, 2d)
+    const int neg = ts >> 31;                                 // -1 if ts < 0
+    const int over = (int)(ts >= (int)d);                     // 1 if ts >= d
+    delta += (u32)(over + neg);
+    u32 t = (u32)(ts + ((int)d & neg) - ((int)d & -over));
+    if (t >= d) {  // never taken when y/d^2 <= 1
+      while (t >= d) {
+        if ((int)t < 0) { delta--; t += d; } else { delta++; t -= d; }
+      }
+    }
+    r = t;
+    yo += delta;
+  }
+  return s;
+}
+
 // floor(v/m) clamped to `clamp` (v may exceed 2^64)
 __device__ __forceinline__ u64 div_clamp(u64 vlo, u64 vhi, double vd, int vb, u64 m, u64 clamp) {
   if (vhi) {
@@ -300,6 +339,7 @@ struct WinArgs {
 __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
   extern __shared__ int4 smem_win[];
   int16_t* sw = (int16_t*)smem_win;
+  const u32 swbase = (u32)__cvta_generic_to_shared(sw);
   __shared__ u64 s_unit;
   const int tid = threadIdx.x;
   const u64 total = a.uoff[a.G.ng];
@@ -347,9 +387,12 @@ __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
         if (bot > dl) dl = bot;
       }
       int s = 0;
-      auto f = [&](u64 y) { s += sw[(u32)(y - W0)]; };
-      if (wide) walk_quotients<true>(vlo, vhi, vd, vb, dh, dl, f);
-      else walk_quotients<false>(vlo, vhi, vd, vb, dh, dl, f);
+      if (wide) {
+        auto f = [&](u64 y) { s += sw[(u32)(y - W0)]; };
+        walk_quotients<true>(vlo, vhi, vd, vb, dh, dl, f);
+      } else {
+        s = walk_window32(vlo, vhi, vd, vb, dh, dl, W0, swbase);
+      }
       const i64 tot = (i64)s + (i64)(dh - dl + 1) * base;
       atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)tot);
     }
