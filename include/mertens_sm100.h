@@ -38,6 +38,7 @@ extern "C" {
 #define MT_FLAG_FORCE_WIDE 1u    /* tests: 64-bit remainders / 64-bit quotient walks everywhere */
 #define MT_FLAG_FORCE_SLOWDIV 2u /* tests: exact 128/64 division in the counted walk            */
 #define MT_FLAG_TIMING 4u        /* per-kernel-class CUDA-event timing into mt_stats.kernel_ms  */
+#define MT_FLAG_CAP32 8u         /* cap_m_out / small_m_out are int32_t* (dense full quotient map) */
 
 /* last error message of the calling thread ("" if none) */
 const char* mt_last_error(void);

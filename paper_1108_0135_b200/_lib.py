@@ -45,7 +45,7 @@ class MtJob(ctypes.Structure):
     ]
 
 
-MT_FLAG_FORCE_WIDE, MT_FLAG_FORCE_SLOWDIV, MT_FLAG_TIMING = 1, 2, 4
+MT_FLAG_FORCE_WIDE, MT_FLAG_FORCE_SLOWDIV, MT_FLAG_TIMING, MT_FLAG_CAP32 = 1, 2, 4, 8
 KERNEL_CLASSES = ("sieve_tile", "sieve_large", "counted", "dwin", "dsparse", "qgather", "other", "unused")
 
 

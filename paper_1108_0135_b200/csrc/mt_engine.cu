@@ -584,12 +584,13 @@ __global__ void k_window_extent(u64 n_elem, const u64* __restrict__ vlo, const u
   atomicMax(out, (unsigned long long)(y > (u128)~0ull ? ~0ull : (u64)y));
 }
 
+template <class T>
 __global__ void k_copy_small(const int16_t* __restrict__ M16, const int64_t* __restrict__ bk, u64 Y0, u64 R,
-                             u64 ymax, int64_t* __restrict__ out) {
+                             u64 ymax, T* __restrict__ out) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   u64 y = Y0 + i;
   if (i >= R || y > ymax) return;
-  out[y] = M16[i] + bk[i / MT_BLK];
+  out[y] = (T)(M16[i] + bk[i / MT_BLK]);
 }
 
 __global__ void k_copy_caps(const int* __restrict__ Q, u64 jq0, u64 c_lo, u64 cnt, int64_t* __restrict__ out) {
@@ -641,6 +642,7 @@ struct mt_plan {
   Sieve2Host* sv = nullptr;
   DevBuf d_mu, d_m, d_bk, d_run, d_caps, d_small;
   u64 cap_c_lo = 1, cap_c_hi = 0, cap_small = 0, nsmall = 0;
+  bool cap32 = false;  // MT_FLAG_CAP32: int32 capture outputs (the dense full quotient map)
   UpdateCtx* uc = nullptr;
   KTimer kt;
   int64_t m_head = 0, tail_total = 0;
@@ -851,7 +853,8 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   if (!P->caps.empty())
     MT_CUDA_CHECK(cudaMemcpyAsync(P->d_caps.p, P->caps.data(), P->caps.size() * sizeof(CaptureTargetH), cudaMemcpyHostToDevice, st));
   P->nsmall = P->cap_small ? P->cap_small + 1 : 0;
-  RC(dalloc(P->d_small, P->nsmall * 8));
+  P->cap32 = (P->flags & MT_FLAG_CAP32) != 0;
+  RC(dalloc(P->d_small, P->nsmall * (P->cap32 ? 4 : 8)));
 
   ElemDev E;
   E.vd = P->d_vd.as<double>(); E.vlo = P->d_vlo.as<u64>(); E.vhi = P->d_vhi.as<u64>(); E.vbits = P->d_vb.as<uint8_t>();
@@ -896,7 +899,10 @@ extern "C" int mt_plan_sieve_update(mt_plan* P, int64_t* m_head, int64_t* tail_t
     P->launches += 2;
     RC(mt_update_head_segment(P->uc, Y0, P->Rh, P->d_mu.as<int8_t>(), P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), st));
     if (P->nsmall && Y0 <= P->cap_small) {
-      k_copy_small<<<(unsigned)((P->Rh + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, P->Rh, P->cap_small, P->d_small.as<int64_t>());
+      if (P->cap32)
+        k_copy_small<int32_t><<<(unsigned)((P->Rh + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, P->Rh, P->cap_small, P->d_small.as<int32_t>());
+      else
+        k_copy_small<int64_t><<<(unsigned)((P->Rh + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, P->Rh, P->cap_small, P->d_small.as<int64_t>());
       P->launches++;
     }
   }
@@ -989,7 +995,11 @@ extern "C" int mt_plan_resolve(mt_plan* P, mt_result* out) {
     MT_CUDA_CHECK(cudaMemcpyAsync(out->finals, P->d_fin.p, P->NE * 8, cudaMemcpyDeviceToHost, st));
   if (out && out->acc_out && P->NE)
     MT_CUDA_CHECK(cudaMemcpyAsync(out->acc_out, P->d_acc.p, P->NE * 8, cudaMemcpyDeviceToHost, st));
-  if (out && out->cap_m_out && P->cap_c_hi >= P->cap_c_lo) {
+  if (out && out->cap_m_out && P->cap_c_hi >= P->cap_c_lo && P->cap32) {  // int32: straight from Q
+    u64 cnt = P->cap_c_hi - P->cap_c_lo + 1;
+    if (P->cap_c_lo < P->jq0[0]) { mt_set_error("capture range below floor(n/(u+1))+1"); return MT_ERR_VALUE; }
+    MT_CUDA_CHECK(cudaMemcpyAsync(out->cap_m_out, P->tdev[0].Q + (P->cap_c_lo - P->jq0[0]), cnt * 4, cudaMemcpyDeviceToHost, st));
+  } else if (out && out->cap_m_out && P->cap_c_hi >= P->cap_c_lo) {
     u64 cnt = P->cap_c_hi - P->cap_c_lo + 1;
     if (P->cap_c_lo < P->jq0[0]) { mt_set_error("capture range below floor(n/(u+1))+1"); return MT_ERR_VALUE; }
     RC(dalloc(d_capm, cnt * 8));
@@ -997,7 +1007,7 @@ extern "C" int mt_plan_resolve(mt_plan* P, mt_result* out) {
     MT_CUDA_CHECK(cudaMemcpyAsync(out->cap_m_out, d_capm.p, cnt * 8, cudaMemcpyDeviceToHost, st));
   }
   if (out && out->small_m_out && P->nsmall)
-    MT_CUDA_CHECK(cudaMemcpyAsync(out->small_m_out, P->d_small.p, P->nsmall * 8, cudaMemcpyDeviceToHost, st));
+    MT_CUDA_CHECK(cudaMemcpyAsync(out->small_m_out, P->d_small.p, P->nsmall * (P->cap32 ? 4 : 8), cudaMemcpyDeviceToHost, st));
   MT_CUDA_CHECK(cudaStreamSynchronize(st));
   MT_CUDA_CHECK(cudaGetLastError());
   P->kt.drain();

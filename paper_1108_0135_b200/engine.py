@@ -35,6 +35,7 @@ from .sieve import ceil_sqrt
 U64_PATH_BOUND = 4 * 10**18       # the reference's cap; kept as a constant for callers
 ENGINE_N_BOUND = 1 << 75          # what this engine accepts
 _DIRECT_CUTOFF = 1024
+_DENSE_MAP_MIN = 1 << 22          # capture-all above this sqrt(n) uses the dense int32 map
 BACKEND_NAME = "sm100"
 
 
@@ -136,8 +137,12 @@ class MertensResult:
     """M(n) plus the simultaneous map c -> M(floor(n/c)) (engine.py:200-239)."""
 
     def __init__(self, n, value, u, array_final, cp_q=None, cp_m=None, stats=None, elapsed=0.0,
-                 backend=""):
+                 backend="", qmap=None, small=None):
         self.n = n
+        # dense full quotient map (capture-all mode for large n): qmap[c - K - 1] =
+        # M(n // c) for K < c <= isqrt(n), small[y] = M(y) for y <= isqrt(n)
+        self._qmap = qmap
+        self._small = small
         self.value = value
         self.u = u
         self._final = array_final
@@ -157,6 +162,14 @@ class MertensResult:
             raise ValueError("c must be >= 1")
         if self._final is not None and c <= len(self._final):
             return int(self._final[c - 1])
+        if self._qmap is not None:
+            K = len(self._final) if self._final is not None else 0
+            if c <= K + len(self._qmap):
+                return int(self._qmap[c - K - 1])
+            q = self.n // c
+            if q < len(self._small):
+                return int(self._small[q])
+            raise KeyError(f"M(n//{c}) was not captured in this run")
         q = self.n // c
         if q < 2**64:
             i = int(np.searchsorted(self._cp_q, np.uint64(q)))
@@ -239,7 +252,7 @@ def make_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, rank=0, world
     return job
 
 
-def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None):
+def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None, cap32=False):
     """One exact job (mt_run, or the plan phases over the process group when
     one is up); returns (finals per n, cap_m, small_m, raw stats)."""
     L = _lib.require_device()
@@ -247,16 +260,19 @@ def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None)
 
     rank, world = distributed.world() if config.distributed else (0, 1)
     job = make_job(ns, u, config, cap_c, cap_small, rank, world)
+    if cap32:
+        job.flags |= _lib.MT_FLAG_CAP32
+    cdt = np.int32 if cap32 else np.int64
     K = [n // u for n in ns]
     finals = np.zeros(sum(K), dtype=np.int64)
     res = _lib.MtResult()
     res.finals = finals.ctypes.data_as(_lib._pi64)
     cap_m = small_m = None
     if cap_c is not None and cap_c[1] >= cap_c[0]:
-        cap_m = np.zeros(cap_c[1] - cap_c[0] + 1, dtype=np.int64)
+        cap_m = np.zeros(cap_c[1] - cap_c[0] + 1, dtype=cdt)
         res.cap_m_out = cap_m.ctypes.data_as(_lib._pi64)
     if cap_small:
-        small_m = np.zeros(cap_small + 1, dtype=np.int64)
+        small_m = np.zeros(cap_small + 1, dtype=cdt)
         res.small_m_out = small_m.ctypes.data_as(_lib._pi64)
     if acc_out is not None:
         res.acc_out = acc_out.ctypes.data_as(_lib._pu64)
@@ -306,6 +322,15 @@ def mertens_exact(n: int, config: EngineConfig | None = None) -> MertensResult:
         return _mertens_direct(n, config, t0)
     u = choose_u(n, 1, config.mem_budget, config.u_alpha)
     K = n // u
+    s = isqrt(n)
+    if s + K <= config.quotient_budget and s > _DENSE_MAP_MIN:
+        # capture-all (engine.py:242-252) as a dense map instead of ~2*sqrt(n)
+        # (q, M) pairs: M(n//c) for K < c <= s from the quotient table, M(y) for
+        # y <= s from the head sieve, both int32 (|M(y)| < 2^31 for y <= u)
+        finals, qmap, small, raw = _run_job([n], u, config, (K + 1, s), s, cap32=True)
+        st = _stats_from(raw, u, n, config)
+        return MertensResult(n, int(finals[0][0]), u, finals[0], stats=st, elapsed=time.perf_counter() - t0,
+                             backend=BACKEND_NAME, qmap=qmap, small=small)
     if n < 2**64:
         cp_q = _quotient_targets(n, K, u, config.quotient_budget)
     else:  # quotient values beyond 2^64 cannot be held in the uint64 capture array
@@ -400,6 +425,19 @@ def mertens_naive(n: int, config: EngineConfig | None = None, checkpoints=None):
 def mertens_identity_residual(result: MertensResult) -> int:
     """sum_{x=1..n} M(floor(n/x)) - 1 over the quotient map (engine.py:606-616)."""
     n = result.n
+    if result._qmap is not None and n < 2**63:  # dense map: vectorised over c <= isqrt(n) and y <= isqrt(n)
+        s = isqrt(n)
+        K = len(result._final)
+        c = np.arange(1, s + 1, dtype=np.int64)
+        q = n // c
+        mult_c = n // q - n // (q + 1)  # number of x with floor(n/x) = q
+        mc = np.concatenate([result._final.astype(np.int64), result._qmap.astype(np.int64)])[:s]
+        tot = int((mult_c * mc).sum())
+        ymax = min(int(q[-1]) - 1, s)  # quotients below floor(n/s); y in (s, n//s) has multiplicity 0
+        y = np.arange(1, ymax + 1, dtype=np.int64)
+        mult_y = n // y - n // (y + 1)
+        tot += int((mult_y * result._small[1:ymax + 1].astype(np.int64)).sum())
+        return tot - 1
     total = 0
     for _, q, m in result.quotients():
         total += (n // q - (n // (q + 1) if q < n else 0)) * m

@@ -361,3 +361,23 @@ def test_batch_extreme_1161e19(engine):
     # u-invariance: a different shared sieve (4 targets) gives the same values
     sub = engine.mertens_exact_multi(ns[2:6])
     assert all(sub[n].value == mm[n].value for n in ns[2:6])
+
+
+def test_dense_full_quotient_map(engine, oracle):
+    """Capture-all for large n (north_star: M(n) and ALL M(floor(n/c))): the
+    dense int32 map covers every c; pinned by the identity sum over the whole
+    map (engine.py:606-616), the oracle's M table for y <= sqrt(n), and
+    independent runs at sampled c."""
+    from math import isqrt
+
+    n = 10**14
+    r = engine.mertens_exact(n, engine.EngineConfig(quotient_budget=10**9))
+    assert r.value == -875575 and r._qmap is not None
+    s = isqrt(n)
+    assert np.array_equal(r._small[1:].astype(np.int64), oracle.mertens_table(s))
+    assert engine.mertens_identity_residual(r) == 0
+    K = len(r._final)
+    rng = np.random.default_rng(7)
+    for c in [K + 1, s] + [int(x) for x in rng.integers(K + 1, s, size=6)]:
+        assert r.quotient(c) == engine.mertens_exact(n // c).value, c
+    assert r.quotient(10) == engine.mertens_exact(10**13).value == 599582

@@ -120,3 +120,20 @@ def test_errors_hierarchy():
     assert issubclass(E.ResourceLimitError, E.MertensError)
     with pytest.raises(ValueError):
         P.mertens_exact(0)
+
+
+def test_dense_map_identity_residual(oracle):
+    """The vectorised identity sum over a dense quotient map (capture-all mode)
+    is 0 on a map built from the oracle, and detects a single wrong value."""
+    from math import isqrt
+
+    n = 10**8 + 12345
+    r = oracle.mertens_exact(n)
+    s, K = isqrt(n), len(r.final)
+    small = np.concatenate([[0], oracle.mertens_table(s)]).astype(np.int32)
+    qmap = np.array([r.quotient(c) for c in range(K + 1, s + 1)], np.int32)
+    R = PE.MertensResult(n, r.value, r.u, r.final, qmap=qmap, small=small)
+    assert P.mertens_identity_residual(R) == 0
+    assert R.quotient(K + 5) == r.quotient(K + 5) and R.quotient(n // 7) == small[7]
+    qmap[3] += 1
+    assert P.mertens_identity_residual(R) != 0
