@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -831,7 +832,9 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   // default segment = 4 tiles per SM (the persistent sieve CTAs each take 4 contiguous tiles)
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P->device);
-  const u64 seg_default = (u64)nsm * 4 * MT_S2_TILE;
+  u64 tiles_per_sm = 4;
+  if (const char* e = getenv("MT_SEG_TILES_PER_SM")) tiles_per_sm = strtoull(e, nullptr, 10);
+  const u64 seg_default = (u64)nsm * tiles_per_sm * MT_S2_TILE;
   P->Rh = job->seg_log2_head ? 1ull << job->seg_log2_head : seg_default;
   P->Rt = job->seg_log2_tail ? 1ull << job->seg_log2_tail : seg_default;
   const u64 Rh = P->Rh, Rt = P->Rt;
