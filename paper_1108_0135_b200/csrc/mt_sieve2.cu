@@ -364,14 +364,22 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
           const u32 v0 = lg << ((j & 3) * 8), v1 = lg << ((j1 & 3) * 8);
           const u32 v2 = lg << ((j2 & 3) * 8), v3 = lg << ((j3 & 3) * 8);
           u32 a0 = sbase + (j & ~3u), a1 = sbase + (j1 & ~3u), a2 = sbase + (j2 & ~3u), a3 = sbase + (j3 & ~3u);
+          // streams past the tile end add into a per-lane scratch word (csum[lane],
+          // rewritten by the classify pass) instead of branching around the reduction
+          const u32 scratch = send + 4 * lane;  // csum[lane]: one word per lane, no contention
           for (; a0 < send; a0 += p4, a1 += p4, a2 += p4, a3 += p4, j += p4) {
             red_add(a0, v0);
-            red_add_if(a1, v1, send);
-            red_add_if(a2, v2, send);
-            red_add_if(a3, v3, send);
+            red_add(a1 < send ? a1 : scratch, v1);
+            red_add(a2 < send ? a2 : scratch, v2);
+            red_add(a3 < send ? a3 : scratch, v3);
           }
-          while (j >= S2_T + p) j -= p;
-          offB[k] = j - S2_T;
+          // j is stream 0's next multiple; the first multiple past the tile is
+          // one of j - 3p .. j (three conditional steps, no division)
+          u32 jn = j;
+          jn = jn - p >= S2_T && jn >= p ? jn - p : jn;
+          jn = jn - p >= S2_T && jn >= p ? jn - p : jn;
+          jn = jn - p >= S2_T && jn >= p ? jn - p : jn;
+          offB[k] = jn - S2_T;
         }
       }
     }
