@@ -35,8 +35,10 @@ import numpy as np  # noqa: E402
 
 BASE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
 METRIC = BASE["metric"]
+# Table 1; 10^21 sign corrected (the table prints +3395895277; see
+# tests/test_explicit_formula_check.py and profiles/r01_paper_e21_*.json)
 PAPER = {10**16: -3195437, 10**17: -21830254, 10**18: -46758740, 10**19: 899990187,
-         10**20: 461113106, 10**21: 3395895277, 10**22: -2061910120,
+         10**20: 461113106, 10**21: -3395895277, 10**22: -2061910120,
          11609864264058592345: -1995900927}
 
 

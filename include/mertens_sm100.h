@@ -170,6 +170,17 @@ int mt_run(const mt_job* job, mt_result* out);
 typedef struct mt_plan mt_plan;
 int mt_plan_create(const mt_job* job, mt_plan** out);
 int mt_plan_sieve_update(mt_plan* p, int64_t* m_head, int64_t* tail_total);
+/* phase 1 in steps (checkpointing): the head on the first call, then at most
+ * max_tail_segments tail segments per call; *done = 1 when the tail is
+ * complete, and then m_head / tail_total are written as by sieve_update */
+int mt_plan_sieve_step(mt_plan* p, uint64_t max_tail_segments, int* done, int64_t* m_head,
+                       int64_t* tail_total);
+/* checkpoint / resume of a single-target, single-rank plan between sieve steps:
+ * the reference's MERTCKP1 header (engine.py:646-680; version 2 = this engine)
+ * followed by the accumulators, M(mcut), the quotient table, the small
+ * captures and the running prefix.  Written to path.tmp, then renamed. */
+int mt_plan_checkpoint(mt_plan* p, const char* path);
+int mt_plan_restore(mt_plan* p, const char* path);
 int mt_plan_tail_offset(mt_plan* p, int64_t offset);
 int mt_plan_q_slice(mt_plan* p, uint32_t target, uint32_t rank, void** dptr, uint64_t* count);
 int mt_plan_acc(mt_plan* p, void** dptr, uint64_t* count);

@@ -103,6 +103,9 @@ def lib():
         "mt_run": [ctypes.POINTER(MtJob), ctypes.POINTER(MtResult)],
         "mt_plan_create": [ctypes.POINTER(MtJob), ctypes.POINTER(ctypes.c_void_p)],
         "mt_plan_sieve_update": [vp, _pi64, _pi64],
+        "mt_plan_sieve_step": [vp, _u64, ctypes.POINTER(ctypes.c_int), _pi64, _pi64],
+        "mt_plan_checkpoint": [vp, ctypes.c_char_p],
+        "mt_plan_restore": [vp, ctypes.c_char_p],
         "mt_plan_tail_offset": [vp, ctypes.c_int64],
         "mt_plan_q_slice": [vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(ctypes.c_void_p), _pu64],
         "mt_plan_acc": [vp, ctypes.POINTER(ctypes.c_void_p), _pu64],
@@ -152,7 +155,8 @@ EXPORTED_SYMBOLS = (
     "mt_last_error", "mt_abi_version", "mt_device_count", "mt_set_device",
     "mt_sieve_logprime", "mt_logprime_states", "mt_sieve_naive", "mt_apply_block",
     "mt_finalize", "mt_build_divisor_arrays", "mt_mertens_range", "mt_mertens_at", "mt_sieve_fast", "mt_sieve_bench", "mt_run",
-    "mt_plan_create", "mt_plan_sieve_update", "mt_plan_tail_offset", "mt_plan_q_slice", "mt_plan_acc",
+    "mt_plan_create", "mt_plan_sieve_update", "mt_plan_sieve_step", "mt_plan_checkpoint", "mt_plan_restore",
+    "mt_plan_tail_offset", "mt_plan_q_slice", "mt_plan_acc",
     "mt_plan_gather", "mt_plan_resolve", "mt_plan_destroy",
 )
 

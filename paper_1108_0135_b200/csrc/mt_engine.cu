@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -650,6 +651,8 @@ struct mt_plan {
   double ms_setup = 0, ms_head = 0, ms_tail = 0, ms_gather = 0, ms_fin = 0;
   cudaEvent_t ev[6] = {};
   int phase = 0;  // 1 after sieve_update, 2 after tail_offset, 3 after gather
+  bool head_done = false;
+  u64 tseg_next = 0;  // next tail segment of this rank (resumable phase 1)
   ~mt_plan() {
     if (device >= 0) cudaSetDevice(device);
     mt_update_destroy(uc);
@@ -886,50 +889,196 @@ extern "C" int mt_plan_create(const mt_job* job, mt_plan** out) {
 extern "C" void mt_plan_destroy(mt_plan* p) { delete p; }
 
 // phase 1: head (sieve + this rank's share of the updates) and this rank's tail segments
-extern "C" int mt_plan_sieve_update(mt_plan* P, int64_t* m_head, int64_t* tail_total) {
+// phase 1, resumable: the head (on the first step) and up to max_tail_segments
+// of this rank's tail segments per call; *done = 1 once the tail is complete
+extern "C" int mt_plan_sieve_step(mt_plan* P, uint64_t max_tail_segments, int* done, int64_t* m_head,
+                                  int64_t* tail_total) {
   PLAN_DEV(P);
   cudaStream_t st = P->st;
-  P->kt.reset();
-  MT_CUDA_CHECK(cudaMemsetAsync(P->d_acc.p, 0, P->NE * 8, st));
-  MT_CUDA_CHECK(cudaMemsetAsync(P->d_mmc.p, 0, P->NE * 4, st));
-  MT_CUDA_CHECK(cudaMemsetAsync(P->d_run.p, 0, 8, st));
-  MT_CUDA_CHECK(cudaEventRecord(P->ev[0], st));
-  for (u64 s = 0; s < P->head_segs; s++) {
-    const u64 Y0 = s * P->Rh;
-    RC(mt_sieve2_run(P->sv, Y0, (uint32_t)(P->Rh / MT_S2_TILE), P->d_run.as<int64_t>(), P->d_mu.as<int8_t>(),
-                     P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), nullptr,
-                     (const CaptureTarget2*)P->d_caps.p, (int)P->caps.size(), st, &P->kt));
-    P->launches += 2;
-    RC(mt_update_head_segment(P->uc, Y0, P->Rh, P->d_mu.as<int8_t>(), P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), st));
-    if (P->nsmall && Y0 <= P->cap_small) {
-      if (P->cap32)
-        k_copy_small<int32_t><<<(unsigned)((P->Rh + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, P->Rh, P->cap_small, P->d_small.as<int32_t>());
-      else
-        k_copy_small<int64_t><<<(unsigned)((P->Rh + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, P->Rh, P->cap_small, P->d_small.as<int64_t>());
-      P->launches++;
+  if (!P->head_done) {
+    P->kt.reset();
+    MT_CUDA_CHECK(cudaMemsetAsync(P->d_acc.p, 0, P->NE * 8, st));
+    MT_CUDA_CHECK(cudaMemsetAsync(P->d_mmc.p, 0, P->NE * 4, st));
+    MT_CUDA_CHECK(cudaMemsetAsync(P->d_run.p, 0, 8, st));
+    MT_CUDA_CHECK(cudaEventRecord(P->ev[0], st));
+    for (u64 s = 0; s < P->head_segs; s++) {
+      const u64 Y0 = s * P->Rh;
+      RC(mt_sieve2_run(P->sv, Y0, (uint32_t)(P->Rh / MT_S2_TILE), P->d_run.as<int64_t>(), P->d_mu.as<int8_t>(),
+                       P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), nullptr,
+                       (const CaptureTarget2*)P->d_caps.p, (int)P->caps.size(), st, &P->kt));
+      P->launches += 2;
+      RC(mt_update_head_segment(P->uc, Y0, P->Rh, P->d_mu.as<int8_t>(), P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), st));
+      if (P->nsmall && Y0 <= P->cap_small) {
+        if (P->cap32)
+          k_copy_small<int32_t><<<(unsigned)((P->Rh + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, P->Rh, P->cap_small, P->d_small.as<int32_t>());
+        else
+          k_copy_small<int64_t><<<(unsigned)((P->Rh + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, P->Rh, P->cap_small, P->d_small.as<int64_t>());
+        P->launches++;
+      }
     }
+    int64_t mh = 0;
+    MT_CUDA_CHECK(cudaMemcpyAsync(&mh, P->d_run.p, 8, cudaMemcpyDeviceToHost, st));
+    MT_CUDA_CHECK(cudaMemsetAsync(P->d_run.p, 0, 8, st));  // tail prefixes are rank-local
+    MT_CUDA_CHECK(cudaEventRecord(P->ev[1], st));
+    MT_CUDA_CHECK(cudaStreamSynchronize(st));
+    float f = 0;
+    cudaEventElapsedTime(&f, P->ev[0], P->ev[1]);
+    P->ms_head = f;
+    P->ms_tail = 0;
+    P->m_head = mh;
+    P->tseg_next = P->tseg0;
+    P->head_done = true;
   }
-  int64_t mh = 0, tt = 0;
-  MT_CUDA_CHECK(cudaMemcpyAsync(&mh, P->d_run.p, 8, cudaMemcpyDeviceToHost, st));
-  MT_CUDA_CHECK(cudaMemsetAsync(P->d_run.p, 0, 8, st));  // tail prefixes are rank-local
-  MT_CUDA_CHECK(cudaEventRecord(P->ev[1], st));
-  for (u64 s = P->tseg0; s < P->tseg1; s++) {
-    RC(mt_sieve2_run(P->sv, P->tail_y0(s), (uint32_t)(P->Rt / MT_S2_TILE), P->d_run.as<int64_t>(), nullptr,
-                     nullptr, nullptr, nullptr, (const CaptureTarget2*)P->d_caps.p, (int)P->caps.size(), st,
-                     &P->kt));
-    P->launches += 2;
+  const u64 room = P->tseg1 > P->tseg_next ? P->tseg1 - P->tseg_next : 0;
+  const u64 s_end = P->tseg_next + std::min<u64>(room, max_tail_segments);
+  if (P->tseg_next < s_end) {
+    MT_CUDA_CHECK(cudaEventRecord(P->ev[1], st));
+    for (u64 s = P->tseg_next; s < s_end; s++) {
+      RC(mt_sieve2_run(P->sv, P->tail_y0(s), (uint32_t)(P->Rt / MT_S2_TILE), P->d_run.as<int64_t>(), nullptr,
+                       nullptr, nullptr, nullptr, (const CaptureTarget2*)P->d_caps.p, (int)P->caps.size(), st,
+                       &P->kt));
+      P->launches += 2;
+    }
+    MT_CUDA_CHECK(cudaEventRecord(P->ev[2], st));
+    MT_CUDA_CHECK(cudaStreamSynchronize(st));
+    float f = 0;
+    cudaEventElapsedTime(&f, P->ev[1], P->ev[2]);
+    P->ms_tail += f;
+    P->tseg_next = s_end;
   }
-  MT_CUDA_CHECK(cudaMemcpyAsync(&tt, P->d_run.p, 8, cudaMemcpyDeviceToHost, st));
-  MT_CUDA_CHECK(cudaEventRecord(P->ev[2], st));
-  MT_CUDA_CHECK(cudaStreamSynchronize(st));
   MT_CUDA_CHECK(cudaGetLastError());
-  P->m_head = mh; P->tail_total = tt;
-  if (m_head) *m_head = mh;
-  if (tail_total) *tail_total = tt;
-  float f = 0;
-  cudaEventElapsedTime(&f, P->ev[0], P->ev[1]); P->ms_head = f;
-  cudaEventElapsedTime(&f, P->ev[1], P->ev[2]); P->ms_tail = f;
-  P->phase = 1;
+  *done = P->tseg_next >= P->tseg1;
+  if (*done) {
+    int64_t tt = 0;
+    MT_CUDA_CHECK(cudaMemcpy(&tt, P->d_run.p, 8, cudaMemcpyDeviceToHost));
+    P->tail_total = tt;
+    P->phase = 1;
+    if (m_head) *m_head = P->m_head;
+    if (tail_total) *tail_total = tt;
+  }
+  return MT_OK;
+}
+
+// phase 1 in one call: head and this rank's whole tail
+extern "C" int mt_plan_sieve_update(mt_plan* P, int64_t* m_head, int64_t* tail_total) {
+  P->head_done = false;
+  int done = 0;
+  RC(mt_plan_sieve_step(P, ~0ull, &done, nullptr, nullptr));
+  if (m_head) *m_head = P->m_head;
+  if (tail_total) *tail_total = P->tail_total;
+  return MT_OK;
+}
+
+// ---- checkpoint / resume (reference MERTCKP1 header, engine.py:646-680, with
+// version 2 marking the sm100 engine state that follows it)
+#pragma pack(push, 1)
+struct CkptHead {
+  char magic[8];
+  uint32_t version, flags;
+  uint64_t n_lo, n_hi, u, next_y1, K;
+  int64_t m_running;
+  uint64_t block_len;
+};
+#pragma pack(pop)
+static_assert(sizeof(CkptHead) == 72, "MERTCKP1 header is <8sII QQ Q Q Q q Q>");
+
+static int write_dev(FILE* f, const void* dptr, u64 bytes) {
+  const u64 CH = 256ull << 20;
+  std::vector<char> h((size_t)std::min(bytes, CH));
+  for (u64 o = 0; o < bytes; o += CH) {
+    const u64 b = std::min(CH, bytes - o);
+    MT_CUDA_CHECK(cudaMemcpy(h.data(), (const char*)dptr + o, b, cudaMemcpyDeviceToHost));
+    if (fwrite(h.data(), 1, b, f) != b) { mt_set_error("checkpoint write failed"); return MT_ERR_RESOURCE; }
+  }
+  return MT_OK;
+}
+static int read_dev(FILE* f, void* dptr, u64 bytes) {
+  const u64 CH = 256ull << 20;
+  std::vector<char> h((size_t)std::min(bytes, CH));
+  for (u64 o = 0; o < bytes; o += CH) {
+    const u64 b = std::min(CH, bytes - o);
+    if (fread(h.data(), 1, b, f) != b) { mt_set_error("checkpoint truncated"); return MT_ERR_CONTRACT; }
+    MT_CUDA_CHECK(cudaMemcpy((char*)dptr + o, h.data(), b, cudaMemcpyHostToDevice));
+  }
+  return MT_OK;
+}
+
+// layout after the header: acc (K u64), M(mcut) (K i32), Q (u64 count + int32),
+// small captures (u64 count + element bytes), head M (i64) and tail running (i64)
+extern "C" int mt_plan_checkpoint(mt_plan* P, const char* path) {
+  if (P->N != 1 || P->world != 1) { mt_set_error("checkpoints cover single-target, single-rank jobs only"); return MT_ERR_CONTRACT; }
+  if (!P->head_done) { mt_set_error("checkpoint before the head is sieved"); return MT_ERR_CONTRACT; }
+  PLAN_DEV(P);
+  MT_CUDA_CHECK(cudaStreamSynchronize(P->st));
+  int64_t run = 0;
+  MT_CUDA_CHECK(cudaMemcpy(&run, P->d_run.p, 8, cudaMemcpyDeviceToHost));
+  std::string tmp = std::string(path) + ".tmp";
+  FILE* f = fopen(tmp.c_str(), "wb");
+  if (!f) { mt_set_error("cannot open %s", tmp.c_str()); return MT_ERR_RESOURCE; }
+  struct Closer { FILE* f; ~Closer() { if (f) fclose(f); } } cl{f};
+  CkptHead h{};
+  memcpy(h.magic, "MERTCKP1", 8);
+  h.version = 2;
+  h.flags = 0;
+  h.n_lo = P->n_lo[0]; h.n_hi = P->n_hi[0]; h.u = P->u;
+  h.next_y1 = P->tseg_next < P->tail_segs ? P->tail_y0(P->tseg_next) : P->y_last + 1;
+  h.K = P->K[0];
+  h.m_running = P->m_head + run;  // M(next_y1 - 1)
+  h.block_len = P->Rt;
+  if (fwrite(&h, sizeof(h), 1, f) != 1) { mt_set_error("checkpoint write failed"); return MT_ERR_RESOURCE; }
+  RC(write_dev(f, P->d_acc.p, P->NE * 8));
+  RC(write_dev(f, P->d_mmc.p, P->NE * 4));
+  const u64 qn = P->jq1[0] >= P->jq0[0] ? P->jq1[0] - P->jq0[0] + 1 : 0;
+  fwrite(&qn, 8, 1, f);
+  RC(write_dev(f, P->tdev[0].Q, qn * 4));
+  const u64 sb = P->nsmall * (P->cap32 ? 4 : 8);
+  fwrite(&sb, 8, 1, f);
+  RC(write_dev(f, P->d_small.p, sb));
+  fwrite(&P->m_head, 8, 1, f);
+  fwrite(&run, 8, 1, f);
+  fclose(f);
+  cl.f = nullptr;
+  if (rename(tmp.c_str(), path) != 0) { mt_set_error("cannot move %s into place", tmp.c_str()); return MT_ERR_RESOURCE; }
+  return MT_OK;
+}
+
+extern "C" int mt_plan_restore(mt_plan* P, const char* path) {
+  if (P->N != 1 || P->world != 1) { mt_set_error("checkpoints cover single-target, single-rank jobs only"); return MT_ERR_CONTRACT; }
+  PLAN_DEV(P);
+  FILE* f = fopen(path, "rb");
+  if (!f) { mt_set_error("cannot open %s", path); return MT_ERR_VALUE; }
+  struct Closer { FILE* f; ~Closer() { fclose(f); } } cl{f};
+  CkptHead h{};
+  if (fread(&h, sizeof(h), 1, f) != 1 || memcmp(h.magic, "MERTCKP1", 8) || h.version != 2) {
+    mt_set_error("not an sm100 checkpoint file");
+    return MT_ERR_CONTRACT;
+  }
+  if (h.n_lo != P->n_lo[0] || h.n_hi != P->n_hi[0] || h.u != P->u || h.K != P->K[0] || h.block_len != P->Rt) {
+    mt_set_error("checkpoint built for another job (n, u, K or segment size differ)");
+    return MT_ERR_CONTRACT;
+  }
+  RC(read_dev(f, P->d_acc.p, P->NE * 8));
+  RC(read_dev(f, P->d_mmc.p, P->NE * 4));
+  u64 qn = 0, sb = 0;
+  if (fread(&qn, 8, 1, f) != 1) { mt_set_error("checkpoint truncated"); return MT_ERR_CONTRACT; }
+  const u64 qn_plan = P->jq1[0] >= P->jq0[0] ? P->jq1[0] - P->jq0[0] + 1 : 0;
+  if (qn != qn_plan) { mt_set_error("checkpoint quotient table differs from this plan's"); return MT_ERR_CONTRACT; }
+  RC(read_dev(f, P->tdev[0].Q, qn * 4));
+  if (fread(&sb, 8, 1, f) != 1 || sb != P->nsmall * (P->cap32 ? 4 : 8)) { mt_set_error("checkpoint capture size differs"); return MT_ERR_CONTRACT; }
+  RC(read_dev(f, P->d_small.p, sb));
+  int64_t mh = 0, run = 0;
+  if (fread(&mh, 8, 1, f) != 1 || fread(&run, 8, 1, f) != 1) { mt_set_error("checkpoint truncated"); return MT_ERR_CONTRACT; }
+  MT_CUDA_CHECK(cudaMemcpy(P->d_run.p, &run, 8, cudaMemcpyHostToDevice));
+  P->m_head = mh;
+  P->head_done = true;
+  P->tseg_next = h.next_y1 > P->y_last ? P->tail_segs : (h.next_y1 - P->head_lim) / P->Rt;
+  if (P->tail_y0(std::min(P->tseg_next, P->tail_segs)) != h.next_y1 && h.next_y1 <= P->y_last) {
+    mt_set_error("checkpoint position is not a tail segment boundary");
+    return MT_ERR_CONTRACT;
+  }
+  P->kt.reset();
+  P->ms_head = 0;
+  P->ms_tail = 0;
   return MT_OK;
 }
 

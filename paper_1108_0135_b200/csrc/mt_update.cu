@@ -101,11 +101,15 @@ __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
   __shared__ int wp[MT_CT / 32], wn[MT_CT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u64 total = a.off[a.ntiles];
+  // thread 0 fetches the next unit while the CTA works on the current one
+  u64 nxt = 0;
+  if (tid == 0) nxt = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
   for (;;) {
-    if (tid == 0) s_unit = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
+    if (tid == 0) s_unit = nxt;
     __syncthreads();
     const u64 unit = s_unit;
     if (unit >= total) break;
+    if (tid == 0) nxt = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
     const u64 tau = upper_idx(a.off, a.ntiles + 1, unit);
     const u64 c = unit - a.off[tau];
     const u64 mlo = a.Y0 + c * MT_CM;
@@ -343,11 +347,14 @@ __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
   __shared__ u64 s_unit;
   const int tid = threadIdx.x;
   const u64 total = a.uoff[a.G.ng];
+  u64 nxt = 0;  // next unit, fetched while the current one is walked
+  if (tid == 0) nxt = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
   for (;;) {
-    if (tid == 0) s_unit = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
+    if (tid == 0) s_unit = nxt;
     __syncthreads();
     const u64 unit = s_unit;
     if (unit >= total) break;
+    if (tid == 0) nxt = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
     const u64 g = upper_idx(a.uoff, a.G.ng + 1, unit);
     const u64 w = a.wfirst[g] + (unit - a.uoff[g]);
     const u64 W0 = a.Y0 + w * MT_BLK, W1 = W0 + MT_BLK;  // [W0, W1)

@@ -21,6 +21,7 @@ the reference's own formulas, so final arrays are bit-identical.
 from __future__ import annotations
 
 import os
+import struct
 import time
 from dataclasses import dataclass, field
 from enum import IntEnum
@@ -86,6 +87,7 @@ class EngineConfig:
     engine_flags: int = 0          # MT_FLAG_FORCE_WIDE / _FORCE_SLOWDIV (tests), MT_FLAG_TIMING
     distributed: bool = True       # shard over the default torch.distributed group when one is up
     stream: int | None = None      # cudaStream_t (int) to run on; None: the engine's own
+    checkpoint_seconds: float = 300.0  # with checkpoint_path: after the head, then at most this often
 
     def effective_workers(self) -> int:
         return self.workers if self.workers > 0 else (os.cpu_count() or 1)
@@ -252,7 +254,36 @@ def make_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, rank=0, world
     return job
 
 
-def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None, cap32=False):
+def _run_checkpointed(L, job, res, config: EngineConfig, restore_from=None):
+    """Single-target job on the plan API, checkpointed after the head and then at
+    most every `checkpoint_seconds` between tail segments (the reference writes
+    after every block, engine.py:391-392; at GPU rates that would be I/O bound)."""
+    import ctypes
+
+    h = ctypes.c_void_p()
+    _lib.check(L.mt_plan_create(ctypes.byref(job), ctypes.byref(h)))
+    try:
+        path = (config.checkpoint_path or "").encode()
+        if restore_from:
+            _lib.check(L.mt_plan_restore(h, restore_from.encode()))
+        done, mh, tt = ctypes.c_int(0), ctypes.c_int64(), ctypes.c_int64()
+        last = time.perf_counter()
+        first = not restore_from
+        while not done.value:
+            _lib.check(L.mt_plan_sieve_step(h, 256, ctypes.byref(done), ctypes.byref(mh), ctypes.byref(tt)))
+            now = time.perf_counter()
+            if path and not done.value and (first or now - last >= config.checkpoint_seconds):
+                _lib.check(L.mt_plan_checkpoint(h, path))
+                last, first = now, False
+        _lib.check(L.mt_plan_tail_offset(h, mh.value))
+        _lib.check(L.mt_plan_gather(h))
+        _lib.check(L.mt_plan_resolve(h, ctypes.byref(res)))
+    finally:
+        L.mt_plan_destroy(h)
+
+
+def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None, cap32=False,
+             restore_from=None):
     """One exact job (mt_run, or the plan phases over the process group when
     one is up); returns (finals per n, cap_m, small_m, raw stats)."""
     L = _lib.require_device()
@@ -282,6 +313,8 @@ def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None,
             distributed.run_phases(plan, None, res)
         finally:
             plan.close()
+    elif (config.checkpoint_path or restore_from) and len(ns) == 1:
+        _run_checkpointed(L, job, res, config, restore_from)
     else:
         _lib.check(L.mt_run(job, res))
     out, o = [], 0
@@ -314,6 +347,10 @@ def _mertens_direct(n: int, config: EngineConfig, t0: float) -> MertensResult:
 
 def mertens_exact(n: int, config: EngineConfig | None = None) -> MertensResult:
     """M(n) and the simultaneous quotient map."""
+    return _mertens_exact(n, config)
+
+
+def _mertens_exact(n: int, config: EngineConfig | None = None, restore_from: str | None = None) -> MertensResult:
     if n < 1:
         raise ValueError("n must be >= 1")
     config = config or EngineConfig()
@@ -327,7 +364,7 @@ def mertens_exact(n: int, config: EngineConfig | None = None) -> MertensResult:
         # capture-all (engine.py:242-252) as a dense map instead of ~2*sqrt(n)
         # (q, M) pairs: M(n//c) for K < c <= s from the quotient table, M(y) for
         # y <= s from the head sieve, both int32 (|M(y)| < 2^31 for y <= u)
-        finals, qmap, small, raw = _run_job([n], u, config, (K + 1, s), s, cap32=True)
+        finals, qmap, small, raw = _run_job([n], u, config, (K + 1, s), s, cap32=True, restore_from=restore_from)
         st = _stats_from(raw, u, n, config)
         return MertensResult(n, int(finals[0][0]), u, finals[0], stats=st, elapsed=time.perf_counter() - t0,
                              backend=BACKEND_NAME, qmap=qmap, small=small)
@@ -346,7 +383,7 @@ def mertens_exact(n: int, config: EngineConfig | None = None) -> MertensResult:
         else:
             cs = np.array([n // q for q in large.tolist()], dtype=np.uint64)
         cap_c = (int(cs.min()), int(cs.max()))
-    finals, cap_m, small_m, raw = _run_job([n], u, config, cap_c, small_lim)
+    finals, cap_m, small_m, raw = _run_job([n], u, config, cap_c, small_lim, restore_from=restore_from)
     cp_m = np.zeros(len(cp_q), dtype=np.int64)
     if len(large):
         idx = (cs - np.uint64(cap_c[0])).astype(np.int64)
@@ -463,7 +500,22 @@ def verify_paired(n_max: int, samples: int, seed: int, config: EngineConfig | No
     return {"n_max": n_max, "checked": len(ns), "seed": seed, "mismatches": bad}
 
 
+_CKPT_HEAD = struct.Struct("<8sII QQ Q Q Q q Q")  # engine.py:659
+
+
 def resume_exact(path: str, config: EngineConfig | None = None) -> MertensResult:
-    """Checkpoint/resume (engine.py:646-741) is not implemented yet in the
-    B200 engine."""
-    raise ContractViolationError("checkpoint/resume is not supported by the sm100 engine yet")
+    """Continue a checkpointed run to completion (engine.py:731-741).  The file
+    carries the reference's MERTCKP1 header (version 2: this engine's state
+    follows it); u must match the one `config` derives (engine.py:697-698)."""
+    config = config or EngineConfig()
+    with open(path, "rb") as f:
+        head = f.read(_CKPT_HEAD.size)
+    if len(head) != _CKPT_HEAD.size:
+        raise ContractViolationError("not a checkpoint file")
+    magic, version, _flags, n_lo, n_hi, u, _next_y1, _K, _m_running, _bl = _CKPT_HEAD.unpack(head)
+    if magic != b"MERTCKP1" or version != 2:
+        raise ContractViolationError("not an sm100 checkpoint file")
+    n = (n_hi << 64) | n_lo
+    if choose_u(n, 1, config.mem_budget, config.u_alpha) != u:
+        raise ContractViolationError(f"checkpoint built with u={u}, config derives another u")
+    return _mertens_exact(n, config, restore_from=path)

@@ -381,3 +381,34 @@ def test_dense_full_quotient_map(engine, oracle):
     for c in [K + 1, s] + [int(x) for x in rng.integers(K + 1, s, size=6)]:
         assert r.quotient(c) == engine.mertens_exact(n // c).value, c
     assert r.quotient(10) == engine.mertens_exact(10**13).value == 599582
+
+
+def test_checkpoint_resume(engine, golden, tmp_path):
+    """Checkpoint after the head and between tail segments, then resume
+    (engine.py:646-741): identical finals and quotients; the file starts with the
+    reference's MERTCKP1 header; wrong u / foreign files are refused."""
+    import struct
+
+    from paper_1108_0135_b200 import _lib
+    from paper_1108_0135_b200.engine import make_job
+
+    n = 10**13
+    path = str(tmp_path / "ck.bin")
+    cfg = engine.EngineConfig(checkpoint_path=path, checkpoint_seconds=0.0, seg_log2_tail=20)
+    full = engine.mertens_exact(n, cfg)
+    assert full.value == 599582
+    head = open(path, "rb").read(72)
+    magic, version, flags, n_lo, n_hi, u, next_y1, K, m_running, bl = struct.unpack("<8sII QQ Q Q Q q Q", head)
+    assert (magic, version, n_lo, u, K) == (b"MERTCKP1", 2, n, full.u, len(full._final))
+    # resume from the last checkpoint of that run (somewhere in the tail)
+    r = engine.resume_exact(path, engine.EngineConfig(seg_log2_tail=20))
+    assert r.value == full.value and np.array_equal(r._final, full._final)
+    assert np.array_equal(r._cp_m, full._cp_m)
+    from paper_1108_0135_b200.errors import ContractViolationError
+
+    with pytest.raises(ContractViolationError):
+        engine.resume_exact(path, engine.EngineConfig(u_alpha=2.0, seg_log2_tail=20))
+    bad = str(tmp_path / "bad.bin")
+    open(bad, "wb").write(b"x" * 100)
+    with pytest.raises(Exception):
+        engine.resume_exact(bad)
