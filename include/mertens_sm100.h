@@ -114,8 +114,9 @@ typedef struct {
   uint64_t cap_small;
   /* tuning (0 = default) */
   uint64_t q_budget_bytes; /* device bytes for the Q tables (default 48 GiB)       */
-  uint32_t seg_log2_head;  /* head segment length 2^x (default 25)                 */
-  uint32_t seg_log2_tail;  /* tail segment length 2^x (default 27)                 */
+  uint32_t seg_log2_head;  /* head segment length 2^x (x >= 17; default: 4 tiles of
+                              2^17 cells per SM, MT_SEG_TILES_PER_SM overrides)    */
+  uint32_t seg_log2_tail;  /* tail segment length 2^x (same default)               */
   int32_t device;          /* CUDA device ordinal (-1: current)                    */
   /* multi-GPU sharding: rank r of w sieves the head redundantly,
    * takes every w-th work unit of the head update and of the Q-gather, and
@@ -132,7 +133,8 @@ typedef struct {
   /* engine-specific */
   uint64_t head_end, n_head_segments, n_tail_segments, kernel_launches;
   uint64_t max_mcut;
-  uint64_t windowed_items, qgather_items, q_entries;
+  uint64_t windowed_items, qgather_items; /* reserved (0) */
+  uint64_t q_entries;
   double ms_total, ms_sieve_head, ms_update_head, ms_sieve_tail, ms_qgather, ms_finalize;
   double ms_counted_kernel, ms_dense_kernel;  /* event-timed (MT_FLAG_TIMING) */
   /* multi-GPU algebra: M(head_end - 1) and this rank's local tail total */
@@ -148,8 +150,9 @@ typedef struct {
 typedef struct {
   int64_t* finals;         /* concatenated: target i's M(floor(n_i/k)), k=1..K_i, K_i = n_i//u,
                               in the order of mt_job.n_lo                         */
-  int64_t* cap_m_out;      /* cap_c_hi - cap_c_lo + 1 entries (or null)         */
-  int64_t* small_m_out;    /* cap_small + 1 entries (or null)                   */
+  int64_t* cap_m_out;      /* cap_c_hi - cap_c_lo + 1 entries (or null); int32_t*
+                              with MT_FLAG_CAP32                                  */
+  int64_t* small_m_out;    /* cap_small + 1 entries (or null); int32_t* with CAP32 */
   uint64_t* acc_out;       /* optional: raw accumulators (ΣK_i) before resolve   */
   mt_stats stats;
 } mt_result;

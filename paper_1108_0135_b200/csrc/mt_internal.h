@@ -138,7 +138,6 @@ struct Sieve2Args {
   const double* rprimes;
   const uint8_t* logs;
   uint32_t p_first, p_warp_end, p_small_end;  // in-tile log primes
-  uint32_t p_mid;                             // first in-tile prime >= 2^14 (lane loop split)
   uint32_t sq_first, sq_end;                  // in-tile squares
   uint32_t nprod, cap;                        // bucket lists (nprod = 0: none)
   const uint32_t* counts;

@@ -47,15 +47,6 @@
 #ifndef S2_DLOADS
 #define S2_DLOADS 2              // bucket entries in flight per lane (measured: 2 > 4 > 8)
 #endif
-#ifndef S2_DYN_D
-#define S2_DYN_D 1               // bucket lists dealt dynamically (1) or round-robin (0)
-#endif
-#ifndef S2_PB_SMEM
-#define S2_PB_SMEM 1             // B primes read from shared memory (1) or global (0)
-#endif
-#ifndef S2_BSPLIT
-#define S2_BSPLIT 0              // lane-per-prime loops: 1 = split at 2^14, 0 = one loop
-#endif
 
 __device__ __forceinline__ void red_add(u32 saddr, u32 v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
@@ -261,11 +252,6 @@ __device__ __forceinline__ int mu_cell(u32 s, int thr) {
 // tile to tile in shared memory (no per-tile division).  Captures and head
 // outputs are tile-relative; k_s3_scan / k_s3_fixup make them absolute.
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ void red_add_if(u32 saddr, u32 v, u32 end) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.lt.u32 q, %0, %2;\n\t@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(saddr), "r"(v),
-               "r"(end)
-               : "memory");
-}
 
 __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
   extern __shared__ u32 st[];                   // S2_W state / mu words
@@ -348,7 +334,6 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
       __syncwarp();
       if (lane == 0) { const u32 tm = tmA[k]; offA[k] = j0 >= tm ? j0 - tm : j0 + p - tm; }
     }
-#if S2_BSPLIT == 0
     // B: lane per prime, groups of 32 in snake order (single loop, predicated tail)
     {
       const u32 nG = (nBp + 31) / 32;
@@ -357,7 +342,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         if (g >= nG) continue;
         const u32 k = g * 32 + lane;
         if (k < nBp) {
-          const u32 p = S2_PB_SMEM ? 2u * pB[k] + 1u : a.primes[a.p_warp_end + k];
+          const u32 p = 2u * pB[k] + 1u;
           const u32 lg = (32 - __clz(p - 1)) | 1;
           u32 j = offB[k];
           const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p, p4 = 4 * p;
@@ -383,54 +368,6 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         }
       }
     }
-#else
-    // B1: lane per prime (p < 2^14, >= 8 marks), four multiples per step; groups
-    //     of 32 consecutive primes in snake order over the warps
-    const u32 nB1 = a.p_mid - a.p_warp_end;
-    {
-      const u32 nG = (nB1 + 31) / 32;
-      for (u32 r = 0; r * 32 < nG; r++) {
-        const u32 g = r * 32 + ((r & 1) ? 31 - warp : warp);
-        if (g >= nG) continue;
-        const u32 k = g * 32 + lane;
-        if (k < nB1) {
-          const u32 p = S2_PB_SMEM ? 2u * pB[k] + 1u : a.primes[a.p_warp_end + k];
-          const u32 lg = (32 - __clz(p - 1)) | 1;  // ceil(log2 p) | 1
-          u32 j = offB[k];
-          const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p, p4 = 4 * p;
-          const u32 v0 = lg << ((j & 3) * 8), v1 = lg << ((j1 & 3) * 8);
-          const u32 v2 = lg << ((j2 & 3) * 8), v3 = lg << ((j3 & 3) * 8);
-          u32 a0 = sbase + (j & ~3u), a1 = sbase + (j1 & ~3u), a2 = sbase + (j2 & ~3u), a3 = sbase + (j3 & ~3u);
-          // full groups of four, then the (at most three) remaining multiples
-          for (; a3 < send; a0 += p4, a1 += p4, a2 += p4, a3 += p4, j += p4) {
-            red_add(a0, v0);
-            red_add(a1, v1);
-            red_add(a2, v2);
-            red_add(a3, v3);
-          }
-          for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), lg << ((j & 3) * 8));
-          offB[k] = j - S2_T;
-        }
-      }
-    }
-    // B2: lane per prime (2^14 <= p <= big_min, <= 8 marks), plain loop
-    {
-      const u32 nB2 = a.p_small_end - a.p_mid;
-      const u32 nG = (nB2 + 31) / 32;
-      for (u32 r = 0; r * 32 < nG; r++) {
-        const u32 g = r * 32 + ((r & 1) ? 31 - warp : warp);
-        if (g >= nG) continue;
-        const u32 k = g * 32 + lane;
-        if (k < nB2) {
-          const u32 p = a.primes[a.p_mid + k];
-          const u32 lg = (32 - __clz(p - 1)) | 1;
-          u32 j = offB[nB1 + k];
-          for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), lg << ((j & 3) * 8));
-          offB[nB1 + k] = j - S2_T;
-        }
-      }
-    }
-#endif
     // C: warp per small square
     for (u32 k = warp; k < nC; k += 32) {
       const u32 p = a.primes[a.sq_first + k], q = p * p;
@@ -443,14 +380,10 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
     //    shared counter so warps that finished A-C early take more lists
     if (a.nprod) {
       const double Yd = (double)Yt;
-      for (u32 rr = 0;; rr++) {
+      for (;;) {
         u32 b = 0;
-#if S2_DYN_D
         if (lane == 0) b = atomicAdd(&s_dnext, 1u);
         b = __shfl_sync(0xffffffffu, b, 0);
-#else
-        b = warp + 32 * rr;  // round-robin: list warp + 32 i
-#endif
         if (b >= a.nprod) break;
         const u32 cw = b < S2_MAXPROD ? s_cnt[b] : a.counts[(u64)b * a.ntiles + tile];
         const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
@@ -866,7 +799,6 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
   a.p_first = std::min(idx_gt(42), end);
   a.p_warp_end = std::max(a.p_first, std::min(idx_gt(1023), end));
   a.p_small_end = std::max(a.p_warp_end, std::min(idx_gt(h->big_min), end));
-  a.p_mid = std::max(a.p_warp_end, std::min(idx_gt(16383), a.p_small_end));
   a.sq_first = std::min(idx_gt(10), end);
   a.sq_end = std::max(a.sq_first, std::min(idx_gt(362), end));
   a.p_lo = a.p_small_end; a.p_hi = end;
