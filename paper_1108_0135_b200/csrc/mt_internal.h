@@ -117,6 +117,7 @@ struct CaptureTarget2 {  // one exact target n for quotient captures (same layou
 struct Bucket2Args {
   uint64_t Y0;
   uint32_t ntiles, cap, nprod_grid;
+  uint32_t bin;          // write-combining entries per tile in shared memory (0 = direct stores)
   const uint32_t* primes;
   const double* rprimes;
   const uint8_t* logs;

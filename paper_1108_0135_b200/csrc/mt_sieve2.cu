@@ -67,31 +67,41 @@ __device__ __forceinline__ u32 neg_mod(u64 Y, double Yd, double r, u32 p) {
 // list of its tile.  Entry = offset (17 bits) | value << 17 (value bit 7 = OR).
 // ----------------------------------------------------------------------------
 // Work is balanced by hits, not by primes: small primes hit the segment up
-// to 16x more often than large ones.  Each round takes FBATCH of this
+// to 16x more often than large ones.  Each batch takes FBATCH of this
 // producer's primes, computes every prime's first hit and hit count (one
-// prime per thread), cuts the hit runs into items of at most FITEM
-// consecutive multiples, lists the items in shared memory, and lets the warps
-// take 32 items at a time (lane per item).  Slots in a tile's list come from
-// shared-memory counters (returning atomics run at ~9 lanes/clk/SM on B200).
-#define FBATCH 1024  // primes per round
-#define FITEM 64     // hits per item
-#define FMAXIT 8192  // items per round (shared-memory list)
+// prime per thread) and cuts the hit runs into items of at most FITEM
+// consecutive multiples (an exclusive scan of items per prime; a thread finds
+// its item's prime by binary search).  Rounds of one item per thread follow.
+// Slots in a tile's list come from shared-memory counters; the entries are
+// write-combined in shared memory (`bin` per tile and round) and flushed as
+// runs (one bulk async copy per tile and round) instead of one 4-byte L2
+// write per hit (ncu: the scattered stores were 60% of the stalls).  Entries
+// past a full bin, and all square flags, are stored directly.
+#define FBATCH 1024  // primes per batch
+#define FITEM 32     // hits per item (1024 items per round: ~32k hits over the tiles)
 __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
-  extern __shared__ u32 cnt[];  // [ntiles + 1] log entries (front; + dummy), then [ntiles] squares (back)
-  u32* cnt2 = cnt + a.ntiles + 1;
+  // dynamic: rcnt[ntiles + 1] (round counts; [ntiles] = dummy), gcnt[ntiles]
+  // (entries before this round), cnt2[ntiles] (square flags), stage[ntiles][bin]
+  extern __shared__ __align__(16) u32 dsm[];
+  u32* rcnt = dsm;
+  u32* gcnt = rcnt + a.ntiles + 1;
+  u32* cnt2 = gcnt + a.ntiles;
+  u32* stage = dsm + ((3 * a.ntiles + 1 + 3) & ~3u);  // 16-byte aligned (bulk copies)
   __shared__ u32 s_q0[FBATCH];
   __shared__ u32 s_step[FBATCH];
   __shared__ u32 s_val[FBATCH];
-  __shared__ u32 s_item[FMAXIT];  // k | chunk << 16
+  __shared__ u32 s_ipre[FBATCH + 1];  // exclusive prefix of items per prime
   __shared__ u32 s_wsum[32];
-  __shared__ u32 s_nitems, s_next;
+  __shared__ u32 s_hits;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 b = blockIdx.x, NP = gridDim.x;
-  for (u32 t = tid; t < 2 * a.ntiles + 1; t += blockDim.x) cnt[t] = 0;
+  const u32 nt = a.ntiles, bin = a.bin;
+  if (tid == 0) s_hits = 0;
+  for (u32 t = tid; t < 3 * nt + 1; t += blockDim.x) dsm[t] = 0;
   const u64 Y0 = a.Y0;
-  const u32 R = a.ntiles * S2_T;  // <= 2^31
+  const u32 R = nt * S2_T;  // <= 2^31
   const double Yd = (double)Y0;
-  u32* __restrict__ out = a.buf + (u64)b * a.ntiles * a.cap;
+  u32* __restrict__ out = a.buf + (u64)b * nt * a.cap;
   const u32 cap = a.cap;
   // this producer's primes: log marks p_lo + b + k*NP, then squares q_lo + b + k*NP
   const u32 nlog = a.p_hi > a.p_lo + b ? (a.p_hi - a.p_lo - b + NP - 1) / NP : 0;
@@ -103,15 +113,15 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
     u32 c = 0;
     {
       const u32 k = base + tid;
-      if (k < nprim && tid < FBATCH) {
-        u32 q0 = R, step = 1, val = 0;
+      u32 q0 = R, step = 1, val = 0;
+      if (k < nprim) {
         if (k < nlog) {
           const u64 i = (u64)a.p_lo + b + (u64)k * NP;
-          const u32 p = a.primes[i];
-          q0 = neg_mod(Y0, Yd, a.rprimes[i], p);
+          const u32 p = a.primes[i];  // reciprocal and log recomputed: one strided load per prime
+          q0 = neg_mod(Y0, Yd, __drcp_rn((double)p), p);
           if (Y0 == 0 && q0 == 0) q0 = p;  // y = 0 is never marked
           step = p;
-          val = (u32)a.logs[i] << 17;
+          val = ((32u - __clz(p - 1)) | 1u) << 17;  // ceil(log2 p) | 1
         } else {
           const u64 i = (u64)a.q_lo + b + (u64)(k - nlog) * NP;
           const u64 p = a.primes[i];
@@ -125,10 +135,11 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
         }
         const u32 hits = q0 < R ? (R - 1 - q0) / step + 1 : 0;
         c = (hits + FITEM - 1) / FITEM;
-        s_q0[tid] = q0;
-        s_step[tid] = step;
-        s_val[tid] = val;
+        if (hits) atomicAdd(&s_hits, hits);
       }
+      s_q0[tid] = q0;
+      s_step[tid] = step;
+      s_val[tid] = val;
     }
     // block exclusive scan of item counts
     u32 incl = c;
@@ -148,44 +159,51 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
         if (lane >= o) ix += t;
       }
       s_wsum[lane] = ix - x;
-      if (lane == 31) { s_nitems = ix; s_next = 0; }
+      if (lane == 31) s_ipre[FBATCH] = ix;
     }
     __syncthreads();
-    {
-      const u32 e = s_wsum[warp] + incl - c;
-      for (u32 q = 0; q < c && e + q < FMAXIT; q++) s_item[e + q] = tid | (q << 16);
-    }
+    s_ipre[tid] = s_wsum[warp] + incl - c;
     __syncthreads();
-    const u32 nit = s_nitems;
-    // items beyond the shared list (only if a batch has > FMAXIT items) are
-    // processed by their owner thread after the shared list
-    for (;;) {
-      u32 i0 = 0;
-      if (lane == 0) i0 = atomicAdd(&s_next, 32u);
-      i0 = __shfl_sync(0xffffffffu, i0, 0);
-      if (i0 >= min(nit, (u32)FMAXIT)) break;
-      const u32 it = i0 + lane;
-      if (it < min(nit, (u32)FMAXIT)) {
-        const u32 w = s_item[it];
-        const u32 k = w & 0xFFFF, ci = w >> 16;
+    const u32 nit = s_ipre[FBATCH];
+    // items per thread and round: large primes give short items, so a round
+    // takes several per thread to fill the bins (~FITEM hits per thread)
+    const u32 per = nit ? max(1u, min(16u, (FITEM * nit + s_hits / 2) / max(1u, s_hits))) : 1u;
+    __syncthreads();
+    if (tid == 0) s_hits = 0;
+    for (u32 r0 = 0; r0 < nit; r0 += 1024 * per) {
+      for (u32 it = r0 + tid; it < min(nit, r0 + 1024 * per); it += 1024) {
+        u32 lo = 0, hi = FBATCH;  // largest k with s_ipre[k] <= it
+        while (hi - lo > 1) {
+          const u32 mid = (lo + hi) >> 1;
+          if (s_ipre[mid] <= it) lo = mid; else hi = mid;
+        }
+        const u32 k = lo, ci = it - s_ipre[k];
         const u32 step = s_step[k], val = s_val[k];
         u32 pos = s_q0[k] + ci * FITEM * step;
         const u32 end = (u32)min((u64)R, (u64)pos + (u64)FITEM * step);
         if (!(val & (0x80u << 17))) {
-          // four independent slot allocations in flight; hits past `end` count
-          // into the dummy counter cnt[ntiles]
+          // four slot allocations in flight; hits past `end` count into the dummy rcnt[nt]
           for (; pos < end; pos += 4 * step) {
             u32 t[4], sl[4];
 #pragma unroll
             for (int h = 0; h < 4; h++) {
               const u32 ph = pos + h * step;
-              t[h] = ph < end ? ph >> 17 : a.ntiles;
+              t[h] = ph < end ? ph >> 17 : nt;
             }
 #pragma unroll
-            for (int h = 0; h < 4; h++) sl[h] = atomicAdd(&cnt[t[h]], 1u);
+            for (int h = 0; h < 4; h++) sl[h] = atomicAdd(&rcnt[t[h]], 1u);
 #pragma unroll
-            for (int h = 0; h < 4; h++)
-              if (t[h] < a.ntiles && sl[h] < cap) out[t[h] * cap + sl[h]] = ((pos + h * step) & (S2_T - 1)) | val;
+            for (int h = 0; h < 4; h++) {
+              if (t[h] < nt) {
+                const u32 e = ((pos + h * step) & (S2_T - 1)) | val;
+                if (sl[h] < bin) {
+                  stage[t[h] * bin + sl[h]] = e;
+                } else {
+                  const u32 g = gcnt[t[h]] + sl[h];
+                  if (g < cap) out[t[h] * cap + g] = e;
+                }
+              }
+            }
           }
         } else {  // square flags fill each list from the back
           for (; pos < end; pos += step) {
@@ -195,32 +213,42 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
           }
         }
       }
-    }
-    if (nit > FMAXIT) {  // overflowed item list: owners finish their own remaining items
-      const u32 e = s_wsum[warp] + incl - c;
-      for (u32 q = 0; q < c; q++) {
-        if (e + q < FMAXIT) continue;
-        const u32 step = s_step[tid], val = s_val[tid];
-        u32 pos = s_q0[tid] + q * FITEM * step;
-        const u32 end = (u32)min((u64)R, (u64)pos + (u64)FITEM * step);
-        for (; pos < end; pos += step) {
-          const u32 t = pos >> 17;
-          if (!(val & (0x80u << 17))) {
-            const u32 sl = atomicAdd(&cnt[t], 1u);
-            if (sl < cap) out[t * cap + sl] = (pos & (S2_T - 1)) | val;
-          } else {
-            const u32 sl = atomicAdd(&cnt2[t], 1u);
-            if (sl < cap) out[t * cap + (cap - 1 - sl)] = pos & (S2_T - 1);
-          }
+      // flush: each tile's run, zero-padded to a multiple of 4 entries (an entry
+      // of 0 adds 0 to cell 0: a no-op mark) so every run starts 16-byte aligned,
+      // goes out as one bulk async copy shared -> global
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      for (u32 t = tid; t < nt; t += blockDim.x) {
+        const u32 rc = rcnt[t], g0 = gcnt[t];
+        if (!rc) continue;
+        const u32 len = (rc + 3) & ~3u;
+        u32* so = stage + t * bin;
+        u32* go = out + t * cap + g0;
+        if (rc < bin) {
+          for (u32 i = rc; i < len; i++) so[i] = 0u;
+        } else {
+          for (u32 i = rc; i < len; i++) if (g0 + i < cap) go[i] = 0u;
         }
+        const u32 ncp = g0 < cap ? min(min(len, bin), cap - g0) : 0u;
+        if (ncp) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       ::"l"(go), "r"((u32)__cvta_generic_to_shared(so)), "r"(ncp * 4u) : "memory");
+        }
+        gcnt[t] = g0 + len;
+        rcnt[t] = 0;
       }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncthreads();
     }
   }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
-  for (u32 t = tid; t < a.ntiles; t += blockDim.x) {
-    const u32 nl = cnt[t], ns = cnt2[t];
+  for (u32 t = tid; t < nt; t += blockDim.x) {
+    const u32 nl = gcnt[t], ns = cnt2[t];
     // overflow (nl + ns > cap) is flagged by an all-ones count
-    a.counts[(u64)b * a.ntiles + t] = (nl + ns > cap || nl > 0xFFFF || ns > 0xFFFF) ? 0xFFFFFFFFu : (nl | (ns << 16));
+    a.counts[(u64)b * nt + t] = (nl + ns > cap || nl > 0xFFFF || ns > 0xFFFF) ? 0xFFFFFFFFu : (nl | (ns << 16));
   }
 }
 
@@ -611,7 +639,7 @@ int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
   Sieve2Args a = g.tile;
   if (a.nprod) {
     Bucket2Args b = g.bucket;
-    const size_t bs = (2 * (size_t)b.ntiles + 1) * sizeof(u32);
+    const size_t bs = (((3 * (size_t)b.ntiles + 1 + 3) & ~(size_t)3) + (size_t)b.ntiles * b.bin) * sizeof(u32);
     if (kt) kt->begin(KT_SIEVE_LARGE, st);
     k_bucket_fill<<<b.nprod_grid, 1024, bs, st>>>(b);
     if (kt) kt->end(st);
@@ -690,6 +718,7 @@ struct Sieve2Host {
   u64 P1 = 485100, P2 = 1062347, P3 = 1363783;
   std::vector<u32> p;
   u32 nprod = 0, cap = 0, max_tiles = 0;
+  u32 fill_smem = 0;  // dynamic shared memory available to k_bucket_fill
   u32 big_min = S2_T;  // primes above this go to the bucket lists
   uint64_t overflows_host = 0;
 };
@@ -741,7 +770,10 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
   if (any && e > 0) {
     h->nprod = (u32)nsm;
     const double m = e / h->nprod;
-    h->cap = (u32)std::ceil(m + 8.0 * std::sqrt(m) + 32.0);
+    // + the fill's zero padding: <= 3 entries per tile and round, a round being
+    //   ~1024 * FITEM hits of one producer spread over the segment's tiles
+    const double rounds = m * max_tiles / (1024.0 * FITEM) + 1.0;
+    h->cap = (u32)std::ceil(m + 8.0 * std::sqrt(m) + 2.0 * rounds + 32.0);
     h->cap = (h->cap + 31) & ~31u;
     if (balloc(h->buf, (size_t)h->nprod * max_tiles * h->cap * 4) ||
         balloc(h->counts, (size_t)h->nprod * max_tiles * 4))
@@ -760,8 +792,8 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
     MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        optin - (int)fa.sharedSizeBytes));
     MT_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_bucket_fill));
-    MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       optin - (int)fa.sharedSizeBytes));
+    h->fill_smem = (u32)(optin - (int)fa.sharedSizeBytes);
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fill_smem));
   }
   if (max_tiles > 16384) { mt_set_error("too many tiles per segment (max 2^31 cells)"); return MT_ERR_VALUE; }
   MT_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -815,6 +847,13 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
   a.caps = caps; a.n_cap = n_cap;
   Bucket2Args& b = g.bucket;
   b.Y0 = Y0; b.ntiles = ntiles; b.cap = h->cap; b.nprod_grid = a.nprod;
+  {  // write-combining bin per tile: what fits next to the counters, 16..128 entries
+    const u64 head = 4ull * ((3ull * ntiles + 1 + 3) & ~3ull);
+    const u64 room = h->fill_smem > head ? h->fill_smem - head : 0;
+    u64 bin = std::min<u64>(128, room / (4ull * ntiles)) & ~7ull;
+    if (const char* e = getenv("MT_FILL_BIN")) bin = std::min<u64>(bin, (u64)atoi(e)) & ~7ull;
+    b.bin = bin >= 16 ? (u32)bin : 0;
+  }
   b.primes = a.primes; b.rprimes = a.rprimes; b.logs = a.logs;
   b.p_lo = a.p_lo; b.p_hi = a.p_hi; b.q_lo = a.q_lo; b.q_hi = a.q_hi;
   b.buf = (u32*)h->buf.p; b.counts = (u32*)h->counts.p;
