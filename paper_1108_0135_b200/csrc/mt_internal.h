@@ -123,6 +123,9 @@ struct Bucket2Args {
   const uint8_t* logs;
   uint32_t p_lo, p_hi;   // log marks of primes [p_lo, p_hi)  (p > 2^17)
   uint32_t q_lo, q_hi;   // square flags of primes [q_lo, q_hi) (p^2 > 2^17)
+  const uint32_t* pperm; // producer-major bucket primes: [nprod][kp] log marks, [nprod][kq] squares
+  const uint32_t* qperm;
+  uint32_t kp, kq;
   uint32_t* buf;         // [nprod][ntiles][cap]
   uint32_t* counts;      // [nprod][ntiles]
 };

@@ -116,15 +116,13 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
       u32 q0 = R, step = 1, val = 0;
       if (k < nprim) {
         if (k < nlog) {
-          const u64 i = (u64)a.p_lo + b + (u64)k * NP;
-          const u32 p = a.primes[i];  // reciprocal and log recomputed: one strided load per prime
+          const u32 p = a.pperm[(u64)b * a.kp + k];  // producer-major copy: coalesced; 1/p and log recomputed
           q0 = neg_mod(Y0, Yd, __drcp_rn((double)p), p);
           if (Y0 == 0 && q0 == 0) q0 = p;  // y = 0 is never marked
           step = p;
           val = ((32u - __clz(p - 1)) | 1u) << 17;  // ceil(log2 p) | 1
         } else {
-          const u64 i = (u64)a.q_lo + b + (u64)(k - nlog) * NP;
-          const u64 p = a.primes[i];
+          const u64 p = a.qperm[(u64)b * a.kq + (k - nlog)];
           const u64 q = p * p;
           const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Y0, q);
           const u64 rem = Y0 - qq * q;
@@ -719,6 +717,10 @@ struct Sieve2Host {
   std::vector<u32> p;
   u32 nprod = 0, cap = 0, max_tiles = 0;
   u32 fill_smem = 0;  // dynamic shared memory available to k_bucket_fill
+  // bucket primes in producer-major order: pperm[b * kp + k] = p[P_lo + b + k * nprod]
+  // (log marks), qperm[b * kq + k] = p[Q_lo + b + k * nprod] (square flags)
+  Buf pperm, qperm;
+  u32 kp = 0, kq = 0, P_lo = 0, Q_lo = 0;
   u32 big_min = S2_T;  // primes above this go to the bucket lists
   uint64_t overflows_host = 0;
 };
@@ -778,6 +780,23 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
     if (balloc(h->buf, (size_t)h->nprod * max_tiles * h->cap * 4) ||
         balloc(h->counts, (size_t)h->nprod * max_tiles * 4))
       return MT_ERR_RESOURCE;
+    auto gt = [&](u64 v) { return (u32)(std::upper_bound(h->p.begin(), h->p.end(), (u32)v) - h->p.begin()); };
+    h->P_lo = gt(h->big_min);
+    h->Q_lo = gt(362);
+    auto perm = [&](Buf& dst, u32 lo, u32& kk) -> int {
+      kk = np > lo ? (u32)((np - lo + h->nprod - 1) / h->nprod) : 0;
+      std::vector<u32> v((size_t)h->nprod * kk + 1, 0);
+      for (u32 b = 0; b < h->nprod; b++)
+        for (u32 k = 0; k < kk; k++) {
+          const size_t i = (size_t)lo + b + (size_t)k * h->nprod;
+          if (i < np) v[(size_t)b * kk + k] = h->p[i];
+        }
+      if (balloc(dst, v.size() * 4)) return MT_ERR_RESOURCE;
+      MT_CUDA_CHECK(cudaMemcpyAsync(dst.p, v.data(), v.size() * 4, cudaMemcpyHostToDevice, st));
+      MT_CUDA_CHECK(cudaStreamSynchronize(st));
+      return MT_OK;
+    };
+    if (perm(h->pperm, h->P_lo, h->kp) || perm(h->qperm, h->Q_lo, h->kq)) return MT_ERR_RESOURCE;
   }
   h->nsm = nsm;
   if (balloc(h->tstate, ((size_t)max_tiles + 1) * 8) || balloc(h->ovf, 8) || balloc(h->tsum, (size_t)max_tiles * 4) ||
@@ -856,6 +875,11 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
   }
   b.primes = a.primes; b.rprimes = a.rprimes; b.logs = a.logs;
   b.p_lo = a.p_lo; b.p_hi = a.p_hi; b.q_lo = a.q_lo; b.q_hi = a.q_hi;
+  b.pperm = (const u32*)h->pperm.p; b.qperm = (const u32*)h->qperm.p; b.kp = h->kp; b.kq = h->kq;
+  if ((b.p_hi > b.p_lo && b.p_lo != h->P_lo) || (b.q_hi > b.q_lo && b.q_lo != h->Q_lo)) {
+    mt_set_error("bucket prime ranges do not match the producer-major tables");
+    return MT_ERR_VALUE;
+  }
   b.buf = (u32*)h->buf.p; b.counts = (u32*)h->counts.p;
   return mt_sieve2_segment(g, st, kt);
 }
