@@ -45,7 +45,7 @@
 #define S2_CH (S2_T / 32)        // 32-cell chunks per tile
 #define S2_MAXPROD 512           // bucket producers whose counts are staged in shared memory
 #ifndef S2_DLOADS
-#define S2_DLOADS 2              // bucket entries in flight per lane (measured: 2 > 4 > 8)
+#define S2_DLOADS 1              // 16-byte bucket vectors in flight per lane (measured: 1 > 2)
 #endif
 
 __device__ __forceinline__ void red_add(u32 saddr, u32 v) {
@@ -415,12 +415,22 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
         if (cw != 0xFFFFFFFFu) {
           const u32 n = cw & 0xFFFF, nsq = cw >> 16;
-          for (u32 k = lane; k < n; k += 32 * S2_DLOADS) {  // log entries (front), S2_DLOADS loads in flight
-            u32 e[S2_DLOADS];
+          // log entries (front): n is a multiple of 4 (the fill pads every run with
+          // no-op zero entries), so the list is read as 16-byte vectors,
+          // S2_DLOADS per lane in flight
+          const uint4* __restrict__ L4 = (const uint4*)L;
+          const u32 n4 = n >> 2;
+          for (u32 k = lane; k < n4; k += 32 * S2_DLOADS) {
+            uint4 e[S2_DLOADS];
 #pragma unroll
-            for (int h = 0; h < S2_DLOADS; h++) e[h] = k + 32 * h < n ? L[k + 32 * h] : 0u;
+            for (int h = 0; h < S2_DLOADS; h++) e[h] = k + 32 * h < n4 ? L4[k + 32 * h] : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-            for (int h = 0; h < S2_DLOADS; h++) red_add(sbase + (e[h] & 0x1FFFCu), (e[h] >> 17) << ((e[h] & 3) * 8));
+            for (int h = 0; h < S2_DLOADS; h++) {
+              red_add(sbase + (e[h].x & 0x1FFFCu), (e[h].x >> 17) << ((e[h].x & 3) * 8));
+              red_add(sbase + (e[h].y & 0x1FFFCu), (e[h].y >> 17) << ((e[h].y & 3) * 8));
+              red_add(sbase + (e[h].z & 0x1FFFCu), (e[h].z >> 17) << ((e[h].z & 3) * 8));
+              red_add(sbase + (e[h].w & 0x1FFFCu), (e[h].w >> 17) << ((e[h].w & 3) * 8));
+            }
           }
           for (u32 k = lane; k < nsq; k += 32) {  // square flags (back)
             const u32 e = L[a.cap - 1 - k];
