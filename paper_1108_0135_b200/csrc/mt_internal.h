@@ -142,6 +142,7 @@ struct Sieve2Args {
   const double* rprimes;
   const uint8_t* logs;
   uint32_t p_first, p_warp_end, p_small_end;  // in-tile log primes
+  uint32_t p_b2;                                // first in-tile prime of the plain-stream B2 range
   uint32_t sq_first, sq_end;                  // in-tile squares
   uint32_t nprod, cap;                        // bucket lists (nprod = 0: none)
   const uint32_t* counts;

@@ -44,6 +44,9 @@
 #define S2_NT 1024               // threads per tile CTA
 #define S2_CH (S2_T / 32)        // 32-cell chunks per tile
 #define S2_MAXPROD 512           // bucket producers whose counts are staged in shared memory
+#ifndef S2_B2_MIN
+#define S2_B2_MIN (1u << 15)     // in-tile primes from here on hit <= 4 times per tile (measured: 2^15 > 2^14 > 2^13)
+#endif
 #ifndef S2_DLOADS
 #define S2_DLOADS 1              // 16-byte bucket vectors in flight per lane (measured: 1 > 2)
 #endif
@@ -284,6 +287,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
   int* csum = (int*)(st + S2_W);                // S2_CH chunk sums -> exclusive chunk prefixes
   const u32 nA = a.p_warp_end - a.p_first;
   const u32 nBp = a.p_small_end - a.p_warp_end;
+  const u32 nB1 = a.p_b2 - a.p_warp_end;        // B1 primes; [nB1, nBp) are B2
   const u32 nC = a.sq_end - a.sq_first;
   u32* offA = (u32*)(csum + S2_CH);             // first multiple of p (lane 0's mark), A primes
   u32* tmA = offA + nA;                         // T mod p
@@ -361,13 +365,14 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
       if (lane == 0) { const u32 tm = tmA[k]; offA[k] = j0 >= tm ? j0 - tm : j0 + p - tm; }
     }
     // B: lane per prime, groups of 32 in snake order (single loop, predicated tail)
+    //    B1 = [1024, S2_B2_MIN): four interleaved streams per prime
     {
-      const u32 nG = (nBp + 31) / 32;
+      const u32 nG = (nB1 + 31) / 32;
       for (u32 r = 0; r * 32 < nG; r++) {
         const u32 g = r * 32 + ((r & 1) ? 31 - warp : warp);
         if (g >= nG) continue;
         const u32 k = g * 32 + lane;
-        if (k < nBp) {
+        if (k < nB1) {
           const u32 p = 2u * pB[k] + 1u;
           const u32 lg = (32 - __clz(p - 1)) | 1;
           u32 j = offB[k];
@@ -391,6 +396,23 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
           jn = jn - p >= S2_T && jn >= p ? jn - p : jn;
           jn = jn - p >= S2_T && jn >= p ? jn - p : jn;
           offB[k] = jn - S2_T;
+        }
+      }
+    }
+    //    B2 = [S2_B2_MIN, big_min): at most T / S2_B2_MIN hits per tile, one plain
+    //    stream per prime (per-prime setup dominates here, so it is kept minimal)
+    {
+      const u32 nG = (nBp - nB1 + 31) / 32;
+      for (u32 r = 0; r * 32 < nG; r++) {
+        const u32 g = r * 32 + ((r & 1) ? 31 - warp : warp);
+        if (g >= nG) continue;
+        const u32 k = nB1 + g * 32 + lane;
+        if (k < nBp) {
+          const u32 p = 2u * pB[k] + 1u;
+          const u32 lg = (32 - __clz(p - 1)) | 1;
+          u32 j = offB[k];
+          for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), lg << ((j & 3) * 8));
+          offB[k] = j - S2_T;
         }
       }
     }
@@ -860,6 +882,7 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
   a.p_first = std::min(idx_gt(42), end);
   a.p_warp_end = std::max(a.p_first, std::min(idx_gt(1023), end));
   a.p_small_end = std::max(a.p_warp_end, std::min(idx_gt(h->big_min), end));
+  a.p_b2 = std::max(a.p_warp_end, std::min(idx_gt(S2_B2_MIN - 1), a.p_small_end));
   a.sq_first = std::min(idx_gt(10), end);
   a.sq_end = std::max(a.sq_first, std::min(idx_gt(362), end));
   a.p_lo = a.p_small_end; a.p_hi = end;
