@@ -333,8 +333,9 @@ def main():
                  "units_per_launch": ys_per_launch, "avg_launch_ms": avg_ms,
                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in pk else "fallback",
                  "note": ("the sieve keeps its state in shared memory: measured DRAM traffic per launch (ncu, "
-                          "profiles/traffic.json) is far below the 10 B/y accounting, so frac > 1; the kernel is "
-                          "bound by shared-memory reductions and issue (profiles/)")}
+                          "profiles/traffic.json; mostly the bucket lists) is ~1 B/y, far below the 10 B/y "
+                          "accounting, so frac compares the tile rate with an HBM-bound design; the kernel "
+                          "itself is bound by shared-memory reductions and issue (profiles/r01_final_ncu.txt)")}
     else:
         ops = 7 * stats_last["counted_items"] + 4 * stats_last["dense_items"]
         A = ops / (kms[dom] / args.steps * 1e-3) / 1e12
