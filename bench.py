@@ -320,10 +320,11 @@ def main():
     avg_ms = kms[dom] / max(1, kcnt[dom])
     roof = {"kernel": dom}
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
-    seg = nsm * 4 * (1 << 17)  # default segment: 4 tiles of 2^17 cells per SM (mt_engine.cu)
+    seg = nsm * 4 * (1 << 17)  # tail segment: 4 tiles of 2^17 cells per SM (mt_engine.cu)
     if dom in ("sieve_tile", "sieve_large"):
-        # 10 algorithmic bytes per y-value (state write+read 2 B, M(y) 8 B)
-        ys_per_launch = (stats_last["n_tail_segments"] + stats_last["n_head_segments"]) * seg \
+        # 10 algorithmic bytes per y-value (state write+read 2 B, M(y) 8 B);
+        # cells sieved per step = the head [0, head_end) + the tail segments
+        ys_per_launch = (stats_last["head_end"] + stats_last["n_tail_segments"] * seg) \
             / max(1, kcnt[dom] / args.steps)
         A = 10 * ys_per_launch / (avg_ms * 1e-3) / 1e9
         P_ = pk.get("hbm_gbs", 6650.0)
