@@ -1126,7 +1126,10 @@ extern "C" int mt_plan_gather(mt_plan* P) {
   if (P->phase < 2) { mt_set_error("gather before tail_offset"); return MT_ERR_CONTRACT; }
   PLAN_DEV(P);
   MT_CUDA_CHECK(cudaEventRecord(P->ev[3], P->st));
-  RC(mt_update_qgather(P->uc, P->st));
+  u64 qmax = 0;
+  for (size_t i = 0; i < P->jq0.size(); i++)
+    if (P->jq1[i] >= P->jq0[i]) qmax = std::max<u64>(qmax, P->jq1[i] - P->jq0[i] + 1);
+  RC(mt_update_qgather(P->uc, qmax, P->st));
   if (P->rank == 0) RC(mt_update_finish(P->uc, P->st));
   MT_CUDA_CHECK(cudaEventRecord(P->ev[4], P->st));
   MT_CUDA_CHECK(cudaStreamSynchronize(P->st));

@@ -221,7 +221,7 @@ int mt_update_create(UpdateCtx** ctx, const ElemDev& E, uint64_t* acc, int32_t* 
 void mt_update_destroy(UpdateCtx* ctx);
 int mt_update_head_segment(UpdateCtx* ctx, uint64_t Y0, uint64_t R, const int8_t* mu,
                            const int16_t* M16, const int64_t* bk, cudaStream_t st);
-int mt_update_qgather(UpdateCtx* ctx, cudaStream_t st);
+int mt_update_qgather(UpdateCtx* ctx, uint64_t qmax, cudaStream_t st);  // qmax: largest table (entries)
 int mt_update_finish(UpdateCtx* ctx, cudaStream_t st);  // acc -= M(mcut)*xcut
 int mt_finalize_dev(const uint64_t* acc, const uint64_t* D, uint64_t K, int64_t* final_out,
                     cudaStream_t st);
