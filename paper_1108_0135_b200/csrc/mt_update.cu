@@ -81,6 +81,24 @@ __device__ __forceinline__ u64 upper_idx(const uint64_t* __restrict__ off, u64 n
   return lo;
 }
 
+// the same search by a whole warp (x warp-uniform): 32 probes per round cut the
+// range 33-fold, so ~4 dependent loads instead of ~17 for 10^5 entries
+__device__ __forceinline__ u64 upper_idx_warp(const uint64_t* __restrict__ off, u64 n, u64 x) {
+  const int lane = threadIdx.x & 31;
+  u64 lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const u64 step = (hi - lo + 32) / 33;
+    const u64 p = lo + step * (u64)(lane + 1);
+    const bool ok = p < hi && off[p] <= x;  // monotone in lane
+    const u32 c = __popc(__ballot_sync(0xffffffffu, ok));
+    const u64 nlo = c ? lo + step * c : lo;
+    const u64 nhi = lo + step * (c + 1);
+    lo = nlo;
+    hi = nhi < hi ? nhi : hi;
+  }
+  return lo;
+}
+
 struct CountedArgs {
   ElemDev E;
   uint64_t* acc;
@@ -110,7 +128,7 @@ __global__ void __launch_bounds__(MT_CT) k_counted(CountedArgs a) {
     const u64 unit = s_unit;
     if (unit >= total) break;
     if (tid == 0) nxt = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
-    const u64 tau = upper_idx(a.off, a.ntiles + 1, unit);
+    const u64 tau = upper_idx_warp(a.off, a.ntiles + 1, unit);
     const u64 c = unit - a.off[tau];
     const u64 mlo = a.Y0 + c * MT_CM;
     u64 mhi = mlo + MT_CM;  // exclusive
@@ -340,12 +358,27 @@ struct WinArgs {
   u32 rank, world, force_wide;
 };
 
+__device__ __forceinline__ void mbar_wait(u32 bar, u32 phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+
 __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
-  extern __shared__ int4 smem_win[];
+  extern __shared__ __align__(128) int4 smem_win[];
   int16_t* sw = (int16_t*)smem_win;
   const u32 swbase = (u32)__cvta_generic_to_shared(sw);
   __shared__ u64 s_unit;
+  __shared__ __align__(8) unsigned long long s_bar;
   const int tid = threadIdx.x;
+  const u32 bar = (u32)__cvta_generic_to_shared(&s_bar);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  u32 phase = 0;
   const u64 total = a.uoff[a.G.ng];
   u64 nxt = 0;  // next unit, fetched while the current one is walked
   if (tid == 0) nxt = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
@@ -355,16 +388,21 @@ __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
     const u64 unit = s_unit;
     if (unit >= total) break;
     if (tid == 0) nxt = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
-    const u64 g = upper_idx(a.uoff, a.G.ng + 1, unit);
+    const u64 g = upper_idx_warp(a.uoff, a.G.ng + 1, unit);
     const u64 w = a.wfirst[g] + (unit - a.uoff[g]);
     const u64 W0 = a.Y0 + w * MT_BLK, W1 = W0 + MT_BLK;  // [W0, W1)
-    {
-      const int4* src = (const int4*)(a.M16 + w * MT_BLK);
-      for (int i = tid; i < (int)(MT_BLK / 8); i += 256) smem_win[i] = src[i];
+    // the 64 KB window arrives by one bulk async copy (TMA) while the threads
+    // compute their elements' d-ranges (two divisions each); they wait on the
+    // mbarrier just before their first window read
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((u32)(MT_BLK * 2)) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(swbase), "l"(a.M16 + w * MT_BLK), "r"((u32)(MT_BLK * 2)), "r"(bar) : "memory");
     }
+    bool ready = false;
     const i64 base = a.bk[w];
     const bool wide = a.G.wide[g] || a.force_wide;
-    __syncthreads();
     const u64 e0g = a.G.start[g], e1 = a.G.start[g + 1];
     // groups smaller than the CTA: S = 256/A threads per element, each walking a
     // contiguous slice of the element's d-range in this window
@@ -393,6 +431,7 @@ __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
         dh = top;
         if (bot > dl) dl = bot;
       }
+      if (!ready) { mbar_wait(bar, phase); ready = true; }
       int s = 0;
       if (wide) {
         auto f = [&](u64 y) { s += sw[(u32)(y - W0)]; };
@@ -403,6 +442,9 @@ __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
       const i64 tot = (i64)s + (i64)(dh - dl + 1) * base;
       atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)tot);
     }
+    // the copy must have landed before the buffer is refilled (thread 0 re-arms)
+    if (tid == 0 && !ready) mbar_wait(bar, phase);
+    phase ^= 1u;
     __syncthreads();
   }
 }
