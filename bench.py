@@ -343,18 +343,22 @@ def main():
         roof |= {"bound": "int", "achieved": A, "peak": 18.56, "unit": "Tops/s", "frac": A / 18.56,
                  "traffic": None}
     # the counted walk against its issue roofline: one exact division per squarefree m
-    # (6/pi^2 of the reference's counted pairs); peak = the microbenchmarked inner loop
-    # (14.15 items/clk/SM, profiles/r01_microbench.txt) x SMs x max clock
+    # (6/pi^2 of the reference's counted pairs).  The k_counted inner loop walks two
+    # elements per list entry; its SASS is 76 instructions per 16 items (16 DFMA,
+    # 18 IMAD, 16 LEA.HI, 16 IADD3, 6 LDS.128, 4 loop), so at 4 warp-instructions
+    # per clock per SM the issue roofline is 128 / 4.75 = 26.9 items/clk/SM
     upd_ms = kms.get("counted", 0.0) / args.steps
     upd = None
     if upd_ms > 0:
         items = 6 / 3.141592653589793 ** 2 * stats_last["counted_items"]
         A = items / (upd_ms * 1e-3) / 1e12
-        Pk = 14.15 * nsm * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        ipc_items = 128.0 / (76.0 / 16.0)
+        Pk = ipc_items * nsm * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         upd = {"kernel": "counted", "bound": "issue", "achieved": A, "peak": Pk, "unit": "T items/s",
                "frac": A / Pk, "per_unit": "one fp64-reciprocal exact division + 64-bit accumulate per squarefree m",
                "reference_count_rate": stats_last["counted_items"] / (upd_ms * 1e-3),
-               "peak_source": "profiles/r01_microbench.txt 'counted' loop (14.15 items/clk/SM) x SMs x sm_max_mhz"}
+               "peak_source": "SASS of the k_counted joint loop: 4.75 instructions per item -> 26.9 items/clk/SM "
+                              "x SMs x sm_max_mhz (DESIGN.md §6)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
