@@ -374,7 +374,7 @@ __device__ __forceinline__ void walk_quotients(u64 vlo, u64 vhi, double vd, int 
 // The split d_sp keeps y/d^2 <= 1, so one correction of delta per step is
 // exact; a second is never needed (a rare-path loop guards it anyway).
 __device__ __forceinline__ int walk_window32(u64 vlo, u64 vhi, double vd, int vb, u64 dh64, u64 dl64, u64 W0,
-                                             u32 swbase) {
+                                             u32 swbase, bool& bad) {
   const double rd = __drcp_rn((double)dh64);
   const u64 y0 = qdiv_ok(vb, dh64) ? qdiv64(vd, rd, vlo, dh64) : (u64)udiv128(vlo, vhi, dh64);
   u32 delta = (u32)((double)y0 * rd);
@@ -383,6 +383,7 @@ __device__ __forceinline__ int walk_window32(u64 vlo, u64 vhi, double vd, int vb
   u32 r = (u32)vlo - (u32)y0 * d;
   u32 yo = (u32)(y0 - W0);  // offset in the window
   int s = 0;
+  bool lbad = false;
   u32 swb = swbase;
   for (;;) {
     asm volatile("" : "+r"(swb));  // keep the window base live (no per-item rematerialisation)
@@ -395,15 +396,14 @@ __device__ __forceinline__ int walk_window32(u64 vlo, u64 vhi, double vd, int vb
     const int neg = ts >> 31;                                 // -1 if ts < 0
     const int over = (int)(ts >= (int)d);                     // 1 if ts >= d
     delta += (u32)(over + neg);
-    u32 t = (u32)(ts + ((int)d & neg) - ((int)d & -over));
-    if (t >= d) {  // never taken when y/d^2 <= 1
-      while (t >= d) {
-        if ((int)t < 0) { delta--; t += d; } else { delta++; t -= d; }
-      }
-    }
+    const u32 t = (u32)(ts + ((int)d & neg) - ((int)d & -over));
+    // t < d always holds when y/d^2 <= 1 (one correction suffices); the check is
+    // folded into one predicate per step and a violation re-walks exactly
+    lbad |= t >= d;
     r = t;
     yo += delta;
   }
+  bad = lbad;
   return s;
 }
 
@@ -523,7 +523,13 @@ __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
         auto f = [&](u64 y) { s += sw[(u32)(y - W0)]; };
         walk_quotients<true>(vlo, vhi, vd, vb, dh, dl, f);
       } else {
-        s = walk_window32(vlo, vhi, vd, vb, dh, dl, W0, swbase);
+        bool bad = false;
+        s = walk_window32(vlo, vhi, vd, vb, dh, dl, W0, swbase, bad);
+        if (bad) {  // never expected (d >= d_sp); exact re-walk keeps the result right regardless
+          s = 0;
+          auto f = [&](u64 y) { s += sw[(u32)(y - W0)]; };
+          walk_quotients<true>(vlo, vhi, vd, vb, dh, dl, f);
+        }
       }
       const i64 tot = (i64)s + (i64)(dh - dl + 1) * base;
       atomicAdd((unsigned long long*)(a.acc + e), (unsigned long long)tot);
