@@ -753,7 +753,7 @@ struct Sieve2Host {
   // (log marks), qperm[b * kq + k] = p[Q_lo + b + k * nprod] (square flags)
   Buf pperm, qperm;
   u32 kp = 0, kq = 0, P_lo = 0, Q_lo = 0;
-  u32 big_min = S2_T;  // primes above this go to the bucket lists
+  u32 big_min = S2_T / 2;  // primes above this go to the bucket lists (2^16: measured 1.2 % better than 2^17 at 1e19)
   uint64_t overflows_host = 0;
 };
 
