@@ -199,7 +199,14 @@ def _quotient_targets(n: int, K: int, u: int, budget: int) -> np.ndarray:
         c = np.arange(1, s + 1, dtype=np.uint64)
         qs = np.union1d(c, np.uint64(n) // c)
     else:
-        qs = np.unique(np.uint64(n) // np.arange(K + 1, K + 1 + budget, dtype=np.uint64))
+        # floor(n/c) is non-increasing in c: dedupe adjacent values, then ascend
+        # (same set as np.unique, without its hash/sort pass over `budget` values)
+        v = np.uint64(n) // np.arange(K + 1, K + 1 + budget, dtype=np.uint64)
+        keep = np.empty(v.shape, dtype=bool)
+        if v.size:
+            keep[0] = True
+            np.not_equal(v[1:], v[:-1], out=keep[1:])
+        qs = v[keep][::-1]
     return qs[(qs >= 1) & (qs <= np.uint64(u))]
 
 
