@@ -33,7 +33,7 @@
 //              shared memory, so a prime costs one division per CTA, not per tile
 //   scan     = tile sums -> one-block scan seeded with the running M; captures
 //              M(floor(n/j)) and the head's 32K block bases are written
-//              tile-relative and made absolute by a fixup pass (k_s3_fixup)
+//              tile-relative and made absolute by one finishing pass (k_s3_finish)
 #include <cstdio>
 
 #include "mt_common.cuh"
@@ -279,7 +279,7 @@ __device__ __forceinline__ int mu_cell(u32 s, int thr) {
 // [c*m, c*m + m) of the segment; the first multiple of every in-tile prime
 // (and square) is computed once per CTA by division and then carried from
 // tile to tile in shared memory (no per-tile division).  Captures and head
-// outputs are tile-relative; k_s3_scan / k_s3_fixup make them absolute.
+// outputs are tile-relative; k_s3_finish makes them absolute.
 // ----------------------------------------------------------------------------
 
 __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
     }
     __syncthreads();
     if (tid == 0) a.tile_sum[tile] = s_total;
-    // 5. head outputs (tile-relative block starts; k_s3_scan makes bk absolute)
+    // 5. head outputs (tile-relative block starts; k_s3_finish makes bk absolute)
     if (a.mu_out) {
       u32* mo = (u32*)(a.mu_out + (u64)tile * S2_T);
       for (int i = tid; i < (int)S2_W; i += S2_NT) mo[i] = st[i];
@@ -608,59 +608,51 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
   }
 }
 
-// exclusive tile bases for one segment, seeded with the running M; absolute
-// 32K block bases for the head
-__global__ void k_s3_scan(const int* __restrict__ tile_sum, u32 ntiles, i64* __restrict__ running,
-                          i64* __restrict__ tile_base, const int* __restrict__ bkrel, i64* __restrict__ bk) {
-  __shared__ i64 wsum[32];
-  __shared__ i64 carry;
-  const int tid = threadIdx.x;
-  if (tid == 0) carry = *running;
+// Segment finish in one launch (one block per tile): each block sums
+// the tile totals before it (<= ntiles L2-resident ints) for its own base,
+// writes its head block bases and fixes its captures; the block of the last
+// tile leaves M(Y0 + R - 1) in done[1] and the last block to finish moves it
+// to *running (every block has read *running by then) and re-arms the counter.
+__global__ void __launch_bounds__(256) k_s3_finish(const int* __restrict__ tile_sum, u32 ntiles, i64* running,
+                                                   const int* __restrict__ bkrel, i64* __restrict__ bk,
+                                                   const CaptureTarget2* __restrict__ caps, int n_cap, u64 Y0,
+                                                   unsigned long long* done) {
+  __shared__ i64 wred[8];
+  __shared__ i64 s_base;
+  const u32 t = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  i64 part = 0;
+  for (u32 i = tid; i < t; i += blockDim.x) part += tile_sum[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) wred[warp] = part;
   __syncthreads();
-  for (u32 base = 0; base < ntiles; base += 1024) {
-    const u32 i = base + tid;
-    const i64 v = i < ntiles ? tile_sum[i] : 0;
-    i64 incl = v;
-    for (int o = 1; o < 32; o <<= 1) {
-      i64 t = __shfl_up_sync(0xffffffffu, incl, o);
-      if ((tid & 31) >= o) incl += t;
-    }
-    if ((tid & 31) == 31) wsum[tid >> 5] = incl;
-    __syncthreads();
-    if (tid < 32) {
-      i64 x = wsum[tid], ix = x;
-      for (int o = 1; o < 32; o <<= 1) {
-        i64 t = __shfl_up_sync(0xffffffffu, ix, o);
-        if (tid >= o) ix += t;
-      }
-      wsum[tid] = ix - x;
-    }
-    __syncthreads();
-    const i64 excl = carry + wsum[tid >> 5] + incl - v;
-    if (i < ntiles) {
-      tile_base[i] = excl;
-      if (bk)
-        for (int q = 0; q < 4; q++) bk[(u64)i * 4 + q] = excl + bkrel[(u64)i * 4 + q];
-    }
-    __syncthreads();
-    if (tid == 1023) carry = excl + v;
-    __syncthreads();
+  if (tid == 0) {
+    i64 b = *(volatile i64*)running;
+    for (int w = 0; w < 8; w++) b += wred[w];
+    s_base = b;
   }
-  if (tid == 0) *running = carry;
-}
-
-// Q[j] += M(Yt - 1) for the captures of each tile (one block per tile)
-__global__ void k_s3_fixup(const CaptureTarget2* __restrict__ caps, int n_cap, u64 Y0,
-                           const i64* __restrict__ tile_base) {
-  const u64 Yt = Y0 + (u64)blockIdx.x * S2_T;
-  const int b = (int)tile_base[blockIdx.x];
-  for (int t = 0; t < n_cap; t++) {
-    const CaptureTarget2& ct = caps[t];
+  __syncthreads();
+  const i64 base = s_base;
+  if (bk && tid < 4) bk[(u64)t * 4 + tid] = base + bkrel[(u64)t * 4 + tid];
+  const u64 Yt = Y0 + (u64)t * S2_T;
+  for (int c = 0; c < n_cap; c++) {
+    const CaptureTarget2& ct = caps[c];
     u64 jhi = Yt ? udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt) : ~0ull;
     u64 jlo = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt + S2_T) + 1;
     if (jlo < ct.jq0) jlo = ct.jq0;
     if (jhi > ct.jq1) jhi = ct.jq1;
-    for (u64 j = jlo + threadIdx.x; j <= jhi; j += blockDim.x) ct.Q[j - ct.jq0] += b;
+    for (u64 j = jlo + tid; j <= jhi; j += blockDim.x) ct.Q[j - ct.jq0] += (int)base;
+  }
+  if (tid == 0) {
+    if (t == ntiles - 1) ((volatile i64*)done)[1] = base + tile_sum[t];
+    __threadfence();
+    const unsigned long long prev = atomicAdd(done, 1ull);
+    if (prev == ntiles - 1) {
+      __threadfence();
+      *(volatile i64*)running = ((volatile i64*)done)[1];
+      *(volatile unsigned long long*)done = 0ull;
+    }
   }
 }
 
@@ -683,8 +675,8 @@ int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
   if (kt) kt->end(st);
   MT_CUDA_CHECK(cudaGetLastError());
   if (kt) kt->begin(KT_OTHER, st);
-  k_s3_scan<<<1, 1024, 0, st>>>(a.tile_sum, a.ntiles, a.running, a.tile_base, a.bkrel, a.bk);
-  if (a.n_cap) k_s3_fixup<<<a.ntiles, 256, 0, st>>>(a.caps, a.n_cap, a.Y0, a.tile_base);
+  k_s3_finish<<<a.ntiles, 256, 0, st>>>(a.tile_sum, a.ntiles, a.running, a.bkrel, a.bk, a.caps, a.n_cap, a.Y0,
+                                        a.tstate);
   if (kt) kt->end(st);
   MT_CUDA_CHECK(cudaGetLastError());
   return MT_OK;
@@ -835,6 +827,7 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
       balloc(h->tbase, (size_t)max_tiles * 8) || balloc(h->bkrel, (size_t)max_tiles * 16))
     return MT_ERR_RESOURCE;
   MT_CUDA_CHECK(cudaMemsetAsync(h->ovf.p, 0, 8, st));
+  MT_CUDA_CHECK(cudaMemsetAsync(h->tstate.p, 0, 16, st));  // k_s3_finish: done counter, next running
   {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
