@@ -136,8 +136,8 @@ struct Sieve2Args {
   uint32_t* ticket;                 // tile order (zeroed per launch)
   unsigned long long* tstate;       // look-back words [ntiles] (zeroed per launch)
   int64_t* running;                 // M(Y0 - 1) in, M(Y0 + R - 1) out
-  const uint32_t *w1, *w2, *w3;     // presieve patterns (words)
-  uint64_t w1_period4, w2_period4, w3_period4;
+  const uint32_t *w1, *w2;          // presieve patterns (words)
+  uint64_t w1_period4, w2_period4;
   const uint32_t* primes;
   const double* rprimes;
   const uint8_t* logs;

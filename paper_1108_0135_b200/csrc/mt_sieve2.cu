@@ -14,13 +14,14 @@
 //   tile     = 2^17 cells (one byte each, 128 KB of shared memory, 1 CTA/SM,
 //              1024 threads); tiles are 2^17-aligned, so every tile but the
 //              first lies in one binade and shares one classification threshold
-//   presieve = three L2-resident byte patterns added word-wise on load:
-//              W1 (2,3,5,7 logs; 0x80 at 4,9,25,49; period 485100),
-//              W2 (11,13,17,19,23; period 1062347), W3 (29,31,37,41; 1363783)
-//   in-tile  = primes 43 <= p <= 2^17 (warp per prime below 1024, lane per
+//   presieve = two L2-resident byte patterns added word-wise on load:
+//              W1 (2,3,5,7,11 logs; 0x80 at 4,9,25,49; period 485100),
+//              W2 (13,17,19,23; period 96577) -- small patterns stay in L2;
+//              a third pattern for 29..41 cost more than marking those primes
+//   in-tile  = primes 29 <= p <= 2^16 (warp per prime below 1024, lane per
 //              prime above) and squares p^2 for 11 <= p <= 362 (shared-memory
 //              byte reductions, red.shared.add / .or, on the cell's 32-bit word)
-//   buckets  = primes p > 2^17 and squares p^2 > 2^17: a producer kernel per
+//   buckets  = primes p > 2^16 and squares p^2 > 2^17: a producer kernel per
 //              segment enumerates every hit (balanced in chunks of hits) and
 //              appends (offset, log) to a producer-private list per tile, square
 //              flags from the list's back (shared-memory cursors, no global
@@ -342,8 +343,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
     {
       const u32* __restrict__ w1 = a.w1 + (u32)((Yt % a.w1_period4) >> 2);
       const u32* __restrict__ w2 = a.w2 + (u32)((Yt % a.w2_period4) >> 2);
-      const u32* __restrict__ w3 = a.w3 + (u32)((Yt % a.w3_period4) >> 2);
-      for (int i = tid; i < (int)S2_W; i += S2_NT) st[i] = w1[i] + w2[i] + w3[i];
+      for (int i = tid; i < (int)S2_W; i += S2_NT) st[i] = w1[i] + w2[i];
     }
     for (u32 b = tid; b < a.nprod && b < S2_MAXPROD; b += S2_NT) s_cnt[b] = a.counts[(u64)b * a.ntiles + tile];
     __syncthreads();
@@ -735,9 +735,9 @@ std::vector<uint32_t> pattern_words(u64 P, const std::vector<u32>& logp_primes, 
 }  // namespace
 
 struct Sieve2Host {
-  Buf w1, w2, w3, prm, rp, lg, buf, counts, tstate, ovf, tsum, tbase, bkrel;
+  Buf w1, w2, prm, rp, lg, buf, counts, tstate, ovf, tsum, tbase, bkrel;
   int nsm = 148;
-  u64 P1 = 485100, P2 = 1062347, P3 = 1363783;
+  u64 P1 = 485100, P2 = 96577;  // 2^2 3^2 5^2 7^2 11, 13 17 19 23
   std::vector<u32> p;
   u32 nprod = 0, cap = 0, max_tiles = 0;
   u32 fill_smem = 0;  // dynamic shared memory available to k_bucket_fill
@@ -778,9 +778,8 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
     MT_CUDA_CHECK(cudaStreamSynchronize(st));  // the host vector dies at return
     return MT_OK;
   };
-  if (up(h->w1, pattern_words(h->P1, {2, 3, 5, 7}, {4, 9, 25, 49}))) return MT_ERR_RESOURCE;
-  if (up(h->w2, pattern_words(h->P2, {11, 13, 17, 19, 23}, {}))) return MT_ERR_RESOURCE;
-  if (up(h->w3, pattern_words(h->P3, {29, 31, 37, 41}, {}))) return MT_ERR_RESOURCE;
+  if (up(h->w1, pattern_words(h->P1, {2, 3, 5, 7, 11}, {4, 9, 25, 49}))) return MT_ERR_RESOURCE;
+  if (up(h->w2, pattern_words(h->P2, {13, 17, 19, 23}, {}))) return MT_ERR_RESOURCE;
   if (const char* e = getenv("MT_S2_BIG_LOG2")) h->big_min = 1u << atoi(e);
   // bucket space: producers = SMs; capacity from the expected hits per (producer, tile)
   int dev, nsm;
@@ -869,10 +868,10 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
   a.tstate = (unsigned long long*)h->tstate.p;
   a.ticket = (uint32_t*)((unsigned long long*)h->tstate.p + ntiles);
   a.running = running;
-  a.w1 = (const u32*)h->w1.p; a.w2 = (const u32*)h->w2.p; a.w3 = (const u32*)h->w3.p;
-  a.w1_period4 = 4 * h->P1; a.w2_period4 = 4 * h->P2; a.w3_period4 = 4 * h->P3;
+  a.w1 = (const u32*)h->w1.p; a.w2 = (const u32*)h->w2.p;
+  a.w1_period4 = 4 * h->P1; a.w2_period4 = 4 * h->P2;
   a.primes = (const u32*)h->prm.p; a.rprimes = (const double*)h->rp.p; a.logs = (const uint8_t*)h->lg.p;
-  a.p_first = std::min(idx_gt(42), end);
+  a.p_first = std::min(idx_gt(28), end);  // A primes start at 29 (2..23 are presieved)
   a.p_warp_end = std::max(a.p_first, std::min(idx_gt(1023), end));
   a.p_small_end = std::max(a.p_warp_end, std::min(idx_gt(h->big_min), end));
   a.p_b2 = std::max(a.p_warp_end, std::min(idx_gt(S2_B2_MIN - 1), a.p_small_end));
