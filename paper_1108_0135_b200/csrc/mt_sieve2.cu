@@ -45,6 +45,9 @@
 #define S2_NT 1024               // threads per tile CTA
 #define S2_CH (S2_T / 32)        // 32-cell chunks per tile
 #define S2_MAXPROD 512           // bucket producers whose counts are staged in shared memory
+#ifndef S2_A_MAX
+#define S2_A_MAX 1024u           // warp-per-prime marks below this, lane-per-prime from here
+#endif
 #ifndef S2_B2_MIN
 #define S2_B2_MIN (1u << 15)     // in-tile primes from here on hit <= 4 times per tile (measured: 2^15 > 2^14 > 2^13)
 #endif
@@ -872,7 +875,7 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
   a.w1_period4 = 4 * h->P1; a.w2_period4 = 4 * h->P2;
   a.primes = (const u32*)h->prm.p; a.rprimes = (const double*)h->rp.p; a.logs = (const uint8_t*)h->lg.p;
   a.p_first = std::min(idx_gt(28), end);  // A primes start at 29 (2..23 are presieved)
-  a.p_warp_end = std::max(a.p_first, std::min(idx_gt(1023), end));
+  a.p_warp_end = std::max(a.p_first, std::min(idx_gt(S2_A_MAX - 1), end));
   a.p_small_end = std::max(a.p_warp_end, std::min(idx_gt(h->big_min), end));
   a.p_b2 = std::max(a.p_warp_end, std::min(idx_gt(S2_B2_MIN - 1), a.p_small_end));
   a.sq_first = std::min(idx_gt(10), end);
