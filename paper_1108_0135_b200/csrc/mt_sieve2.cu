@@ -265,11 +265,11 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
 __device__ __forceinline__ u32 mu_word(u32 w, u32 kthr, int& sum) {
   const u32 nsq = ~w & 0x80808080u;                              // not square-flagged
   const u32 g = ((w & 0x7f7f7f7fu) + kthr) & 0x80808080u;        // s > thr
-  const u32 x = g ^ ((w & 0x01010101u) << 7);                    // mu = +1 iff (s > thr) xor odd
+  const u32 x = g ^ ((w << 7) & 0x80808080u);                    // mu = +1 iff (s > thr) xor odd
   const u32 pl = x & nsq, mi = ~x & nsq;
-  sum += __popc(pl) - __popc(mi);
-  const u32 p1 = pl >> 7, m1 = mi >> 7;
-  return p1 | (m1 * 255u);
+  const u32 out = (pl >> 7) + (mi >> 7) * 255u;                  // bytes +1 / -1 (0xff) / 0
+  sum = __dp4a((int)out, 0x01010101, sum);                        // signed byte sum
+  return out;
 }
 
 __device__ __forceinline__ int mu_cell(u32 s, int thr) {
