@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
   u32* gcnt = rcnt + a.ntiles + 1;
   u32* cnt2 = gcnt + a.ntiles;
   u32* stage = dsm + ((3 * a.ntiles + 1 + 3) & ~3u);  // 16-byte aligned (bulk copies)
+  const u32 rcnt_s = (u32)__cvta_generic_to_shared(rcnt);
+  const u32 stage_s = (u32)__cvta_generic_to_shared(stage);
   __shared__ u32 s_q0[FBATCH];
   __shared__ u32 s_step[FBATCH];
   __shared__ u32 s_val[FBATCH];
@@ -187,7 +189,11 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
         u32 pos = s_q0[k] + ci * FITEM * step;
         const u32 end = (u32)min((u64)R, (u64)pos + (u64)FITEM * step);
         if (!(val & (0x80u << 17))) {
-          // four slot allocations in flight; hits past `end` count into the dummy rcnt[nt]
+          // four slot allocations in flight; hits past `end` count into the dummy
+          // rcnt[nt].  Shared addresses are explicit 32-bit (the generic stage
+          // pointer made the compiler rebuild the window base per store); the
+          // common case is one predicated st.shared, a full bin falls back to a
+          // direct global store
           for (; pos < end; pos += 4 * step) {
             u32 t[4], sl[4];
 #pragma unroll
@@ -196,16 +202,22 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
               t[h] = ph < end ? ph >> 17 : nt;
             }
 #pragma unroll
-            for (int h = 0; h < 4; h++) sl[h] = atomicAdd(&rcnt[t[h]], 1u);
+            for (int h = 0; h < 4; h++)
+              asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(sl[h]) : "r"(rcnt_s + 4 * t[h]) : "memory");
+            bool spill = false;
 #pragma unroll
             for (int h = 0; h < 4; h++) {
-              if (t[h] < nt) {
-                const u32 e = ((pos + h * step) & (S2_T - 1)) | val;
-                if (sl[h] < bin) {
-                  stage[t[h] * bin + sl[h]] = e;
-                } else {
+              const u32 e = ((pos + h * step) & (S2_T - 1)) | val;
+              const bool in = t[h] < nt && sl[h] < bin;
+              if (in) asm volatile("st.shared.u32 [%0], %1;" ::"r"(stage_s + 4 * (t[h] * bin + sl[h])), "r"(e) : "memory");
+              spill |= t[h] < nt && sl[h] >= bin;
+            }
+            if (spill) {  // rare: a full bin
+#pragma unroll
+              for (int h = 0; h < 4; h++) {
+                if (t[h] < nt && sl[h] >= bin) {
                   const u32 g = gcnt[t[h]] + sl[h];
-                  if (g < cap) out[t[h] * cap + g] = e;
+                  if (g < cap) out[t[h] * cap + g] = ((pos + h * step) & (S2_T - 1)) | val;
                 }
               }
             }
