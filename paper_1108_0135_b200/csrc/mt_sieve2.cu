@@ -814,6 +814,7 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
     //   ~1024 * FITEM hits of one producer spread over the segment's tiles
     const double rounds = m * max_tiles / (1024.0 * FITEM) + 1.0;
     h->cap = (u32)std::ceil(m + 8.0 * std::sqrt(m) + 2.0 * rounds + 32.0);
+    if (const char* ev = getenv("MT_S2_CAP")) h->cap = std::min<u32>(h->cap, (u32)std::max(32, atoi(ev)));  // test hook
     h->cap = (h->cap + 31) & ~31u;
     if (balloc(h->buf, (size_t)h->nprod * max_tiles * h->cap * 4) ||
         balloc(h->counts, (size_t)h->nprod * max_tiles * 4))

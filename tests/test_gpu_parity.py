@@ -261,6 +261,22 @@ def test_production_sieve_mu(engine, oracle, y1, length):
     assert np.array_equal(mu, ref), int((mu != ref).sum())
 
 
+@pytest.mark.parametrize("env", [{"MT_FILL_BIN": "16"}, {"MT_FILL_BIN": "0"}, {"MT_S2_CAP": "64"}])
+def test_production_sieve_stress_paths(engine, oracle, monkeypatch, env):
+    """The sieve's rare paths give the same mu: bins too small for a round (entries
+    spill to direct global stores), no write-combining at all, and bucket lists far
+    over capacity (flagged, and the tile recomputes that producer's hits exactly)."""
+    from paper_1108_0135_b200 import _lib
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    y1, length = 4_641_588_833_612 - 10**6, 2 * 10**6
+    mu = np.zeros(length, np.int8)
+    _lib.check(_lib.lib().mt_sieve_fast(y1, y1 + length - 1, _lib.ptr(mu), None))
+    ref = oracle.mu_range(oracle.get_kernels("c"), y1, y1 + length - 1)
+    assert np.array_equal(mu, ref), int((mu != ref).sum())
+
+
 def test_production_sieve_prefix(engine, oracle):
     from paper_1108_0135_b200 import _lib
 
