@@ -244,25 +244,31 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
-    cfg = P.EngineConfig(device=local, engine_flags=_lib.MT_FLAG_TIMING, stream=stream.cuda_stream)
+    # the timed steps run the plain engine: per-kernel CUDA events (MT_FLAG_TIMING)
+    # cost ~4 % of a step, so the kernel breakdown and the roofline's per-launch
+    # times come from one instrumented step right after the timed region
+    cfg = P.EngineConfig(device=local, stream=stream.cuda_stream)
+    cfg_t = P.EngineConfig(device=local, engine_flags=_lib.MT_FLAG_TIMING, stream=stream.cuda_stream)
     job = engine.make_job([n], u, cfg, rank=rank, world=world)
+    job_t = engine.make_job([n], u, cfg_t, rank=rank, world=world)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    def make_plan(j):
+        return distributed.DevicePlan(j) if world > 1 else _SinglePlan(j)
+
     # ---- device-timed job: plan resident in HBM, phases + collectives per step
-    plan = distributed.DevicePlan(job) if world > 1 else None
-    if plan is None:
-        plan = _SinglePlan(job)
+    plan = make_plan(job)
     res = _lib.MtResult()
     fin = np.zeros(n // u, np.int64)
     res.finals = fin.ctypes.data_as(_lib._pi64)  # M(n) is read back once per step
     for _ in range(args.warmup):
         _one(plan, world, res)
     barrier()
-    times, launches, kms, kcnt = [], 0, {}, {}
+    times, launches = [], 0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             barrier()
@@ -272,14 +278,19 @@ def main():
             e1.record(stream)
             barrier()
             times.append(e0.elapsed_time(e1))
-            st = _lib.stats_dict(res.stats)
-            launches += int(st["kernel_launches"])
-            for k, v in st["kernel_ms"].items():
-                kms[k] = kms.get(k, 0.0) + v
-                kcnt[k] = kcnt.get(k, 0) + st["kernel_count"][k]
+            launches += int(_lib.stats_dict(res.stats)["kernel_launches"])
     value_m = int(fin[0])
-    stats_last = _lib.stats_dict(res.stats)
     plan.close()
+    # ---- one instrumented step (same job, per-kernel events on the engine's stream)
+    plan = make_plan(job_t)
+    _one(plan, world, res)
+    barrier()
+    stats_last = _lib.stats_dict(res.stats)
+    kms = dict(stats_last["kernel_ms"])
+    kcnt = dict(stats_last["kernel_count"])
+    plan.close()
+    if int(fin[0]) != value_m:
+        raise RuntimeError("instrumented step disagrees with the timed steps")
     ms = max(times)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -320,18 +331,21 @@ def main():
     avg_ms = kms[dom] / max(1, kcnt[dom])
     roof = {"kernel": dom}
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
-    seg = nsm * 4 * (1 << 17)  # tail segment: 4 tiles of 2^17 cells per SM (mt_engine.cu)
+    # tail segment: MT_SEG_TILES_PER_SM (default 6) tiles of 2^17 cells per SM (mt_engine.cu)
+    seg = nsm * int(os.environ.get("MT_SEG_TILES_PER_SM", "6")) * (1 << 17)
     if dom in ("sieve_tile", "sieve_large"):
         # 10 algorithmic bytes per y-value (state write+read 2 B, M(y) 8 B);
         # cells sieved per step = the head [0, head_end) + the tail segments
         ys_per_launch = (stats_last["head_end"] + stats_last["n_tail_segments"] * seg) \
-            / max(1, kcnt[dom] / args.steps)
+            / max(1, kcnt[dom])
         A = 10 * ys_per_launch / (avg_ms * 1e-3) / 1e9
         P_ = pk.get("hbm_gbs", 6650.0)
         tr = _ncu_traffic(dom)
         roof |= {"bound": "hbm", "achieved": A, "peak": P_, "unit": "GB/s", "frac": A / P_,
                  "traffic": tr, "per_unit": "10 B per y-value (SURVEY.md §8(d))",
                  "units_per_launch": ys_per_launch, "avg_launch_ms": avg_ms,
+                 "timing": "CUDA events around every launch on the engine's stream, one instrumented "
+                           "step right after the timed region (events inside the timed steps cost ~4 %)",
                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in pk else "fallback",
                  "note": ("the sieve keeps its state in shared memory: measured DRAM traffic per launch (ncu, "
                           "profiles/traffic.json; mostly the bucket lists) is ~1 B/y, far below the 10 B/y "
@@ -339,7 +353,7 @@ def main():
                           "itself is bound by shared-memory reductions and issue (profiles/r01_final_ncu.txt)")}
     else:
         ops = 7 * stats_last["counted_items"] + 4 * stats_last["dense_items"]
-        A = ops / (kms[dom] / args.steps * 1e-3) / 1e12
+        A = ops / (kms[dom] * 1e-3) / 1e12
         roof |= {"bound": "int", "achieved": A, "peak": 18.56, "unit": "Tops/s", "frac": A / 18.56,
                  "traffic": None}
     # the counted walk against its issue roofline: one exact division per squarefree m
@@ -347,7 +361,7 @@ def main():
     # elements per list entry; its SASS is 76 instructions per 16 items (16 DFMA,
     # 18 IMAD, 16 LEA.HI, 16 IADD3, 6 LDS.128, 4 loop), so at 4 warp-instructions
     # per clock per SM the issue roofline is 128 / 4.75 = 26.9 items/clk/SM
-    upd_ms = kms.get("counted", 0.0) / args.steps
+    upd_ms = kms.get("counted", 0.0)
     upd = None
     if upd_ms > 0:
         items = 6 / 3.141592653589793 ** 2 * stats_last["counted_items"]
@@ -381,7 +395,7 @@ def main():
         "clocks": clocks,
         "phases_ms": {k: stats_last[k] for k in ("ms_update_head", "ms_sieve_tail", "ms_qgather", "ms_finalize",
                                                   "ms_setup")},
-        "kernel_ms_per_step": {k: v / args.steps for k, v in kms.items() if v},
+        "kernel_ms_per_step": {k: v for k, v in kms.items() if v},  # the instrumented step
         "work": {"counted_items": stats_last["counted_items"], "dense_items": stats_last["dense_items"],
                  "head_end": stats_last["head_end"], "q_entries": stats_last["q_entries"]},
     }

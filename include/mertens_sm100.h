@@ -116,7 +116,7 @@ typedef struct {
   uint64_t q_budget_bytes; /* device bytes for the Q tables (default 48 GiB)       */
   uint32_t seg_log2_head;  /* head segment length 2^x (x >= 17; default: 2 tiles of
                               2^17 cells per SM, MT_SEG_TILES_PER_SM_HEAD overrides) */
-  uint32_t seg_log2_tail;  /* tail segment length 2^x (x >= 17; default: 4 tiles of
+  uint32_t seg_log2_tail;  /* tail segment length 2^x (x >= 17; default: 6 tiles of
                               2^17 cells per SM, MT_SEG_TILES_PER_SM overrides)    */
   int32_t device;          /* CUDA device ordinal (-1: current)                    */
   /* multi-GPU sharding: rank r of w sieves the head redundantly,
