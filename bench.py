@@ -1,6 +1,7 @@
 """Benchmark: exact M(n) (default n = 10^19, BASELINE.json's metric) on N B200s.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--n 1e19] [--impl ours|reference]
+                    [--dist-backend nccl|gloo]
 
 One step = one complete exact job: segmented Moebius sieve of y in [1, u],
 the harmonic-array update of all K = n // u elements, the quotient-table
@@ -10,9 +11,16 @@ CUDA events on the engine's stream, max over ranks).  `e2e` is the same
 metric through the public API `mertens_exact(n)` (host in, host out: M(n),
 the K finals and the 4M captured quotients copied back every step).
 
+--gpus N > 1 without a torchrun environment re-launches this script under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU,
+NCCL; --dist-backend gloo lets N ranks share the GPUs of a smaller box, the
+ranks then take cuda:(local_rank mod device_count)).  The ranks split the
+job as DESIGN.md §5 describes; the world size actually used is asserted.
+
 --impl reference times the reference algorithm on the host cores instead
 (oracle/_ref's compiled kernels where they apply, else the oracle's C port),
-on a bounded sample of the same job, extrapolated to the whole job.
+on a bounded sample of the same job, extrapolated to the whole job, and
+measures the reference end to end at the anchor config n = 10^13.
 Under torchrun (N > 1) rank 0 alone runs the reference arm.
 """
 
@@ -21,12 +29,11 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
-import threading
 import time
-from concurrent.futures import ThreadPoolExecutor
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -40,6 +47,8 @@ METRIC = BASE["metric"]
 PAPER = {10**16: -3195437, 10**17: -21830254, 10**18: -46758740, 10**19: 899990187,
          10**20: 461113106, 10**21: -3395895277, 10**22: -2061910120,
          11609864264058592345: -1995900927}
+# reference values measured by running the reference (tests/golden)
+ANCHOR_M = {10**13: 599582, 10**12: 62366}
 
 
 def parse_n(s: str) -> int:
@@ -53,6 +62,14 @@ def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except OSError:
+        return {}
+
+
+def ncu_metrics():
+    """Per-kernel ncu counters committed under profiles/ (one `--set full` capture each)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_metrics.json")))
+    except (OSError, ValueError):
         return {}
 
 
@@ -101,31 +118,37 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU reference arm
-def _closed_form_items(n: int, u: int):
-    """counted / dense pair totals of the reference's block loop (engine.py:134-159)."""
+def _walk_state_at(H, y1):
+    """The dense-walk cursor of every element at block start y1, in closed form
+    (the reference's _replay_walk_state, engine.py:715-728): the next d is the
+    largest d <= xcut with floor(v/d) >= y1."""
     from oracle import engine_port as E
 
-    if n < 2**64:
-        H = E.HarmonicArray(n, u)
-        counted = int(H.mcut.sum(dtype=np.uint64))
-        dense = int(np.where(H.xcut >= H.lo, H.xcut - H.lo + np.uint64(1), 0).sum(dtype=np.uint64))
-        return counted, dense, H
-    ps = E.big_params(n, u)
-    return sum(p[3] for p in ps), sum(max(0, p[2] - p[4] + 1) for p in ps), None
+    d = np.minimum(H.xcut, H.v // np.uint64(max(1, y1)))
+    act = d >= H.lo
+    dn = np.where(act, d, H.lo - np.uint64(1))
+    yn = np.where(act, H.v // np.maximum(dn, np.uint64(1)), E.SENTINEL)
+    return dn, yn
 
 
-def cpu_reference_sample(n: int, u: int, threads: int, budget_s: float = 12.0):
-    """Time the reference algorithm on a bounded sample of the job on `threads`
-    host cores and extrapolate to the whole job.
+def cpu_reference_sample(n: int, u: int, threads: int):
+    """Time the reference algorithm on a bounded sample of the job and
+    extrapolate to the whole job (SURVEY.md §8(d) CPU-baseline plan).
 
-    apply : the reference's apply_block on the first y-block [1, 2^20] for every
-            S-th element (oracle/_ref's compiled kernel when n <= 4e18, where it
-            is defined; above that the oracle's C port with mod-2^64 wrap, since
-            the reference's i128 guard rejects those n), element chunks on
-            `threads` threads -> pair rate.
-    sieve : the reference's sieve_logprime on 2^26 y-values at y = u/2 split
-            over `threads` threads (sieve.py:168-174) -> y rate.
-    job   ~= (counted + dense pairs) / pair rate + u / y rate."""
+    apply : the reference's apply_block, single-threaded as the reference runs it
+            (engine.py:380-384), for every S-th element on two y-blocks: the first
+            block [1, 2^22] (counted-walk heavy) and a block at y = 2^30 inside
+            the dense region (random M gathers).  The two blocks' (counted, dense)
+            pair counts and times give the per-pair costs t_c, t_d.  oracle/_ref's
+            compiled kernel when n <= 4e18 (where it is defined), else the oracle's C
+            port with mod-2^64 wrap (the reference's i128 guard rejects those n).
+    sieve : the reference's sieve_logprime on 2^28 y at y = u/2 over `threads`
+            threads (its `workers`, sieve.py:168-174).
+    job   ~= counted * t_c + dense * t_d + u / sieve rate (the reference overlaps
+            one block of sieve with the apply; the head is apply-bound, the tail
+            sieve-bound, so the two add)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     from oracle import engine_port as E
 
     kern_c = E.get_kernels("c")
@@ -133,39 +156,37 @@ def cpu_reference_sample(n: int, u: int, threads: int, budget_s: float = 12.0):
         kern_ref = E.get_kernels("ref")
     except Exception:
         kern_ref = None
-    counted, dense, H = _closed_form_items(n, u)
-    # ---- apply sample
-    L = 1 << 22
+    H = E.HarmonicArray(n, u)
+    counted = int(H.mcut.sum(dtype=np.uint64))
+    dense = int(np.where(H.xcut >= H.lo, H.xcut - H.lo + np.uint64(1), 0).sum(dtype=np.uint64))
     K = n // u
     stride = max(1, K // 1024)
     ks = np.arange(0, K, stride)
-    if H is None:
-        raise RuntimeError("CPU sample for n >= 2^64 not supported")
-    sub = {f: np.ascontiguousarray(getattr(H, f)[ks]) for f in ("v", "lo", "xcut", "mcut", "dnext", "ynext", "D")}
     primes = E.generate_primes(E.ceil_sqrt(u) + 1)
     logs, wheel = E.build_logs(primes), E.build_wheel()
-    mu = E.mu_range(kern_c, 1, L, primes, logs, wheel)
-    mp = np.cumsum(mu, dtype=np.int64)
     use_ref_apply = kern_ref is not None and n <= 4 * 10**18
-    chunks = np.array_split(np.arange(len(ks)), threads)
-
-    def run_chunk(ix):
-        acc = np.zeros(len(ix), np.int64 if use_ref_apply else np.uint64)
-        a = {f: np.ascontiguousarray(sub[f][ix]) for f in sub}
+    L = 1 << 22
+    blocks = []
+    for y1 in (1, 1 << 30):
+        y2 = min(y1 + L - 1, u)
+        mu = E.mu_range(kern_c, y1, y2, primes, logs, wheel)
+        mp = np.cumsum(mu, dtype=np.int64)  # the base M(y1 - 1) does not change the work
+        dn, yn = _walk_state_at(H, y1)
+        a = {f: np.ascontiguousarray(getattr(H, f)[ks]) for f in ("v", "lo", "xcut", "mcut")}
+        dn, yn = np.ascontiguousarray(dn[ks]), np.ascontiguousarray(yn[ks])
+        acc = np.zeros(len(ks), np.int64 if use_ref_apply else np.uint64)
+        t0 = time.perf_counter()
         if use_ref_apply:
-            c, d = kern_ref.apply_block(acc, a["v"], a["lo"], a["xcut"], a["mcut"], a["dnext"], a["ynext"],
-                                        1, L, mp, None)
+            c, d = kern_ref.apply_block(acc, a["v"], a["lo"], a["xcut"], a["mcut"], dn, yn, y1, y2, mp, None)
         else:
-            c, d = kern_c.apply_block_wrap(acc, a["v"], a["lo"], a["xcut"], a["mcut"], a["dnext"], a["ynext"],
-                                           1, L, mp)
-        return int(c) + int(d)
-
-    t0 = time.perf_counter()
-    with ThreadPoolExecutor(threads) as ex:
-        pairs = sum(ex.map(run_chunk, chunks))
-    t_apply = time.perf_counter() - t0
-    pair_rate = pairs / t_apply
-    # ---- sieve sample
+            c, d = kern_c.apply_block_wrap(acc, a["v"], a["lo"], a["xcut"], a["mcut"], dn, yn, y1, y2, mp)
+        blocks.append((int(c), int(d), time.perf_counter() - t0))
+    (c1, d1, s1), (c2, d2, s2) = blocks
+    det = c1 * d2 - c2 * d1
+    tc = (s1 * d2 - s2 * d1) / det if det else 0.0
+    td = (c1 * s2 - c2 * s1) / det if det else 0.0
+    if not (tc > 0 and td > 0):  # ill-conditioned: one blended rate
+        tc = td = (s1 + s2) / max(1, c1 + d1 + c2 + d2)
     SL = 1 << 28
     y0 = max(2, u // 2)
     sk = kern_ref if kern_ref is not None else kern_c
@@ -175,15 +196,39 @@ def cpu_reference_sample(n: int, u: int, threads: int, budget_s: float = 12.0):
         list(ex.map(lambda r: sk.sieve_logprime(r[0], r[1], primes, logs, wheel), rngs))
     t_sieve = time.perf_counter() - t0
     y_rate = SL / t_sieve
-    est = (counted + dense) / pair_rate + u / y_rate
+    t_apply = counted * tc + dense * td
+    est = t_apply + u / y_rate
     kind = "reference" if (use_ref_apply and kern_ref is not None) else "port"
-    sample = (f"apply_block on y in [1,2^22] for every {stride}-th of K={K} elements ({pairs:.3g} pairs, "
-              f"{'oracle/_ref compiled kernel' if use_ref_apply else 'oracle C port, mod-2^64 (reference kernel rejects n>4e18)'})"
-              f" + sieve_logprime of 2^28 y at y={y0} ({'oracle/_ref' if kern_ref is not None else 'oracle C port'}), "
-              f"{threads} threads; job extrapolated as {counted + dense:.4g} pairs / {pair_rate:.4g} pairs/s + "
-              f"u / {y_rate:.4g} y/s = {est:.4g} s")
+    sample = (f"apply_block single-threaded (as the reference) on every {stride}-th of K={K} elements over the "
+              f"blocks [1,2^22] ({c1:.3g} counted + {d1:.3g} dense pairs, {s1:.3g} s) and [2^30,2^30+2^22) "
+              f"({c2:.3g} + {d2:.3g} pairs, {s2:.3g} s) -> {tc * 1e9:.3g} ns/counted pair, "
+              f"{td * 1e9:.3g} ns/dense pair ({'oracle/_ref compiled kernel' if use_ref_apply else 'oracle C port, mod-2^64 (reference kernel rejects n>4e18)'})"
+              f"; sieve_logprime of 2^28 y at y={y0} on {threads} threads ({'oracle/_ref' if kern_ref is not None else 'oracle C port'}); "
+              f"job extrapolated as {counted:.4g} counted x t_c + {dense:.4g} dense x t_d + u / {y_rate:.4g} y/s "
+              f"= {t_apply:.4g} + {u / y_rate:.4g} = {est:.4g} s")
     return {"value": u / est, "unit": "y-values/s", "cores": threads, "kind": kind, "sample": sample,
-            "est_job_s": est, "pair_rate": pair_rate, "y_rate": y_rate, "sample_s": t_apply + t_sieve}
+            "est_job_s": est, "t_counted_ns": tc * 1e9, "t_dense_ns": td * 1e9, "y_rate": y_rate,
+            "sample_s": s1 + s2 + t_sieve, "fits_in_driver_run": False}
+
+
+def reference_anchor(n: int, threads: int):
+    """The reference end to end at a config it finishes in the driver window:
+    oracle/engine_port's restated job loop (engine.py:255-402) driving the
+    reference's own compiled kernels (oracle/_ref), sieve on `threads` workers,
+    apply on one thread -- as the reference runs."""
+    from oracle import engine_port as E
+
+    try:
+        E.get_kernels("ref")
+        kern = "ref"
+    except Exception:
+        kern = "c"
+    t0 = time.perf_counter()
+    r = E.mertens_exact(n, kern, workers=threads)
+    wall = time.perf_counter() - t0
+    return {"n": str(n), "M": r.value, "M_ok": ANCHOR_M.get(n) in (None, r.value), "u": r.u, "wall_s": wall,
+            "value": r.u / wall, "unit": "y-values/s", "kernels": "oracle/_ref" if kern == "ref" else "oracle C port",
+            "cores": threads, "measured": "end to end, one run", "fits_in_driver_run": True}
 
 
 def reference_arm(args, n, u, rank, world):
@@ -195,6 +240,7 @@ def reference_arm(args, n, u, rank, world):
     vals = [cpu_reference_sample(n, u, threads) for _ in range(args.steps)]
     v = statistics.median(r["value"] for r in vals)
     last = vals[-1]
+    anchor = None if args.no_anchor else reference_anchor(parse_n(args.anchor_n), threads)
     line = {
         "metric": METRIC, "value": v, "unit": "y-values/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * u / v, "higher_is_better": True, "scaling": "strong",
@@ -203,14 +249,36 @@ def reference_arm(args, n, u, rank, world):
         "cpu_baseline": {k: last[k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "y-values/s"},
         "e2e": {"value": v, "unit": "y-values/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
+        "extrapolated": True,
+        "anchor": anchor,
     }
     print(json.dumps(line), flush=True)
 
 
 def config_block(n, u, world):
     return {"workload": f"M({n}) plus all M(floor(n/c)) for c <= K (exact, 1 target)", "n": str(n), "u": u,
-            "K": n // u, "parallelism": f"y-shard x{world} (head redundant, tail y-segments split, 1 int64 allreduce)",
+            "K": n // u, "parallelism": f"y-shard x{world} (head redundant, odd-y tail ranges, 1 int64 allreduce)",
             "l2": "inputs larger than L2: the job streams u sieve cells and a multi-GB quotient table per step"}
+
+
+# ---------------------------------------------------------------- launch
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _relaunch(args) -> int:
+    """--gpus N outside torchrun: re-run this script as N ranks (one per GPU)."""
+    env = dict(os.environ)
+    if args.dist_backend == "nccl":
+        env.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nranks) for the record
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 # ---------------------------------------------------------------- our arm
@@ -221,13 +289,20 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--n", default="1e19")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-anchor", action="store_true")
+    ap.add_argument("--anchor-n", default="1e13", help="end-to-end config both arms run in full")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch(args))
     n = parse_n(args.n)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but the launcher started {world} ranks")
 
     import paper_1108_0135_b200 as P
 
@@ -240,15 +315,20 @@ def main():
 
     from paper_1108_0135_b200 import _lib, distributed, engine
 
-    torch.cuda.set_device(local)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+    tdev = torch.device("cuda", dev) if args.dist_backend == "nccl" else torch.device("cpu")
     stream = torch.cuda.current_stream()
     # the timed steps run the plain engine: per-kernel CUDA events (MT_FLAG_TIMING)
     # cost ~4 % of a step, so the kernel breakdown and the roofline's per-launch
     # times come from one instrumented step right after the timed region
-    cfg = P.EngineConfig(device=local, stream=stream.cuda_stream)
-    cfg_t = P.EngineConfig(device=local, engine_flags=_lib.MT_FLAG_TIMING, stream=stream.cuda_stream)
+    cfg = P.EngineConfig(device=dev, stream=stream.cuda_stream)
+    cfg_t = P.EngineConfig(device=dev, engine_flags=_lib.MT_FLAG_TIMING, stream=stream.cuda_stream)
     job = engine.make_job([n], u, cfg, rank=rank, world=world)
     job_t = engine.make_job([n], u, cfg_t, rank=rank, world=world)
 
@@ -256,6 +336,13 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=tdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     def make_plan(j):
         return distributed.DevicePlan(j) if world > 1 else _SinglePlan(j)
@@ -268,8 +355,8 @@ def main():
     for _ in range(args.warmup):
         _one(plan, world, res)
     barrier()
-    times, launches = [], 0
-    with ClockSampler(local) as clk:
+    times, launches = [], []
+    with ClockSampler(dev) as clk:
         for _ in range(args.steps):
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -278,7 +365,7 @@ def main():
             e1.record(stream)
             barrier()
             times.append(e0.elapsed_time(e1))
-            launches += int(_lib.stats_dict(res.stats)["kernel_launches"])
+            launches.append(int(_lib.stats_dict(res.stats)["kernel_launches"]))
     value_m = int(fin[0])
     plan.close()
     # ---- one instrumented step (same job, per-kernel events on the engine's stream)
@@ -291,17 +378,12 @@ def main():
     plan.close()
     if int(fin[0]) != value_m:
         raise RuntimeError("instrumented step disagrees with the timed steps")
-    ms = max(times)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        ms_all = ms
+    ms = allmax(max(times))
     clocks = clk.summary()
 
     # ---- end to end through the public API (host in, host out)
     e2e_steps = args.e2e_steps or args.steps
-    e2e_cfg = P.EngineConfig(device=local)
+    e2e_cfg = P.EngineConfig(device=dev, distributed=world > 1)
     r = P.mertens_exact(n, e2e_cfg)  # warm
     wall = []
     for _ in range(e2e_steps):
@@ -312,74 +394,30 @@ def main():
         if world > 1:
             dist.barrier()
         wall.append(time.perf_counter() - t0)
-    e2e_s = max(wall)
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = allmax(max(wall))
     K = n // u
     d2h = 8 * K + 8 * len(r._cp_m)
     h2d = 16
+    # ---- the anchor config, end to end (the reference arm runs it in full too)
+    anchor = None
+    if not args.no_anchor:
+        na = parse_n(args.anchor_n)
+        ra = P.mertens_exact(na, e2e_cfg)  # warm
+        aw = []
+        for _ in range(3):
+            barrier()
+            t0 = time.perf_counter()
+            ra = P.mertens_exact(na, e2e_cfg)
+            aw.append(time.perf_counter() - t0)
+        a_s = allmax(min(aw))
+        anchor = {"n": str(na), "M": ra.value, "M_ok": ANCHOR_M.get(na) in (None, ra.value), "u": ra.u,
+                  "wall_s": a_s, "value": ra.u / a_s, "unit": "y-values/s",
+                  "measured": "end to end through mertens_exact, best of 3"}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    # ---- roofline of the dominant kernel (largest summed event time)
-    pk = peaks()
-    dom = max(kms, key=lambda k: kms[k])
-    avg_ms = kms[dom] / max(1, kcnt[dom])
-    roof = {"kernel": dom}
-    nsm = torch.cuda.get_device_properties(local).multi_processor_count
-    # tail segment: MT_SEG_TILES_PER_SM (default 6) tiles of 2^17 cells per SM (mt_engine.cu)
-    seg = nsm * int(os.environ.get("MT_SEG_TILES_PER_SM", "6")) * (1 << 17)
-    if dom in ("sieve_tile", "sieve_large"):
-        # 10 algorithmic bytes per y-value (state write+read 2 B, M(y) 8 B);
-        # cells sieved per step = the head [0, head_end) + the tail segments
-        ys_per_launch = (stats_last["head_end"] + stats_last["n_tail_segments"] * seg) \
-            / max(1, kcnt[dom])
-        A = 10 * ys_per_launch / (avg_ms * 1e-3) / 1e9
-        P_ = pk.get("hbm_gbs", 6650.0)
-        tr = _ncu_traffic(dom)
-        roof |= {"bound": "hbm", "achieved": A, "peak": P_, "unit": "GB/s", "frac": A / P_,
-                 "traffic": tr, "per_unit": "10 B per y-value (SURVEY.md §8(d))",
-                 "units_per_launch": ys_per_launch, "avg_launch_ms": avg_ms,
-                 "timing": "CUDA events around every launch on the engine's stream, one instrumented "
-                           "step right after the timed region (events inside the timed steps cost ~4 %)",
-                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in pk else "fallback",
-                 "note": ("the sieve keeps its state in shared memory: measured DRAM traffic per launch (ncu, "
-                          "profiles/traffic.json; mostly the bucket lists) is ~1 B/y, far below the 10 B/y "
-                          "accounting, so frac compares the tile rate with an HBM-bound design; the kernel "
-                          "itself is bound by shared-memory reductions and issue (profiles/r01_final_ncu.txt)")}
-    else:
-        ops = 7 * stats_last["counted_items"] + 4 * stats_last["dense_items"]
-        A = ops / (kms[dom] * 1e-3) / 1e12
-        roof |= {"bound": "int", "achieved": A, "peak": 18.56, "unit": "Tops/s", "frac": A / 18.56,
-                 "traffic": None}
-    # the counted walk against its issue roofline: one exact division per squarefree m
-    # (6/pi^2 of the reference's counted pairs).  The k_counted inner loop walks two
-    # elements per list entry; its SASS is 76 instructions per 16 items (16 DFMA,
-    # 18 IMAD, 16 LEA.HI, 16 IADD3, 6 LDS.128, 4 loop), so at 4 warp-instructions
-    # per clock per SM the issue roofline is 128 / 4.75 = 26.9 items/clk/SM
-    upd_ms = kms.get("counted", 0.0)
-    upd = None
-    if upd_ms > 0:
-        items = 6 / 3.141592653589793 ** 2 * stats_last["counted_items"]
-        A = items / (upd_ms * 1e-3) / 1e12
-        ipc_items = 128.0 / (76.0 / 16.0)
-        Pk = ipc_items * nsm * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        upd = {"kernel": "counted", "bound": "issue", "achieved": A, "peak": Pk, "unit": "T items/s",
-               "frac": A / Pk, "per_unit": "one fp64-reciprocal exact division + 64-bit accumulate per squarefree m",
-               "reference_count_rate": stats_last["counted_items"] / (upd_ms * 1e-3),
-               "peak_source": "SASS of the k_counted joint loop: 4.75 instructions per item -> 26.9 items/clk/SM "
-                              "x SMs x sm_max_mhz (DESIGN.md §6)"}
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = cpu_reference_sample(n, u, os.cpu_count() or 1)
-        except Exception as ex:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": "y-values/s", "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"failed: {ex!r}"}
     line = {
         "metric": METRIC, "value": u / (ms * 1e-3), "unit": "y-values/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -387,30 +425,100 @@ def main():
         "data": f"synthetic: n={n} (deterministic, no dataset)", "config": config_block(n, u, world),
         "result": {"M": value_m, "paper": PAPER.get(n), "match": PAPER.get(n) in (None, value_m),
                    "e2e_M": r.value},
-        "roofline": roof, "roofline_update": upd,
+    }
+    line.update(_rooflines(stats_last, kms, kcnt, torch.cuda.get_device_properties(dev).multi_processor_count))
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(n, u, os.cpu_count() or 1)
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "y-values/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {ex!r}"}
+    line |= {
         "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": u / e2e_s, "unit": "y-values/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "wall_s": e2e_s},
-        "gpu_launches": launches // args.steps,
+        "anchor": anchor,
+        "gpu_launches": int(statistics.median(launches)) if launches else 0,
         "clocks": clocks,
+        "dist": {"backend": args.dist_backend if world > 1 else None, "world": world},
         "phases_ms": {k: stats_last[k] for k in ("ms_update_head", "ms_sieve_tail", "ms_qgather", "ms_finalize",
                                                   "ms_setup")},
-        "kernel_ms_per_step": {k: v for k, v in kms.items() if v},  # the instrumented step
+        "kernel_ms_per_step": {k: v for k, v in kms.items() if v},  # the instrumented step (rank 0)
         "work": {"counted_items": stats_last["counted_items"], "dense_items": stats_last["dense_items"],
-                 "head_end": stats_last["head_end"], "q_entries": stats_last["q_entries"]},
+                 "head_end": stats_last["head_end"], "q_entries": stats_last["q_entries"],
+                 "head_cells": stats_last["head_cells"], "tail_cells": stats_last["tail_cells"]},
     }
-    print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    print(json.dumps(line), flush=True)
 
 
-def _ncu_traffic(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu capture (profiles/), or None."""
-    p = os.path.join(ROOT, "profiles", "traffic.json")
-    try:
-        return json.load(open(p)).get(kernel)
-    except (OSError, ValueError):
-        return None
+def _rooflines(st, kms, kcnt, nsm):
+    """`roofline` of the dominant kernel plus the sieve and counted-walk rooflines.
+
+    sieve tile (k_sieve3): unit = one sieved cell (a y whose mu is computed: every
+      y of the head, the odd y of the tail -- the even y follow from mu(2z) =
+      -mu(z)); algorithmic bytes = SURVEY.md §8(d)'s 10 B per sieved value (state
+      write + read 2 B, M(y) 8 B) against the measured HBM copy bandwidth.  The
+      kernel keeps state and prefix on chip, so the ncu DRAM traffic per launch
+      (profiles/ncu_metrics.json) is far below that accounting and ncu's
+      issue-active is reported beside it.
+    counted walk (k_counted): unit = one squarefree m of an element's counted
+      range (6/pi^2 of the reference's counted pairs); the implemented
+      algorithm needs one fp64-reciprocal DFMA, one IMAD (remainder) and two
+      ALU adds (quotient, sign-correction) per unit = 4 issue slots, against the
+      measured 4 warp-instructions/clk/SM issue rate -> 32 units/clk/SM."""
+    pk = peaks()
+    nm = ncu_metrics()
+    mhz = pk.get("sm_max_mhz", 1965.0)
+    out = {}
+    cells = st["head_cells"] + st["tail_cells"]
+    tile_ms = kms.get("sieve_tile", 0.0)
+    roof_s = None
+    if tile_ms > 0:
+        n_l = max(1, kcnt.get("sieve_tile", 1))
+        avg = tile_ms / n_l
+        A = 10 * (cells / n_l) / (avg * 1e-3) / 1e9
+        P_ = pk.get("hbm_gbs", 6650.0)
+        m = nm.get("k_sieve3", {})
+        roof_s = {"kernel": "sieve_tile", "bound": "hbm", "achieved": A, "peak": P_, "unit": "GB/s", "frac": A / P_,
+                  "traffic": m.get("dram_bytes_per_launch"),
+                  "per_unit": "10 B per sieved value (SURVEY.md §8(d)); tail cells are odd y only",
+                  "units_per_launch": cells / n_l, "avg_launch_ms": avg, "launches": n_l,
+                  "y_covered_per_launch": (st["head_cells"] + 2 * st["tail_cells"]) / n_l,
+                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in pk else "fallback",
+                  "ncu": {k: m.get(k) for k in ("issue_active", "warps_active", "dram_bytes_per_launch",
+                                                "shared_bank_conflicts", "source")} if m else None,
+                  "timing": "CUDA events around every launch on the engine's stream, one instrumented step "
+                            "right after the timed region (events inside the timed steps cost ~4 %)",
+                  "note": "state and prefix stay in shared memory: the kernel is bound by shared-memory "
+                          "reductions and issue (ncu issue_active), not DRAM; frac compares its cell rate "
+                          "with an HBM-bound design of the same algorithmic bytes"}
+    roof_u = None
+    upd_ms = kms.get("counted", 0.0)
+    if upd_ms > 0:
+        items = 6 / 3.141592653589793 ** 2 * st["counted_items"]
+        A = items / (upd_ms * 1e-3) / 1e12
+        Pk = 32.0 * nsm * mhz * 1e6 / 1e12
+        m = nm.get("k_counted", {})
+        roof_u = {"kernel": "counted", "bound": "issue", "achieved": A, "peak": Pk, "unit": "T items/s",
+                  "frac": A / Pk,
+                  "per_unit": "one squarefree m: DFMA (fp64 reciprocal quotient) + IMAD (remainder) + 2 ALU "
+                              "(accumulate, correction) = 4 issue slots",
+                  "peak_source": "4 warp-instructions/clk/SM x 32 lanes / 4 slots x SMs x sm_max_mhz; the "
+                                 "FP64 and IMAD pipes alone allow 63.8 units/clk/SM (profiles/r01_microbench.txt)",
+                  "reference_count_rate": st["counted_items"] / (upd_ms * 1e-3),
+                  "ncu": {k: m.get(k) for k in ("issue_active", "warps_active", "pipe_alu", "pipe_fma",
+                                                "pipe_fp64", "source")} if m else None}
+    dom = max(kms, key=lambda k: kms[k]) if kms else None
+    if dom == "counted" and roof_u:
+        out["roofline"] = roof_u
+    elif roof_s:
+        out["roofline"] = roof_s | ({"dominant": dom} if dom != "sieve_tile" else {})
+    out["roofline_sieve"] = roof_s
+    out["roofline_update"] = roof_u
+    return out
 
 
 class _SinglePlan:

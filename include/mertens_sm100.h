@@ -94,11 +94,17 @@ int mt_mertens_at(const uint64_t* pts, uint64_t npts, int64_t* m_out);
  * mu_out and, if m_out is non-null, M(y) into m_out (either may be null) */
 int mt_sieve_fast(uint64_t y1, uint64_t y2, int8_t* mu_out, int64_t* m_out);
 
+/* the production sieve in odd-cell (tail) mode, the one the engine runs above
+ * the head: mu of the odd y of [y1, y2] (y1 >= 2^18) into mu_out[(y - y0)/2],
+ * y0 = the first odd y >= y1 */
+int mt_sieve_odd(uint64_t y1, uint64_t y2, int8_t* mu_out);
+
 /* profiling entry (tools/sieve_bench.py): the production sieve in tail mode
- * over nseg default-size segments from Y0 (a multiple of 2^17) with the primes
- * of y_last; summed CUDA-event ms per kernel class into ms_out[7]
- * (sieve_tile, bucket_fill, -, -, -, -, scan+fixup) */
-int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, double* ms_out);
+ * over nseg segments of 6 tiles per SM from Y0 (a multiple of the tile's y-span:
+ * 2^17, or 2^18 with odd = 1) with the primes of y_last; summed CUDA-event ms
+ * per kernel class into ms_out[7] (sieve_tile, bucket_fill, -, -, -, -, finish) */
+int mt_sieve_bench2(uint64_t Y0, uint64_t nseg, uint64_t y_last, int odd, double* ms_out);
+int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, double* ms_out); /* odd = 0 */
 
 /* ---- 2. job-level production entry ----------------------------------------- */
 
@@ -120,8 +126,9 @@ typedef struct {
                               2^17 cells per SM, MT_SEG_TILES_PER_SM overrides)    */
   int32_t device;          /* CUDA device ordinal (-1: current)                    */
   /* multi-GPU sharding: rank r of w sieves the head redundantly,
-   * takes every w-th work unit of the head update and of the Q-gather, and
-   * sieves the r-th contiguous share of the tail y-segments.  w <= 1: all. */
+   * takes every w-th work unit of the head update and of the head part of the
+   * Q-gather, and owns the r-th of w tail ranges balanced by sieve work (odd y of
+   * [ya/2, yb/2) U [ya, yb)).  w <= 1: all. */
   uint32_t shard_rank, shard_world;
   uint32_t flags;          /* MT_FLAG_*                                          */
   void* stream;            /* cudaStream_t to run on (null: the engine's own)    */
@@ -144,8 +151,10 @@ typedef struct {
    * other): summed CUDA-event ms and launch counts (MT_FLAG_TIMING) */
   double kernel_ms[8];
   uint64_t kernel_count[8];
-  uint64_t tail_seg_begin, tail_seg_end; /* this rank's tail segments     */
+  uint64_t tail_seg_begin, tail_seg_end; /* this rank's tail range [ya, yb) (y values) */
   double ms_setup;                        /* mt_plan_create wall time      */
+  uint64_t head_cells, tail_cells;        /* sieve cells of this execution: head (all y
+                                             below head_end), tail (odd y only)          */
 } mt_stats;
 
 typedef struct {
@@ -161,16 +170,21 @@ typedef struct {
 /* one exact job: sieve 1..u, update every element, resolve (shard_world <= 1) */
 int mt_run(const mt_job* job, mt_result* out);
 
-/* ---- 3. plan API: the same job split at its two exchange points ---------------
+/* ---- 3. plan API: the same job split at its exchange points --------------------
  * mt_run == create, sieve_update, tail_offset(m_head), gather, resolve, destroy.
  * With shard_world = w > 1 every rank runs the phases and the caller performs
  * the collectives between them (paper_1108_0135_b200/distributed.py):
  *   after sieve_update : allgather tail_total -> offset_r = m_head + sum_{h<r} T_h
- *   after tail_offset  : for every target t and rank h, broadcast the Q slice
- *                        mt_plan_q_slice(t, h) from rank h (device int32)
+ *   after tail_offset  : (only when quotient captures are requested) sum-reduce
+ *                        mt_plan_cap_window (device int32; each rank holds its
+ *                        own entries and zeros elsewhere)
  *   after gather       : allreduce(sum, int64 two's complement) of mt_plan_acc
- * A plan is re-executable (sieve_update re-initialises the accumulators), and
- * all device memory of the job lives in the plan. */
+ * Rank r owns the tail range [ya_r, yb_r) (mt_stats.tail_seg_begin/end) and the
+ * quotient-table slice mt_plan_q_slice(t, r) whose quotients fall in it; the
+ * Q-gather of rank r reads only that slice and the replicated head part, so no
+ * rank needs another rank's slice.  A plan is re-executable (sieve_update
+ * re-initialises the accumulators), and all device memory of the job lives in
+ * the plan. */
 typedef struct mt_plan mt_plan;
 int mt_plan_create(const mt_job* job, mt_plan** out);
 int mt_plan_sieve_update(mt_plan* p, int64_t* m_head, int64_t* tail_total);
@@ -179,14 +193,19 @@ int mt_plan_sieve_update(mt_plan* p, int64_t* m_head, int64_t* tail_total);
  * complete, and then m_head / tail_total are written as by sieve_update */
 int mt_plan_sieve_step(mt_plan* p, uint64_t max_tail_segments, int* done, int64_t* m_head,
                        int64_t* tail_total);
-/* checkpoint / resume of a single-target, single-rank plan between sieve steps:
- * the reference's MERTCKP1 header (engine.py:646-680; version 2 = this engine)
- * followed by the accumulators, M(mcut), the quotient table, the small
- * captures and the running prefix.  Written to path.tmp, then renamed. */
+/* checkpoint / resume of a single-target plan between sieve steps (one file per
+ * rank): the reference's MERTCKP1 header (engine.py:646-680; version 3 = this
+ * engine, flags = rank | world << 16) followed by the accumulators, M(mcut), the
+ * quotient table, the tail-slice P2 table, the small captures and the running
+ * prefixes.  Written to path.tmp, flushed, fsync'ed, then renamed; a failed write
+ * removes path.tmp and leaves the previous checkpoint in place. */
 int mt_plan_checkpoint(mt_plan* p, const char* path);
 int mt_plan_restore(mt_plan* p, const char* path);
 int mt_plan_tail_offset(mt_plan* p, int64_t offset);
 int mt_plan_q_slice(mt_plan* p, uint32_t target, uint32_t rank, void** dptr, uint64_t* count);
+/* target 0's quotient-capture window (M(floor(n0/c)), c in [cap_c_lo, cap_c_hi]) as
+ * device int32; count = 0 when no capture was requested */
+int mt_plan_cap_window(mt_plan* p, void** dptr, uint64_t* count);
 int mt_plan_acc(mt_plan* p, void** dptr, uint64_t* count);
 int mt_plan_gather(mt_plan* p);
 /* finalize every target; copies into the non-null host pointers of out */

@@ -59,7 +59,8 @@ class MtStats(ctypes.Structure):
             "ms_finalize", "ms_counted_kernel", "ms_dense_kernel")] + [
         ("m_head", ctypes.c_int64), ("tail_total", ctypes.c_int64),
         ("kernel_ms", ctypes.c_double * 8), ("kernel_count", _u64 * 8),
-        ("tail_seg_begin", _u64), ("tail_seg_end", _u64), ("ms_setup", ctypes.c_double)]
+        ("tail_seg_begin", _u64), ("tail_seg_end", _u64), ("ms_setup", ctypes.c_double),
+        ("head_cells", _u64), ("tail_cells", _u64)]
 
 
 class MtResult(ctypes.Structure):
@@ -100,6 +101,8 @@ def lib():
         "mt_mertens_at": [vp, _u64, vp],
         "mt_sieve_fast": [_u64, _u64, vp, vp],
         "mt_sieve_bench": [_u64, _u64, _u64, vp],
+        "mt_sieve_bench2": [_u64, _u64, _u64, ctypes.c_int, vp],
+        "mt_sieve_odd": [_u64, _u64, vp],
         "mt_run": [ctypes.POINTER(MtJob), ctypes.POINTER(MtResult)],
         "mt_plan_create": [ctypes.POINTER(MtJob), ctypes.POINTER(ctypes.c_void_p)],
         "mt_plan_sieve_update": [vp, _pi64, _pi64],
@@ -109,6 +112,7 @@ def lib():
         "mt_plan_tail_offset": [vp, ctypes.c_int64],
         "mt_plan_q_slice": [vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(ctypes.c_void_p), _pu64],
         "mt_plan_acc": [vp, ctypes.POINTER(ctypes.c_void_p), _pu64],
+        "mt_plan_cap_window": [vp, ctypes.POINTER(ctypes.c_void_p), _pu64],
         "mt_plan_gather": [vp],
         "mt_plan_resolve": [vp, ctypes.POINTER(MtResult)],
     }
@@ -154,9 +158,10 @@ def ptr(a: np.ndarray):
 EXPORTED_SYMBOLS = (
     "mt_last_error", "mt_abi_version", "mt_device_count", "mt_set_device",
     "mt_sieve_logprime", "mt_logprime_states", "mt_sieve_naive", "mt_apply_block",
-    "mt_finalize", "mt_build_divisor_arrays", "mt_mertens_range", "mt_mertens_at", "mt_sieve_fast", "mt_sieve_bench", "mt_run",
+    "mt_finalize", "mt_build_divisor_arrays", "mt_mertens_range", "mt_mertens_at", "mt_sieve_fast", "mt_sieve_odd", "mt_sieve_bench",
+    "mt_sieve_bench2", "mt_run",
     "mt_plan_create", "mt_plan_sieve_update", "mt_plan_sieve_step", "mt_plan_checkpoint", "mt_plan_restore",
-    "mt_plan_tail_offset", "mt_plan_q_slice", "mt_plan_acc",
+    "mt_plan_tail_offset", "mt_plan_q_slice", "mt_plan_cap_window", "mt_plan_acc",
     "mt_plan_gather", "mt_plan_resolve", "mt_plan_destroy",
 )
 

@@ -22,6 +22,8 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include <cub/cub.cuh>
 
 #include "mt_common.cuh"
@@ -347,16 +349,44 @@ extern "C" int mt_sieve_fast(uint64_t y1, uint64_t y2, int8_t* mu_out, int64_t* 
   return MT_OK;
 }
 
+// the production sieve in odd-cell (tail) mode over the odd y of [y1, y2]
+// (y1 >= 2^18): mu_out[i] = mu(y0 + 2i), y0 = the first odd y >= y1
+extern "C" int mt_sieve_odd(uint64_t y1, uint64_t y2, int8_t* mu_out) {
+  const u64 SPAN = 2ull * MT_S2_TILE, NT = 256, RY = SPAN * NT;
+  if (y2 < y1 || y1 < SPAN) { mt_set_error("bad range (odd-cell sieve needs y1 >= 2^18)"); return MT_ERR_VALUE; }
+  u64 Y0 = (y1 / SPAN) * SPAN;
+  const u64 y0 = y1 | 1;
+  if (y0 > y2) return MT_OK;
+  const u64 y_last = ((y2 - Y0) / RY + 1) * RY + Y0 - 1;
+  Sieve2Host* h = nullptr;
+  struct G { Sieve2Host*& h; ~G() { mt_sieve2_destroy(h); } } g{h};
+  RC(mt_sieve2_create(&h, y_last, (uint32_t)NT, 0));
+  DevBuf d_mu, d_run;
+  RC(dalloc(d_mu, NT * MT_S2_TILE)); RC(dalloc(d_run, 8));
+  MT_CUDA_CHECK(cudaMemset(d_run.p, 0, 8));
+  for (; Y0 <= y2; Y0 += RY) {
+    RC(mt_sieve2_run(h, Y0, (uint32_t)NT, d_run.as<int64_t>(), d_mu.as<int8_t>(), nullptr, nullptr, nullptr,
+                     nullptr, 0, 0, nullptr, true));
+    const u64 ya = std::max(Y0 + 1, y0), yb = std::min(Y0 + RY - 1, y2);  // odd y of this segment
+    if (yb < ya) continue;
+    const u64 ca = (ya - Y0 - 1) / 2, cb = (yb - Y0 - 1) / 2;
+    MT_CUDA_CHECK(cudaMemcpy(mu_out + (ya - y0) / 2, d_mu.as<int8_t>() + ca, cb - ca + 1, cudaMemcpyDeviceToHost));
+  }
+  MT_CUDA_CHECK(cudaDeviceSynchronize());
+  return MT_OK;
+}
+
 // profiling entry: the production sieve in tail mode (sums only, no outputs)
 // over nseg segments of the default size from Y0 (multiple of 2^17), with
 // primes for y_last; per-kernel-class CUDA-event ms into ms_out[KT_NCLASS]
-extern "C" int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, double* ms_out) {
-  if (Y0 % MT_S2_TILE) { mt_set_error("Y0 must be a multiple of 2^17"); return MT_ERR_VALUE; }
+extern "C" int mt_sieve_bench2(uint64_t Y0, uint64_t nseg, uint64_t y_last, int odd, double* ms_out) {
+  const u64 span = odd ? 2ull * MT_S2_TILE : MT_S2_TILE;
+  if (Y0 % span || (odd && Y0 == 0)) { mt_set_error("Y0 must be a positive multiple of the tile span"); return MT_ERR_VALUE; }
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const uint32_t NT = (uint32_t)nsm * 4;
-  const u64 R = (u64)NT * MT_S2_TILE;
+  const uint32_t NT = (uint32_t)nsm * 6;
+  const u64 R = (u64)NT * span;
   if (y_last < Y0 + nseg * R) y_last = Y0 + nseg * R;
   Sieve2Host* h = nullptr;
   struct G { Sieve2Host*& h; ~G() { mt_sieve2_destroy(h); } } g{h};
@@ -367,11 +397,16 @@ extern "C" int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, doubl
   KTimer kt;
   kt.init(true);
   for (u64 s = 0; s < nseg; s++)
-    RC(mt_sieve2_run(h, Y0 + s * R, NT, d_run.as<int64_t>(), nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, &kt));
+    RC(mt_sieve2_run(h, Y0 + s * R, NT, d_run.as<int64_t>(), nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, &kt,
+                     odd != 0));
   MT_CUDA_CHECK(cudaDeviceSynchronize());
   kt.drain();
   for (int c = 0; c < KT_NCLASS; c++) ms_out[c] = kt.ms[c];
   return MT_OK;
+}
+
+extern "C" int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, double* ms_out) {
+  return mt_sieve_bench2(Y0, nseg, y_last, 0, ms_out);
 }
 
 // ============================================================================
@@ -601,15 +636,97 @@ __global__ void k_copy_caps(const int* __restrict__ Q, u64 jq0, u64 c_lo, u64 cn
   out[i] = Q[c_lo + i - jq0];
 }
 
-
-// Q[j] += off for j in [j0, j1] (one target's slice owned by this rank's tail)
-__global__ void k_q_offset(int* __restrict__ Q, u64 cnt, int off) {
+// Q[j] = Q[j] - P2[j] + delta over one target's own tail slice: the odd-cell
+// prefix P at floor(n/j) minus P at floor(n/(2j)) is M(floor(n/j)) - M(ya - 1)
+// up to the constant P(ya - 1) folded into delta
+__global__ void k_q_combine(int* __restrict__ Q, const int* __restrict__ P2, u64 cnt, int delta) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < cnt) Q[i] += off;
+  if (i < cnt) Q[i] = Q[i] - P2[i] + delta;
+}
+
+// multi-rank output assembly: zero the capture-window entries this rank does
+// not own (own tail slice [s0, s1]; the head part j >= jh belongs to rank 0)
+__global__ void k_cap_mask(int* __restrict__ Q, u64 jq0, u64 c0, u64 c1, u64 s0, u64 s1, u64 jh, int head_mine) {
+  const u64 j = c0 + (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > c1) return;
+  const bool mine = (j >= s0 && j <= s1) || (head_mine && j >= jh);
+  if (!mine) Q[j - jq0] = 0;
 }
 
 static double ms_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ============================================================================
+// the tail split
+// ============================================================================
+// M(x) = O(x) - O(floor(x/2)) with O the sum of mu over ODD y <= x (mu(2z) =
+// -mu(z) for odd z, mu = 0 on multiples of 4).  A rank owning the tail range
+// [a, b) therefore sieves only odd y, over [a/2, b/2) U [a, b), with one running
+// prefix P (P(a/2 - 1) = 0): for x in [a, b),
+//   M(x) - M(a - 1) = P(x) - P(floor(x/2)) - P(a - 1).
+// Boundaries are multiples of TAIL_ALIGN so that a/2 is a multiple of the odd
+// tile's y-span (2^18).
+#define TAIL_ALIGN (1ull << 19)
+#define TILE_Y_ODD (2ull * MT_S2_TILE)
+
+// y-values a rank owning [a, b) covers: |[a/2, b/2) U [a, b)| (odd cells = half of it)
+static u64 tail_cost(u64 a, u64 b) {
+  if (b <= a) return 0;
+  const u64 h0 = a / 2, h1 = b / 2;
+  u64 c = (b - a) + (h1 - h0);
+  if (h1 > a) c -= h1 - a;
+  return c;
+}
+
+// boundaries H = y[0] < ... <= y[w] = E on TAIL_ALIGN, balancing tail_cost
+static std::vector<u64> tail_partition(u64 H, u64 E, uint32_t w) {
+  std::vector<u64> yb(w + 1, E);
+  yb[0] = H;
+  if (w <= 1 || E <= H) return yb;
+  auto cover = [&](u64 c, std::vector<u64>* out) -> bool {
+    u64 a = H;
+    for (uint32_t r = 0; r + 1 < w; r++) {
+      u64 lo = 0, hi = (E - a) / TAIL_ALIGN;  // largest step with cost <= c
+      while (lo < hi) {
+        const u64 mid = (lo + hi + 1) / 2;
+        if (tail_cost(a, a + mid * TAIL_ALIGN) <= c) lo = mid; else hi = mid - 1;
+      }
+      a += lo * TAIL_ALIGN;
+      if (out) (*out)[r + 1] = a;
+    }
+    return tail_cost(a, E) <= c;
+  };
+  u64 lo = 0, hi = tail_cost(H, E);
+  while (lo < hi) {
+    const u64 mid = lo + (hi - lo) / 2;
+    if (cover(mid, nullptr)) hi = mid; else lo = mid + 1;
+  }
+  cover(lo, &yb);
+  yb[w] = E;
+  return yb;
+}
+
+struct TailSeg { u64 Y0; uint32_t ntiles; };
+
+// this rank's odd-cell segments over [a/2, b/2) U [a, b), cut at a and b/2;
+// snap_a / snap_h = number of segments ending at or before a / b/2
+static void tail_segments(u64 a, u64 b, u64 seg_y, std::vector<TailSeg>& out, size_t& snap_a, size_t& snap_h) {
+  out.clear();
+  snap_a = snap_h = 0;
+  if (b <= a) return;
+  const u64 h0 = a / 2, h1 = b / 2;
+  std::vector<std::pair<u64, u64>> iv;
+  if (h1 > a) iv = {{h0, a}, {a, h1}, {h1, b}};
+  else iv = {{h0, h1}, {a, b}};
+  for (auto& x : iv)
+    for (u64 s = x.first; s < x.second; s += seg_y)
+      out.push_back({s, (uint32_t)((std::min(x.second, s + seg_y) - s) / TILE_Y_ODD)});
+  for (auto& s : out) {
+    const u64 e = s.Y0 + (u64)s.ntiles * TILE_Y_ODD;
+    if (e <= a) snap_a++;
+    if (e <= h1) snap_h++;
+  }
 }
 
 // ============================================================================
@@ -626,28 +743,36 @@ struct mt_plan {
   u64 NE = 0;
   cudaStream_t st = nullptr;
   bool own_stream = false;
-  u64 launches = 0;
+  u64 launches = 0;  // kernels of the current execution (reset by the head step)
   u64 counted_items = 0, dense_items = 0, Ymc = 0;
   // elements
   DevBuf d_nlo, d_nhi, d_e0, d_vd, d_vlo, d_vhi, d_vb, d_k, d_tgt, d_D, d_x, d_mc, d_lo, d_low, d_dq,
       d_acc, d_mmc, d_dsp, d_J, d_gs, d_gylo, d_gyhi, d_gw, d_tmax, d_tbits, d_fin;
   std::vector<u64> gstart;
   u64 ng = 0, ntiles = 0;
-  // quotient tables
+  // quotient tables Q_t[j - jq0] = M(floor(n_t/j)), j in [jq0, jq1]
   std::vector<u64> J, jq0, jq1;
   std::vector<DevBuf> d_Q;
   std::vector<TargetDev> tdev;
-  std::vector<CaptureTargetH> caps;
+  std::vector<CaptureTargetH> caps_head, caps_tail;
+  // own tail slice per target (j with floor(n/j) in [ya, yb); empty: sj0 > sj1)
+  // and P2[j - sj0] = P(floor(n/(2j))) for it
+  std::vector<u64> sj0, sj1;
+  std::vector<DevBuf> d_P2;
   // segments
-  u64 Rh = 0, Rt = 0, head_end = 0, head_segs = 0, head_lim = 0, tail_segs = 0, y_last = 0;
-  u64 tseg0 = 0, tseg1 = 0;  // this rank's tail segments [tseg0, tseg1)
+  u64 Rh = 0, head_end = 0, head_segs = 0, head_lim = 0, y_last = 0;
+  u64 tail_end = 0, seg_y = 0;       // tail = [head_lim, tail_end); odd segments span <= seg_y
+  std::vector<u64> ybound;           // rank r owns [ybound[r], ybound[r+1])
+  u64 ya = 0, yb = 0;
+  std::vector<TailSeg> tsegs;
+  size_t snap_a = 0, snap_h = 0;
   Sieve2Host* sv = nullptr;
-  DevBuf d_mu, d_m, d_bk, d_run, d_caps, d_small;
+  DevBuf d_mu, d_m, d_bk, d_run, d_snap, d_caps_head, d_caps_tail, d_small;
   u64 cap_c_lo = 1, cap_c_hi = 0, cap_small = 0, nsmall = 0;
   bool cap32 = false;  // MT_FLAG_CAP32: int32 capture outputs (the dense full quotient map)
   UpdateCtx* uc = nullptr;
   KTimer kt;
-  int64_t m_head = 0, tail_total = 0;
+  int64_t m_head = 0, tail_total = 0, s_a = 0, s_h = 0, p_end = 0;
   double ms_setup = 0, ms_head = 0, ms_tail = 0, ms_gather = 0, ms_fin = 0;
   cudaEvent_t ev[6] = {};
   int phase = 0;  // 1 after sieve_update, 2 after tail_offset, 3 after gather
@@ -661,24 +786,38 @@ struct mt_plan {
     kt.drain();
     if (own_stream && st) cudaStreamDestroy(st);
   }
-  // y of the first cell of tail segment s
-  u64 tail_y0(u64 s) const { return head_lim + s * Rt; }
-  // Q slice [j0, j1] of target t whose quotients fall in rank r's tail (empty: j0 > j1)
+  // Q slice [j0, j1] of target t whose quotients fall in rank r's tail range (empty: j0 > j1)
   void q_slice(int t, uint32_t r, u64& j0, u64& j1) const {
-    u64 s0 = tail_segs * r / world, s1 = tail_segs * (r + 1) / world;
     j0 = 1; j1 = 0;
-    if (s0 >= s1 || jq1[t] < jq0[t]) return;
-    const u64 ya = tail_y0(s0), yb = tail_y0(s1) - 1;  // y in [ya, yb]
-    // floor(n/j) in [ya, yb]  <=>  j in [floor(n/(yb+1)) + 1, floor(n/ya)]
-    u128 lo = n[t] / ((u128)yb + 1) + 1, hi = n[t] / (u128)ya;
+    const u64 a = ybound[r], b = ybound[r + 1];
+    if (a >= b || jq1[t] < jq0[t]) return;
+    // floor(n/j) in [a, b)  <=>  j in [floor(n/b) + 1, floor(n/a)]
+    u128 lo = n[t] / (u128)b + 1, hi = n[t] / (u128)a;
     if (lo < jq0[t]) lo = jq0[t];
     if (hi > jq1[t]) hi = jq1[t];
     if (lo > hi) return;
     j0 = (u64)lo; j1 = (u64)hi;
   }
+  // first j of target t whose quotient lies in the head (y < head_lim)
+  u64 head_j(int t) const { return (u64)(n[t] / (u128)head_lim) + 1; }
+  u64 tail_cells() const {
+    u64 c = 0;
+    for (auto& s : tsegs) c += (u64)s.ntiles * MT_S2_TILE;
+    return c;
+  }
 };
 
 #define PLAN_DEV(p) do { if ((p)->device >= 0) MT_CUDA_CHECK(cudaSetDevice((p)->device)); } while (0)
+
+static CaptureTargetH make_cap(u128 n, u64 j0, u64 j1, int* Q) {
+  CaptureTargetH c;
+  c.n_lo = (u64)n; c.n_hi = (u64)(n >> 64);
+  c.nd = c.n_hi ? (double)c.n_hi * 18446744073709551616.0 + (double)c.n_lo : (double)c.n_lo;
+  c.nbits = 0;
+  for (u128 x = n; x; x >>= 1) c.nbits++;
+  c.jq0 = j0; c.jq1 = j1; c.Q = Q;
+  return c;
+}
 
 static int plan_setup(mt_plan* P, const mt_job* job) {
   auto T0 = std::chrono::steady_clock::now();
@@ -725,7 +864,6 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
                    P->d_vd.as<double>(), P->d_vlo.as<u64>(), P->d_vhi.as<u64>(), P->d_vb.as<uint8_t>(), P->d_k.as<u64>(),
                    P->d_tgt.as<uint32_t>(), P->d_D.as<u64>(), P->d_x.as<u64>(), P->d_mc.as<u64>(), P->d_lo.as<u64>()};
     if (NE) k_elem_init<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(a);
-    P->launches++;
     MT_CUDA_CHECK(cudaGetLastError());
   }
   std::vector<unsigned long long> tstat(3 * N, 0);
@@ -734,7 +872,6 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
     RC(dalloc(d_ts, 3 * N * 8));
     MT_CUDA_CHECK(cudaMemsetAsync(d_ts.p, 0, 3 * N * 8, st));
     if (NE) k_elem_stats<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, P->d_tgt.as<uint32_t>(), P->d_mc.as<u64>(), P->d_x.as<u64>(), P->d_lo.as<u64>(), d_ts.as<unsigned long long>());
-    P->launches++;
     MT_CUDA_CHECK(cudaMemcpyAsync(tstat.data(), d_ts.p, 3 * N * 8, cudaMemcpyDeviceToHost, st));
     MT_CUDA_CHECK(cudaStreamSynchronize(st));
   }
@@ -744,8 +881,10 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
     P->dense_items += tstat[3 * i + 2];
   }
 
-  // ---- quotient tables: Q_t[j] = M(floor(n_t/j)), j in [jq0_t, jq1_t]
-  const u64 q_budget = job->q_budget_bytes ? job->q_budget_bytes : (48ull << 30);
+  // ---- quotient tables: Q_t[j] = M(floor(n_t/j)), j in [jq0_t, jq1_t]; the tail
+  // part also needs P2 (odd-prefix captures at floor(n/(2j))), so a table entry
+  // is budgeted at 8 bytes
+  const u64 q_budget = job->q_budget_bytes ? job->q_budget_bytes : (96ull << 30);
   P->J.assign(N, 0); P->jq0.assign(N, 0); P->jq1.assign(N, 0);
   P->cap_c_lo = job->cap_c_lo; P->cap_c_hi = job->cap_c_hi;
   for (int i = 0; i < N; i++) {
@@ -760,7 +899,7 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
       P->jq1[i] = hi;
       if (hi >= P->jq0[i]) q_total += (hi - P->jq0[i] + 1);
     }
-    if (q_total * 4 <= q_budget) break;
+    if (q_total * 8 <= q_budget) break;
     for (int i = 0; i < N; i++) P->J[i] = P->J[i] / 2;
   }
   for (int i = 0; i < N; i++)
@@ -774,21 +913,14 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
     RC(dalloc(P->d_Q[i], cnt * 4));
     P->tdev[i].Q = P->d_Q[i].as<int>();
     P->tdev[i].jq0 = P->jq0[i];
-    if (cnt) {
-      CaptureTargetH c;
-      c.n_lo = job->n_lo[i]; c.n_hi = job->n_hi[i];
-      c.nd = job->n_hi[i] ? (double)job->n_hi[i] * 18446744073709551616.0 + (double)job->n_lo[i] : (double)job->n_lo[i];
-      c.nbits = 0;
-      for (u128 x = P->n[i]; x; x >>= 1) c.nbits++;
-      c.jq0 = P->jq0[i]; c.jq1 = P->jq1[i]; c.Q = P->tdev[i].Q;
-      P->caps.push_back(c);
-    }
+    P->tdev[i].wlo = 0;
+    P->tdev[i].whi = cnt;
+    if (cnt) P->caps_head.push_back(make_cap(P->n[i], P->jq0[i], P->jq1[i], P->tdev[i].Q));
   }
   RC(dalloc(P->d_J, N * 8));
   MT_CUDA_CHECK(cudaMemcpyAsync(P->d_J.p, P->J.data(), N * 8, cudaMemcpyHostToDevice, st));
   if (NE) k_elem_split<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, P->d_k.as<u64>(), P->d_tgt.as<uint32_t>(), P->d_J.as<u64>(), P->d_lo.as<u64>(), P->d_x.as<u64>(), P->d_low.as<u64>(), P->d_dq.as<u64>());
   if (NE) k_elem_dsp<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, P->d_vd.as<double>(), P->d_dsp.as<u64>());
-  P->launches += 2;
   // element groups for the window walk: consecutive k of one target, size ~clamp(k/8, 32, 1024)
   for (int i = 0; i < N; i++) {
     u64 k0 = 1;
@@ -806,7 +938,6 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   RC(dalloc(P->d_gs, (ng + 1) * 8)); RC(dalloc(P->d_gylo, ng * 8)); RC(dalloc(P->d_gyhi, ng * 8)); RC(dalloc(P->d_gw, ng));
   MT_CUDA_CHECK(cudaMemcpyAsync(P->d_gs.p, P->gstart.data(), (ng + 1) * 8, cudaMemcpyHostToDevice, st));
   if (ng) k_group_meta<<<(unsigned)ng, 256, 0, st>>>(P->d_gs.as<u64>(), ng, P->d_vlo.as<u64>(), P->d_vhi.as<u64>(), P->d_x.as<u64>(), P->d_low.as<u64>(), P->d_dsp.as<u64>(), P->d_gylo.as<u64>(), P->d_gyhi.as<u64>(), P->d_gw.as<uint8_t>());
-  P->launches++;
   GroupDev grp{P->d_gs.as<u64>(), P->d_gylo.as<u64>(), P->d_gyhi.as<u64>(), P->d_gw.as<uint8_t>(), ng};
   u64 head_end = P->Ymc;
   {
@@ -814,7 +945,6 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
     RC(dalloc(d_we, 8));
     MT_CUDA_CHECK(cudaMemsetAsync(d_we.p, 0, 8, st));
     if (NE) k_window_extent<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, P->d_vlo.as<u64>(), P->d_vhi.as<u64>(), P->d_low.as<u64>(), P->d_x.as<u64>(), d_we.as<unsigned long long>());
-    P->launches++;
     unsigned long long we = 0;
     MT_CUDA_CHECK(cudaMemcpyAsync(&we, d_we.p, 8, cudaMemcpyDeviceToHost, st));
     MT_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -829,7 +959,6 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   const u64 ntiles = P->ntiles = (NE + MT_CT - 1) / MT_CT;
   RC(dalloc(P->d_tmax, ntiles * 8)); RC(dalloc(P->d_tbits, ntiles));
   if (ntiles) k_tile_meta<<<(unsigned)ntiles, MT_CT, 0, st>>>(NE, P->d_mc.as<u64>(), P->d_vb.as<uint8_t>(), P->d_tmax.as<u64>(), P->d_tbits.as<uint8_t>());
-  P->launches++;
 
   // ---- segments (production sieve tiles of 2^17 cells)
   // default tail segment = 6 tiles per SM (the persistent sieve CTAs each take 6
@@ -843,25 +972,51 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   if (const char* e = getenv("MT_SEG_TILES_PER_SM")) tiles_per_sm = strtoull(e, nullptr, 10);
   if (const char* e = getenv("MT_SEG_TILES_PER_SM_HEAD")) tiles_per_sm_head = strtoull(e, nullptr, 10);
   P->Rh = job->seg_log2_head ? 1ull << job->seg_log2_head : (u64)nsm * tiles_per_sm_head * MT_S2_TILE;
-  P->Rt = job->seg_log2_tail ? 1ull << job->seg_log2_tail : (u64)nsm * tiles_per_sm * MT_S2_TILE;
-  const u64 Rh = P->Rh, Rt = P->Rt;
-  if (Rh < MT_S2_TILE || Rt < MT_S2_TILE || (Rh % MT_S2_TILE) || (Rt % MT_S2_TILE) || Rt > (1ull << 31) || Rh > (1ull << 31)) {
+  // tail segments: tiles of 2^17 odd cells, 2^18 y each
+  const u64 tail_tiles = job->seg_log2_tail ? 1ull << (job->seg_log2_tail - 17) : (u64)nsm * tiles_per_sm;
+  const u64 Rh = P->Rh;
+  if (Rh < MT_S2_TILE || (Rh % MT_S2_TILE) || Rh > (1ull << 31) || (job->seg_log2_tail && job->seg_log2_tail < 17) ||
+      tail_tiles == 0 || tail_tiles * MT_S2_TILE > (1ull << 31)) {
     mt_set_error("bad segment sizes");
     return MT_ERR_VALUE;
   }
+  P->seg_y = tail_tiles * TILE_Y_ODD;
   P->head_segs = (head_end + 1 + Rh - 1) / Rh;
+  while ((P->head_segs * Rh) % TAIL_ALIGN) P->head_segs++;  // the tail starts on TAIL_ALIGN
   P->head_lim = P->head_segs * Rh;  // first y of the tail
-  P->tail_segs = 0;
-  if (u + 1 > P->head_lim) P->tail_segs = (u + 1 - P->head_lim + Rt - 1) / Rt;
-  P->y_last = P->head_lim + P->tail_segs * Rt - 1;
-  P->tseg0 = P->tail_segs * P->rank / P->world;
-  P->tseg1 = P->tail_segs * (P->rank + 1) / P->world;
-  RC(mt_sieve2_create(&P->sv, P->y_last, (uint32_t)(std::max(Rh, Rt) / MT_S2_TILE), st));
+  P->tail_end = P->head_lim;
+  if (u + 1 > P->head_lim) P->tail_end = (u + 1 + TAIL_ALIGN - 1) / TAIL_ALIGN * TAIL_ALIGN;
+  P->ybound = tail_partition(P->head_lim, P->tail_end, P->world);
+  P->ya = P->ybound[P->rank];
+  P->yb = P->ybound[P->rank + 1];
+  tail_segments(P->ya, P->yb, P->seg_y, P->tsegs, P->snap_a, P->snap_h);
+  P->y_last = std::max(P->tail_end, P->head_lim) - 1;
+  RC(mt_sieve2_create(&P->sv, P->y_last, (uint32_t)std::max<u64>(Rh / MT_S2_TILE, tail_tiles), st));
   RC(dalloc(P->d_mu, Rh)); RC(dalloc(P->d_m, Rh * 2)); RC(dalloc(P->d_bk, (Rh / MT_BLK) * 8 + 8));
-  RC(dalloc(P->d_run, 8));
-  RC(dalloc(P->d_caps, P->caps.size() * sizeof(CaptureTargetH)));
-  if (!P->caps.empty())
-    MT_CUDA_CHECK(cudaMemcpyAsync(P->d_caps.p, P->caps.data(), P->caps.size() * sizeof(CaptureTargetH), cudaMemcpyHostToDevice, st));
+  RC(dalloc(P->d_run, 8)); RC(dalloc(P->d_snap, 16));
+  // own tail slices, their P2 tables, and the tail capture list: Q at floor(n/j)
+  // and P2 at floor(floor(n/2)/j) = floor(n/(2j)) for j in the slice
+  P->sj0.assign(N, 1); P->sj1.assign(N, 0);
+  P->d_P2.clear();
+  P->d_P2.reserve(N);
+  for (int i = 0; i < N; i++) {
+    P->d_P2.emplace_back();
+    u64 j0, j1;
+    P->q_slice(i, P->rank, j0, j1);
+    P->sj0[i] = j0; P->sj1[i] = j1;
+    const u64 cnt = j1 >= j0 ? j1 - j0 + 1 : 0;
+    RC(dalloc(P->d_P2[i], cnt * 4));
+    if (cnt) {
+      P->caps_tail.push_back(make_cap(P->n[i], j0, j1, P->tdev[i].Q + (j0 - P->jq0[i])));
+      P->caps_tail.push_back(make_cap(P->n[i] / 2, j0, j1, P->d_P2[i].as<int>()));
+    }
+  }
+  RC(dalloc(P->d_caps_head, P->caps_head.size() * sizeof(CaptureTargetH)));
+  RC(dalloc(P->d_caps_tail, P->caps_tail.size() * sizeof(CaptureTargetH)));
+  if (!P->caps_head.empty())
+    MT_CUDA_CHECK(cudaMemcpyAsync(P->d_caps_head.p, P->caps_head.data(), P->caps_head.size() * sizeof(CaptureTargetH), cudaMemcpyHostToDevice, st));
+  if (!P->caps_tail.empty())
+    MT_CUDA_CHECK(cudaMemcpyAsync(P->d_caps_tail.p, P->caps_tail.data(), P->caps_tail.size() * sizeof(CaptureTargetH), cudaMemcpyHostToDevice, st));
   P->nsmall = P->cap_small ? P->cap_small + 1 : 0;
   P->cap32 = (P->flags & MT_FLAG_CAP32) != 0;
   RC(dalloc(P->d_small, P->nsmall * (P->cap32 ? 4 : 8)));
@@ -892,25 +1047,28 @@ extern "C" int mt_plan_create(const mt_job* job, mt_plan** out) {
 
 extern "C" void mt_plan_destroy(mt_plan* p) { delete p; }
 
-// phase 1: head (sieve + this rank's share of the updates) and this rank's tail segments
-// phase 1, resumable: the head (on the first step) and up to max_tail_segments
-// of this rank's tail segments per call; *done = 1 once the tail is complete
+// phase 1, resumable: the head (on the first step: sieve, this rank's share of
+// the head update, captures) and up to max_tail_segments of this rank's odd-cell
+// tail segments per call; *done = 1 once the tail is complete
 extern "C" int mt_plan_sieve_step(mt_plan* P, uint64_t max_tail_segments, int* done, int64_t* m_head,
                                   int64_t* tail_total) {
   PLAN_DEV(P);
   cudaStream_t st = P->st;
   if (!P->head_done) {
     P->kt.reset();
+    P->launches = 0;
+    mt_update_reset_launches(P->uc);
+    mt_sieve2_launches(P->sv, true);
     MT_CUDA_CHECK(cudaMemsetAsync(P->d_acc.p, 0, P->NE * 8, st));
     MT_CUDA_CHECK(cudaMemsetAsync(P->d_mmc.p, 0, P->NE * 4, st));
     MT_CUDA_CHECK(cudaMemsetAsync(P->d_run.p, 0, 8, st));
+    MT_CUDA_CHECK(cudaMemsetAsync(P->d_snap.p, 0, 16, st));
     MT_CUDA_CHECK(cudaEventRecord(P->ev[0], st));
     for (u64 s = 0; s < P->head_segs; s++) {
       const u64 Y0 = s * P->Rh;
       RC(mt_sieve2_run(P->sv, Y0, (uint32_t)(P->Rh / MT_S2_TILE), P->d_run.as<int64_t>(), P->d_mu.as<int8_t>(),
                        P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), nullptr,
-                       (const CaptureTarget2*)P->d_caps.p, (int)P->caps.size(), st, &P->kt));
-      P->launches += 2;
+                       (const CaptureTarget2*)P->d_caps_head.p, (int)P->caps_head.size(), st, &P->kt));
       RC(mt_update_head_segment(P->uc, Y0, P->Rh, P->d_mu.as<int8_t>(), P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), st));
       if (P->nsmall && Y0 <= P->cap_small) {
         if (P->cap32)
@@ -930,18 +1088,21 @@ extern "C" int mt_plan_sieve_step(mt_plan* P, uint64_t max_tail_segments, int* d
     P->ms_head = f;
     P->ms_tail = 0;
     P->m_head = mh;
-    P->tseg_next = P->tseg0;
+    P->tseg_next = 0;
     P->head_done = true;
   }
-  const u64 room = P->tseg1 > P->tseg_next ? P->tseg1 - P->tseg_next : 0;
+  const u64 ns = P->tsegs.size();
+  const u64 room = ns > P->tseg_next ? ns - P->tseg_next : 0;
   const u64 s_end = P->tseg_next + std::min<u64>(room, max_tail_segments);
   if (P->tseg_next < s_end) {
     MT_CUDA_CHECK(cudaEventRecord(P->ev[1], st));
     for (u64 s = P->tseg_next; s < s_end; s++) {
-      RC(mt_sieve2_run(P->sv, P->tail_y0(s), (uint32_t)(P->Rt / MT_S2_TILE), P->d_run.as<int64_t>(), nullptr,
-                       nullptr, nullptr, nullptr, (const CaptureTarget2*)P->d_caps.p, (int)P->caps.size(), st,
-                       &P->kt));
-      P->launches += 2;
+      RC(mt_sieve2_run(P->sv, P->tsegs[s].Y0, P->tsegs[s].ntiles, P->d_run.as<int64_t>(), nullptr, nullptr, nullptr,
+                       nullptr, (const CaptureTarget2*)P->d_caps_tail.p, (int)P->caps_tail.size(), st, &P->kt,
+                       true));
+      // prefix snapshots P(ya - 1) and P(yb/2 - 1)
+      if (s + 1 == P->snap_a) MT_CUDA_CHECK(cudaMemcpyAsync(P->d_snap.as<int64_t>(), P->d_run.p, 8, cudaMemcpyDeviceToDevice, st));
+      if (s + 1 == P->snap_h) MT_CUDA_CHECK(cudaMemcpyAsync(P->d_snap.as<int64_t>() + 1, P->d_run.p, 8, cudaMemcpyDeviceToDevice, st));
     }
     MT_CUDA_CHECK(cudaEventRecord(P->ev[2], st));
     MT_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -951,14 +1112,17 @@ extern "C" int mt_plan_sieve_step(mt_plan* P, uint64_t max_tail_segments, int* d
     P->tseg_next = s_end;
   }
   MT_CUDA_CHECK(cudaGetLastError());
-  *done = P->tseg_next >= P->tseg1;
+  *done = P->tseg_next >= ns;
   if (*done) {
-    int64_t tt = 0;
-    MT_CUDA_CHECK(cudaMemcpy(&tt, P->d_run.p, 8, cudaMemcpyDeviceToHost));
-    P->tail_total = tt;
+    int64_t v[3] = {0, 0, 0};
+    MT_CUDA_CHECK(cudaMemcpy(v, P->d_run.p, 8, cudaMemcpyDeviceToHost));
+    MT_CUDA_CHECK(cudaMemcpy(v + 1, P->d_snap.p, 16, cudaMemcpyDeviceToHost));
+    P->p_end = v[0]; P->s_a = v[1]; P->s_h = v[2];
+    // this rank's M-total over [ya, yb): (own odd sum) - (half-range odd sum)
+    P->tail_total = ns ? (P->p_end - P->s_a) - P->s_h : 0;
     P->phase = 1;
     if (m_head) *m_head = P->m_head;
-    if (tail_total) *tail_total = tt;
+    if (tail_total) *tail_total = P->tail_total;
   }
   return MT_OK;
 }
@@ -974,7 +1138,7 @@ extern "C" int mt_plan_sieve_update(mt_plan* P, int64_t* m_head, int64_t* tail_t
 }
 
 // ---- checkpoint / resume (reference MERTCKP1 header, engine.py:646-680, with
-// version 2 marking the sm100 engine state that follows it)
+// version 3 marking the sm100 engine state that follows it)
 #pragma pack(push, 1)
 struct CkptHead {
   char magic[8];
@@ -985,14 +1149,19 @@ struct CkptHead {
 };
 #pragma pack(pop)
 static_assert(sizeof(CkptHead) == 72, "MERTCKP1 header is <8sII QQ Q Q Q q Q>");
+#define MT_CKPT_VERSION 3
 
+static int write_all(FILE* f, const void* p, u64 bytes) {
+  if (bytes && fwrite(p, 1, bytes, f) != bytes) { mt_set_error("checkpoint write failed (disk full?)"); return MT_ERR_RESOURCE; }
+  return MT_OK;
+}
 static int write_dev(FILE* f, const void* dptr, u64 bytes) {
   const u64 CH = 256ull << 20;
   std::vector<char> h((size_t)std::min(bytes, CH));
   for (u64 o = 0; o < bytes; o += CH) {
     const u64 b = std::min(CH, bytes - o);
     MT_CUDA_CHECK(cudaMemcpy(h.data(), (const char*)dptr + o, b, cudaMemcpyDeviceToHost));
-    if (fwrite(h.data(), 1, b, f) != b) { mt_set_error("checkpoint write failed"); return MT_ERR_RESOURCE; }
+    RC(write_all(f, h.data(), b));
   }
   return MT_OK;
 }
@@ -1006,99 +1175,140 @@ static int read_dev(FILE* f, void* dptr, u64 bytes) {
   }
   return MT_OK;
 }
+static int read_u64(FILE* f, u64* v) {
+  if (fread(v, 8, 1, f) != 1) { mt_set_error("checkpoint truncated"); return MT_ERR_CONTRACT; }
+  return MT_OK;
+}
 
+// header flags: shard rank | world << 16 (one file per rank; single-target jobs)
 // layout after the header: acc (K u64), M(mcut) (K i32), Q (u64 count + int32),
-// small captures (u64 count + element bytes), head M (i64) and tail running (i64)
-extern "C" int mt_plan_checkpoint(mt_plan* P, const char* path) {
-  if (P->N != 1 || P->world != 1) { mt_set_error("checkpoints cover single-target, single-rank jobs only"); return MT_ERR_CONTRACT; }
-  if (!P->head_done) { mt_set_error("checkpoint before the head is sieved"); return MT_ERR_CONTRACT; }
-  PLAN_DEV(P);
-  MT_CUDA_CHECK(cudaStreamSynchronize(P->st));
-  int64_t run = 0;
-  MT_CUDA_CHECK(cudaMemcpy(&run, P->d_run.p, 8, cudaMemcpyDeviceToHost));
-  std::string tmp = std::string(path) + ".tmp";
-  FILE* f = fopen(tmp.c_str(), "wb");
-  if (!f) { mt_set_error("cannot open %s", tmp.c_str()); return MT_ERR_RESOURCE; }
-  struct Closer { FILE* f; ~Closer() { if (f) fclose(f); } } cl{f};
+// P2 (u64 count + int32), small captures (u64 count + element bytes), head M,
+// running prefix and the two prefix snapshots (i64 each)
+static int ckpt_write(mt_plan* P, FILE* f) {
+  int64_t tail[4] = {P->m_head, 0, 0, 0};
+  MT_CUDA_CHECK(cudaMemcpy(tail + 1, P->d_run.p, 8, cudaMemcpyDeviceToHost));
+  MT_CUDA_CHECK(cudaMemcpy(tail + 2, P->d_snap.p, 16, cudaMemcpyDeviceToHost));
   CkptHead h{};
   memcpy(h.magic, "MERTCKP1", 8);
-  h.version = 2;
-  h.flags = 0;
+  h.version = MT_CKPT_VERSION;
+  h.flags = P->rank | (P->world << 16);
   h.n_lo = P->n_lo[0]; h.n_hi = P->n_hi[0]; h.u = P->u;
-  h.next_y1 = P->tseg_next < P->tail_segs ? P->tail_y0(P->tseg_next) : P->y_last + 1;
+  h.next_y1 = P->tseg_next < P->tsegs.size() ? P->tsegs[P->tseg_next].Y0 : P->y_last + 1;
   h.K = P->K[0];
-  h.m_running = P->m_head + run;  // M(next_y1 - 1)
-  h.block_len = P->Rt;
-  if (fwrite(&h, sizeof(h), 1, f) != 1) { mt_set_error("checkpoint write failed"); return MT_ERR_RESOURCE; }
+  h.m_running = P->m_head;
+  h.block_len = P->seg_y;
+  RC(write_all(f, &h, sizeof(h)));
   RC(write_dev(f, P->d_acc.p, P->NE * 8));
   RC(write_dev(f, P->d_mmc.p, P->NE * 4));
   const u64 qn = P->jq1[0] >= P->jq0[0] ? P->jq1[0] - P->jq0[0] + 1 : 0;
-  fwrite(&qn, 8, 1, f);
+  RC(write_all(f, &qn, 8));
   RC(write_dev(f, P->tdev[0].Q, qn * 4));
+  const u64 pn = P->sj1[0] >= P->sj0[0] ? P->sj1[0] - P->sj0[0] + 1 : 0;
+  RC(write_all(f, &pn, 8));
+  RC(write_dev(f, P->d_P2[0].p, pn * 4));
   const u64 sb = P->nsmall * (P->cap32 ? 4 : 8);
-  fwrite(&sb, 8, 1, f);
+  RC(write_all(f, &sb, 8));
   RC(write_dev(f, P->d_small.p, sb));
-  fwrite(&P->m_head, 8, 1, f);
-  fwrite(&run, 8, 1, f);
-  fclose(f);
-  cl.f = nullptr;
-  if (rename(tmp.c_str(), path) != 0) { mt_set_error("cannot move %s into place", tmp.c_str()); return MT_ERR_RESOURCE; }
+  RC(write_all(f, tail, sizeof(tail)));
+  return MT_OK;
+}
+
+// written to path.tmp, flushed and synced, then renamed over path: a failed
+// write leaves the previous checkpoint in place
+extern "C" int mt_plan_checkpoint(mt_plan* P, const char* path) {
+  if (P->N != 1) { mt_set_error("checkpoints cover single-target jobs only"); return MT_ERR_CONTRACT; }
+  if (!P->head_done) { mt_set_error("checkpoint before the head is sieved"); return MT_ERR_CONTRACT; }
+  PLAN_DEV(P);
+  MT_CUDA_CHECK(cudaStreamSynchronize(P->st));
+  std::string tmp = std::string(path) + ".tmp";
+  FILE* f = fopen(tmp.c_str(), "wb");
+  if (!f) { mt_set_error("cannot open %s", tmp.c_str()); return MT_ERR_RESOURCE; }
+  int rc = ckpt_write(P, f);
+  if (rc == MT_OK && fflush(f) != 0) { mt_set_error("checkpoint flush failed"); rc = MT_ERR_RESOURCE; }
+  if (rc == MT_OK && fsync(fileno(f)) != 0) { mt_set_error("checkpoint fsync failed"); rc = MT_ERR_RESOURCE; }
+  if (fclose(f) != 0 && rc == MT_OK) { mt_set_error("checkpoint close failed"); rc = MT_ERR_RESOURCE; }
+  if (rc != MT_OK) { remove(tmp.c_str()); return rc; }
+  if (rename(tmp.c_str(), path) != 0) { remove(tmp.c_str()); mt_set_error("cannot move %s into place", tmp.c_str()); return MT_ERR_RESOURCE; }
   return MT_OK;
 }
 
 extern "C" int mt_plan_restore(mt_plan* P, const char* path) {
-  if (P->N != 1 || P->world != 1) { mt_set_error("checkpoints cover single-target, single-rank jobs only"); return MT_ERR_CONTRACT; }
+  if (P->N != 1) { mt_set_error("checkpoints cover single-target jobs only"); return MT_ERR_CONTRACT; }
   PLAN_DEV(P);
   FILE* f = fopen(path, "rb");
   if (!f) { mt_set_error("cannot open %s", path); return MT_ERR_VALUE; }
   struct Closer { FILE* f; ~Closer() { fclose(f); } } cl{f};
   CkptHead h{};
-  if (fread(&h, sizeof(h), 1, f) != 1 || memcmp(h.magic, "MERTCKP1", 8) || h.version != 2) {
-    mt_set_error("not an sm100 checkpoint file");
+  if (fread(&h, sizeof(h), 1, f) != 1 || memcmp(h.magic, "MERTCKP1", 8) || h.version != MT_CKPT_VERSION) {
+    mt_set_error("not an sm100 checkpoint file (version %u)", MT_CKPT_VERSION);
     return MT_ERR_CONTRACT;
   }
-  if (h.n_lo != P->n_lo[0] || h.n_hi != P->n_hi[0] || h.u != P->u || h.K != P->K[0] || h.block_len != P->Rt) {
-    mt_set_error("checkpoint built for another job (n, u, K or segment size differ)");
+  if (h.n_lo != P->n_lo[0] || h.n_hi != P->n_hi[0] || h.u != P->u || h.K != P->K[0] || h.block_len != P->seg_y ||
+      h.flags != (P->rank | (P->world << 16))) {
+    mt_set_error("checkpoint built for another job (n, u, K, segment size or rank/world differ)");
     return MT_ERR_CONTRACT;
   }
   RC(read_dev(f, P->d_acc.p, P->NE * 8));
   RC(read_dev(f, P->d_mmc.p, P->NE * 4));
-  u64 qn = 0, sb = 0;
-  if (fread(&qn, 8, 1, f) != 1) { mt_set_error("checkpoint truncated"); return MT_ERR_CONTRACT; }
+  u64 qn = 0, pn = 0, sb = 0;
+  RC(read_u64(f, &qn));
   const u64 qn_plan = P->jq1[0] >= P->jq0[0] ? P->jq1[0] - P->jq0[0] + 1 : 0;
   if (qn != qn_plan) { mt_set_error("checkpoint quotient table differs from this plan's"); return MT_ERR_CONTRACT; }
   RC(read_dev(f, P->tdev[0].Q, qn * 4));
-  if (fread(&sb, 8, 1, f) != 1 || sb != P->nsmall * (P->cap32 ? 4 : 8)) { mt_set_error("checkpoint capture size differs"); return MT_ERR_CONTRACT; }
+  RC(read_u64(f, &pn));
+  const u64 pn_plan = P->sj1[0] >= P->sj0[0] ? P->sj1[0] - P->sj0[0] + 1 : 0;
+  if (pn != pn_plan) { mt_set_error("checkpoint tail slice differs from this plan's"); return MT_ERR_CONTRACT; }
+  RC(read_dev(f, P->d_P2[0].p, pn * 4));
+  RC(read_u64(f, &sb));
+  if (sb != P->nsmall * (P->cap32 ? 4 : 8)) { mt_set_error("checkpoint capture size differs"); return MT_ERR_CONTRACT; }
   RC(read_dev(f, P->d_small.p, sb));
-  int64_t mh = 0, run = 0;
-  if (fread(&mh, 8, 1, f) != 1 || fread(&run, 8, 1, f) != 1) { mt_set_error("checkpoint truncated"); return MT_ERR_CONTRACT; }
-  MT_CUDA_CHECK(cudaMemcpy(P->d_run.p, &run, 8, cudaMemcpyHostToDevice));
-  P->m_head = mh;
+  int64_t tail[4];
+  if (fread(tail, sizeof(tail), 1, f) != 1) { mt_set_error("checkpoint truncated"); return MT_ERR_CONTRACT; }
+  MT_CUDA_CHECK(cudaMemcpy(P->d_run.p, tail + 1, 8, cudaMemcpyHostToDevice));
+  MT_CUDA_CHECK(cudaMemcpy(P->d_snap.p, tail + 2, 16, cudaMemcpyHostToDevice));
+  P->m_head = tail[0];
   P->head_done = true;
-  P->tseg_next = h.next_y1 > P->y_last ? P->tail_segs : (h.next_y1 - P->head_lim) / P->Rt;
-  if (P->tail_y0(std::min(P->tseg_next, P->tail_segs)) != h.next_y1 && h.next_y1 <= P->y_last) {
+  u64 s = 0;
+  while (s < P->tsegs.size() && P->tsegs[s].Y0 != h.next_y1) s++;
+  if (s == P->tsegs.size() && h.next_y1 != P->y_last + 1) {
     mt_set_error("checkpoint position is not a tail segment boundary");
     return MT_ERR_CONTRACT;
   }
+  P->tseg_next = s;
   P->kt.reset();
+  P->launches = 0;
+  mt_update_reset_launches(P->uc);
+  mt_sieve2_launches(P->sv, true);
   P->ms_head = 0;
   P->ms_tail = 0;
   return MT_OK;
 }
 
-// phase 2: absolute prefixes for this rank's tail captures: Q += M(Y_r - 1)
+// phase 2: absolute M on this rank's tail slices: Q[j] = P(floor(n/j)) -
+// P(floor(n/(2j))) - P(ya - 1) + M(ya - 1), offset = M(ya - 1).  With world > 1
+// the capture window is then masked to the entries this rank owns, ready for
+// the caller's sum-reduction (mt_plan_cap_window).
 extern "C" int mt_plan_tail_offset(mt_plan* P, int64_t offset) {
   if (P->phase < 1) { mt_set_error("tail_offset before sieve_update"); return MT_ERR_CONTRACT; }
   PLAN_DEV(P);
-  if (offset > INT32_MAX || offset < INT32_MIN) { mt_set_error("M offset beyond int32"); return MT_ERR_OVERFLOW; }
+  const int64_t delta = offset - P->s_a;
+  if (delta > INT32_MAX || delta < INT32_MIN) { mt_set_error("M offset beyond int32"); return MT_ERR_OVERFLOW; }
   for (int t = 0; t < P->N; t++) {
-    u64 j0, j1;
-    P->q_slice(t, P->rank, j0, j1);
-    if (j0 > j1 || offset == 0) continue;
-    u64 cnt = j1 - j0 + 1;
-    k_q_offset<<<(unsigned)((cnt + 255) / 256), 256, 0, P->st>>>(P->tdev[t].Q + (j0 - P->jq0[t]), cnt, (int)offset);
+    if (P->sj0[t] > P->sj1[t]) continue;
+    const u64 cnt = P->sj1[t] - P->sj0[t] + 1;
+    k_q_combine<<<(unsigned)((cnt + 255) / 256), 256, 0, P->st>>>(P->tdev[t].Q + (P->sj0[t] - P->jq0[t]),
+                                                                  P->d_P2[t].as<int>(), cnt, (int)delta);
     P->launches++;
     MT_CUDA_CHECK(cudaGetLastError());
+  }
+  if (P->world > 1 && P->cap_c_hi >= P->cap_c_lo && P->jq1[0] >= P->jq0[0]) {
+    const u64 c0 = std::max(P->cap_c_lo, P->jq0[0]), c1 = std::min(P->cap_c_hi, P->jq1[0]);
+    if (c1 >= c0) {
+      k_cap_mask<<<(unsigned)((c1 - c0 + 1 + 255) / 256), 256, 0, P->st>>>(P->tdev[0].Q, P->jq0[0], c0, c1, P->sj0[0],
+                                                                           P->sj1[0], P->head_j(0), P->rank == 0);
+      P->launches++;
+      MT_CUDA_CHECK(cudaGetLastError());
+    }
   }
   MT_CUDA_CHECK(cudaStreamSynchronize(P->st));
   P->phase = 2;
@@ -1115,22 +1325,49 @@ extern "C" int mt_plan_q_slice(mt_plan* P, uint32_t target, uint32_t rank, void*
   return MT_OK;
 }
 
+// target 0's capture window Q[cap_c_lo .. cap_c_hi] (device int32): with world > 1,
+// after tail_offset each rank holds its own entries and zeros elsewhere, so one
+// sum-reduction assembles the window (the M(floor(n/c)) outputs) on every rank
+extern "C" int mt_plan_cap_window(mt_plan* P, void** dptr, uint64_t* count) {
+  *dptr = nullptr;
+  *count = 0;
+  if (P->cap_c_hi < P->cap_c_lo || P->jq1[0] < P->jq0[0]) return MT_OK;
+  const u64 c0 = std::max(P->cap_c_lo, P->jq0[0]), c1 = std::min(P->cap_c_hi, P->jq1[0]);
+  if (c1 < c0) return MT_OK;
+  *dptr = (void*)(P->tdev[0].Q + (c0 - P->jq0[0]));
+  *count = c1 - c0 + 1;
+  return MT_OK;
+}
+
 extern "C" int mt_plan_acc(mt_plan* P, void** dptr, uint64_t* count) {
   *dptr = P->d_acc.p;
   *count = P->NE;
   return MT_OK;
 }
 
-// phase 3: dense items from the (complete) quotient tables; rank 0 also
-// applies the summation-by-parts correction -M(mcut)*xcut
+// phase 3: dense items from the quotient tables -- with world > 1 rank r takes
+// the items whose table entry lies in its own tail slice plus every w-th chunk
+// of the items in the (replicated) head part; rank 0 also applies the
+// summation-by-parts correction -M(mcut)*xcut
 extern "C" int mt_plan_gather(mt_plan* P) {
   if (P->phase < 2) { mt_set_error("gather before tail_offset"); return MT_ERR_CONTRACT; }
   PLAN_DEV(P);
   MT_CUDA_CHECK(cudaEventRecord(P->ev[3], P->st));
-  u64 qmax = 0;
-  for (size_t i = 0; i < P->jq0.size(); i++)
-    if (P->jq1[i] >= P->jq0[i]) qmax = std::max<u64>(qmax, P->jq1[i] - P->jq0[i] + 1);
-  RC(mt_update_qgather(P->uc, qmax, P->st));
+  const int N = P->N;
+  std::vector<u64> wlo(N, 0), whi(N, 0);
+  for (int t = 0; t < N; t++) whi[t] = P->jq1[t] >= P->jq0[t] ? P->jq1[t] - P->jq0[t] + 1 : 0;
+  if (P->world == 1) {
+    RC(mt_update_qgather(P->uc, wlo.data(), whi.data(), false, P->st));
+  } else {
+    std::vector<u64> slo(N, 0), shi(N, 0), hlo(N, 0);
+    for (int t = 0; t < N; t++) {
+      if (P->sj1[t] >= P->sj0[t]) { slo[t] = P->sj0[t] - P->jq0[t]; shi[t] = P->sj1[t] - P->jq0[t] + 1; }
+      const u64 jh = P->head_j(t);
+      hlo[t] = jh > P->jq0[t] ? std::min(jh - P->jq0[t], whi[t]) : 0;
+    }
+    RC(mt_update_qgather(P->uc, slo.data(), shi.data(), false, P->st));
+    RC(mt_update_qgather(P->uc, hlo.data(), whi.data(), true, P->st));
+  }
   if (P->rank == 0) RC(mt_update_finish(P->uc, P->st));
   MT_CUDA_CHECK(cudaEventRecord(P->ev[4], P->st));
   MT_CUDA_CHECK(cudaStreamSynchronize(P->st));
@@ -1147,7 +1384,7 @@ extern "C" int mt_plan_resolve(mt_plan* P, mt_result* out) {
   cudaStream_t st = P->st;
   MT_CUDA_CHECK(cudaEventRecord(P->ev[4], st));
   for (int i = 0; i < P->N; i++)
-    RC(mt_finalize_dev(P->d_acc.as<u64>() + P->e0[i], P->d_D.as<u64>() + P->e0[i], P->K[i], P->d_fin.as<int64_t>() + P->e0[i], st));
+    RC(mt_finalize_dev(P->d_acc.as<u64>() + P->e0[i], P->d_D.as<u64>() + P->e0[i], P->K[i], P->d_fin.as<int64_t>() + P->e0[i], st, &P->launches));
   MT_CUDA_CHECK(cudaEventRecord(P->ev[5], st));
   DevBuf d_capm;
   if (out && out->finals && P->NE)
@@ -1163,6 +1400,7 @@ extern "C" int mt_plan_resolve(mt_plan* P, mt_result* out) {
     if (P->cap_c_lo < P->jq0[0]) { mt_set_error("capture range below floor(n/(u+1))+1"); return MT_ERR_VALUE; }
     RC(dalloc(d_capm, cnt * 8));
     k_copy_caps<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(P->tdev[0].Q, P->jq0[0], P->cap_c_lo, cnt, d_capm.as<int64_t>());
+    P->launches++;
     MT_CUDA_CHECK(cudaMemcpyAsync(out->cap_m_out, d_capm.p, cnt * 8, cudaMemcpyDeviceToHost, st));
   }
   if (out && out->small_m_out && P->nsmall)
@@ -1181,8 +1419,10 @@ extern "C" int mt_plan_resolve(mt_plan* P, mt_result* out) {
   S.head_end = P->head_lim;
   S.max_mcut = P->Ymc;
   S.n_head_segments = P->head_segs;
-  S.n_tail_segments = P->tail_segs;
-  S.kernel_launches = P->launches + mt_update_launches(P->uc);
+  S.n_tail_segments = P->tsegs.size();
+  // kernels of this execution: the plan's own, the update context's (cub scans
+  // count 2 each) and the sieve's (fill + tile + finish per segment)
+  S.kernel_launches = P->launches + mt_update_launches(P->uc) + mt_sieve2_launches(P->sv, false);
   u64 qe = 0;
   for (int i = 0; i < P->N; i++) qe += P->jq1[i] >= P->jq0[i] ? P->jq1[i] - P->jq0[i] + 1 : 0;
   S.q_entries = qe;
@@ -1194,11 +1434,13 @@ extern "C" int mt_plan_resolve(mt_plan* P, mt_result* out) {
   S.ms_setup = P->ms_setup;
   S.m_head = P->m_head;
   S.tail_total = P->tail_total;
-  S.tail_seg_begin = P->tseg0;
-  S.tail_seg_end = P->tseg1;
+  S.tail_seg_begin = P->ya;
+  S.tail_seg_end = P->yb;
   for (int c = 0; c < KT_NCLASS && c < 8; c++) { S.kernel_ms[c] = P->kt.ms[c]; S.kernel_count[c] = P->kt.n[c]; }
   S.ms_counted_kernel = P->kt.ms[KT_COUNTED];
   S.ms_dense_kernel = P->kt.ms[KT_DWIN] + P->kt.ms[KT_DSPARSE] + P->kt.ms[KT_QGATHER];
+  S.head_cells = P->head_lim;
+  S.tail_cells = P->tail_cells();
   return MT_OK;
 }
 

@@ -157,6 +157,7 @@ struct Sieve2Args {
   int64_t* tile_base;                         // [ntiles] M(tile start - 1)
   int* bkrel;                                 // head: tile-relative 32K block starts [ntiles*4]
   uint32_t tiles_per_cta;                     // persistent CTAs: contiguous tiles each
+  uint32_t odd;                               // odd-cell mode: cell c of the segment is y = Y0 + 2c + 1
   const CaptureTarget2* caps;
   int n_cap;
 };
@@ -172,10 +173,13 @@ struct Sieve2Host;
 int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cudaStream_t st);
 void mt_sieve2_destroy(Sieve2Host* h);
 // one segment [Y0, Y0 + ntiles*2^17): outputs as requested (null = skip)
+// odd = true: the segment's cells are the odd y of [Y0, Y0 + ntiles * 2^18) (tail
+// mode: sums and captures of the odd-y prefix; mu_out gets mu of the odd y)
 int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running, int8_t* mu_out,
                   int16_t* m16_out, int64_t* bk, uint8_t* states_out, const CaptureTarget2* caps,
-                  int n_cap, cudaStream_t st, KTimer* kt);
+                  int n_cap, cudaStream_t st, KTimer* kt, bool odd = false);
 uint64_t mt_sieve2_overflows(Sieve2Host* h);
+uint64_t mt_sieve2_launches(Sieve2Host* h, bool reset);
 #define MT_S2_TILE (1u << 17)
 
 // element arrays (device, SoA), one entry per harmonic-array element of every target
@@ -198,6 +202,7 @@ struct ElemDev {
 struct TargetDev {       // per-target constants for Q lookups
   int* Q;                // Q[j - jq0]
   uint64_t jq0;
+  uint64_t wlo, whi;     // Q-gather window of this pass: table indices [wlo, whi)
 };
 
 // update-side launchers (mt_update.cu)
@@ -221,10 +226,13 @@ int mt_update_create(UpdateCtx** ctx, const ElemDev& E, uint64_t* acc, int32_t* 
 void mt_update_destroy(UpdateCtx* ctx);
 int mt_update_head_segment(UpdateCtx* ctx, uint64_t Y0, uint64_t R, const int8_t* mu,
                            const int16_t* M16, const int64_t* bk, cudaStream_t st);
-int mt_update_qgather(UpdateCtx* ctx, uint64_t qmax, cudaStream_t st);  // qmax: largest table (entries)
+// dense items whose table index k*d - jq0 lies in the per-target window [wlo[t], whi[t]);
+// interleave: this rank takes every world-th work chunk (else all of them)
+int mt_update_qgather(UpdateCtx* ctx, const uint64_t* wlo, const uint64_t* whi, bool interleave, cudaStream_t st);
+void mt_update_reset_launches(UpdateCtx* ctx);
 int mt_update_finish(UpdateCtx* ctx, cudaStream_t st);  // acc -= M(mcut)*xcut
 int mt_finalize_dev(const uint64_t* acc, const uint64_t* D, uint64_t K, int64_t* final_out,
-                    cudaStream_t st);
+                    cudaStream_t st, uint64_t* launches = nullptr);
 int mt_apply_block_dev(uint64_t K, int64_t* acc, const uint64_t* v, const uint64_t* lo,
                        const uint64_t* xcut, const uint64_t* mcut, uint64_t* dnext,
                        uint64_t* ynext, uint64_t y1, uint64_t y2, const int64_t* mp,

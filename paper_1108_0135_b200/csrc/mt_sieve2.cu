@@ -45,6 +45,7 @@
 #define S2_NT 1024               // threads per tile CTA
 #define S2_CH (S2_T / 32)        // 32-cell chunks per tile
 #define S2_MAXPROD 512           // bucket producers whose counts are staged in shared memory
+#define S2_MAXCAP 128            // capture targets whose j ranges are staged per tile
 #ifndef S2_A_MAX
 #define S2_A_MAX 1024u           // warp-per-prime marks below this, lane-per-prime from here
 #endif
@@ -68,6 +69,33 @@ __device__ __forceinline__ u32 neg_mod(u64 Y, double Yd, double r, u32 p) {
   return rem ? p - rem : 0u;
 }
 
+// first cell >= C0 hit by prime p.  Full mode: cells are y (y = 0 is never
+// marked).  Odd mode (the tail): cell c holds y = 2c + 1, and
+// p | 2c + 1  <=>  c == (p - 1)/2 (mod p), so the hits of p are the cells
+// (p - 1)/2 + p*t -- one plain stream of stride p, as in full mode.
+template <bool ODD>
+__device__ __forceinline__ u32 first_hit(u64 C0, double Cd, double r, u32 p) {
+  u32 j = neg_mod(C0, Cd, r, p);
+  if (ODD) {
+    const u64 jj = (u64)j + (p >> 1);
+    j = (u32)(jj >= p ? jj - p : jj);
+  } else if (C0 == 0 && j == 0) {
+    j = p;
+  }
+  return j;
+}
+// same for a square q = p^2 (q < 2^63)
+template <bool ODD>
+__device__ __forceinline__ u64 first_hit_sq(u64 C0, double Cd, u64 q) {
+  const u64 qq = qdiv64(Cd, __drcp_rn((double)q), C0, q);
+  const u64 rem = C0 - qq * q;
+  if (ODD) {
+    const u64 f = (rem ? q - rem : 0) + (q >> 1);
+    return f >= q ? f - q : f;
+  }
+  return rem ? q - rem : (C0 ? 0 : q);
+}
+
 // ----------------------------------------------------------------------------
 // bucket producer: every hit of a prime p > S2_T (log marks) and of p^2 > S2_T
 // (square flags) in the segment [Y0, Y0 + R), appended to the producer-private
@@ -86,6 +114,7 @@ __device__ __forceinline__ u32 neg_mod(u64 Y, double Yd, double r, u32 p) {
 // past a full bin, and all square flags, are stored directly.
 #define FBATCH 1024  // primes per batch
 #define FITEM 32     // hits per item (1024 items per round: ~32k hits over the tiles)
+template <bool ODD>
 __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
   // dynamic: rcnt[ntiles + 1] (round counts; [ntiles] = dummy), gcnt[ntiles]
   // (entries before this round), cnt2[ntiles] (square flags), stage[ntiles][bin]
@@ -108,8 +137,9 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
   if (tid == 0) s_hits = 0;
   for (u32 t = tid; t < 3 * nt + 1; t += blockDim.x) dsm[t] = 0;
   const u64 Y0 = a.Y0;
+  const u64 C0 = ODD ? Y0 >> 1 : Y0;  // first cell of the segment (odd mode: cell c <-> y = 2c + 1)
   const u32 R = nt * S2_T;  // <= 2^31
-  const double Yd = (double)Y0;
+  const double Yd = (double)C0;
   u32* __restrict__ out = a.buf + (u64)b * nt * a.cap;
   const u32 cap = a.cap;
   // this producer's primes: log marks p_lo + b + k*NP, then squares q_lo + b + k*NP
@@ -126,16 +156,13 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
       if (k < nprim) {
         if (k < nlog) {
           const u32 p = a.pperm[(u64)b * a.kp + k];  // producer-major copy: coalesced; 1/p and log recomputed
-          q0 = neg_mod(Y0, Yd, __drcp_rn((double)p), p);
-          if (Y0 == 0 && q0 == 0) q0 = p;  // y = 0 is never marked
+          q0 = first_hit<ODD>(C0, Yd, __drcp_rn((double)p), p);
           step = p;
           val = ((32u - __clz(p - 1)) | 1u) << 17;  // ceil(log2 p) | 1
         } else {
           const u64 p = a.qperm[(u64)b * a.kq + (k - nlog)];
           const u64 q = p * p;
-          const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Y0, q);
-          const u64 rem = Y0 - qq * q;
-          const u64 f = rem ? q - rem : (Y0 ? 0 : q);
+          const u64 f = first_hit_sq<ODD>(C0, Yd, q);
           q0 = f < R ? (u32)f : R;
           step = q < R ? (u32)q : R;  // one hit at most when q >= R
           val = 0x80u << 17;
@@ -298,7 +325,9 @@ __device__ __forceinline__ int mu_cell(u32 s, int thr) {
 // outputs are tile-relative; k_s3_finish makes them absolute.
 // ----------------------------------------------------------------------------
 
+template <bool ODD>
 __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
+  constexpr u64 SPAN = ODD ? 2ull * S2_T : (u64)S2_T;  // y per tile
   extern __shared__ u32 st[];                   // S2_W state / mu words
   int* csum = (int*)(st + S2_W);                // S2_CH chunk sums -> exclusive chunk prefixes
   const u32 nA = a.p_warp_end - a.p_first;
@@ -315,6 +344,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
   __shared__ int s_total;
   __shared__ u32 s_dnext;
   __shared__ u32 s_cnt[S2_MAXPROD];  // this tile's bucket-list counts
+  __shared__ u64 s_cj[2][S2_MAXCAP];   // capture j ranges of this tile
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 m = a.tiles_per_cta;
   const u32 tile0 = blockIdx.x * m;
@@ -325,39 +355,35 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
 
   // ---- first multiples at the CTA's first tile
   {
-    const u64 Y = a.Y0 + (u64)tile0 * S2_T;
-    const double Yd = (double)Y;
+    const u64 Y = a.Y0 + (u64)tile0 * SPAN;
+    const u64 C = ODD ? Y >> 1 : Y;
+    const double Cd = (double)C;
     for (u32 k = tid; k < nA; k += S2_NT) {
       const u32 i = a.p_first + k, p = a.primes[i];
-      u32 j = neg_mod(Y, Yd, a.rprimes[i], p);
-      if (Y == 0 && j == 0) j = p;
-      offA[k] = j;
+      offA[k] = first_hit<ODD>(C, Cd, a.rprimes[i], p);
       tmA[k] = S2_T % p;
     }
     for (u32 k = tid; k < nBp; k += S2_NT) {
       const u32 i = a.p_warp_end + k, p = a.primes[i];
-      u32 j = neg_mod(Y, Yd, a.rprimes[i], p);
-      if (Y == 0 && j == 0) j = p;
-      offB[k] = j;
+      offB[k] = first_hit<ODD>(C, Cd, a.rprimes[i], p);
       pB[k] = (uint16_t)((p - 1) >> 1);
     }
     for (u32 k = tid; k < nC; k += S2_NT) {
       const u32 p = a.primes[a.sq_first + k], q = p * p;
-      u32 j = neg_mod(Y, Yd, __drcp_rn((double)q), q);
-      if (Y == 0 && j == 0) j = q;
-      offC[k] = j;
+      offC[k] = first_hit<ODD>(C, Cd, __drcp_rn((double)q), q);
       tmC[k] = S2_T % q;
     }
   }
 
   for (u32 tile = tile0; tile < tile_end; tile++) {
-    const u64 Yt = a.Y0 + (u64)tile * S2_T;
+    const u64 Yt = a.Y0 + (u64)tile * SPAN;    // first y of the tile
+    const u64 Ct = ODD ? Yt >> 1 : Yt;         // first cell of the tile
     __syncthreads();  // offsets ready / previous tile's outputs done
     if (tid == 0) s_dnext = 0;
     // 1. presieve patterns
     {
-      const u32* __restrict__ w1 = a.w1 + (u32)((Yt % a.w1_period4) >> 2);
-      const u32* __restrict__ w2 = a.w2 + (u32)((Yt % a.w2_period4) >> 2);
+      const u32* __restrict__ w1 = a.w1 + (u32)((Ct % a.w1_period4) >> 2);
+      const u32* __restrict__ w2 = a.w2 + (u32)((Ct % a.w2_period4) >> 2);
       for (int i = tid; i < (int)S2_W; i += S2_NT) st[i] = w1[i] + w2[i];
     }
     for (u32 b = tid; b < a.nprod && b < S2_MAXPROD; b += S2_NT) s_cnt[b] = a.counts[(u64)b * a.ntiles + tile];
@@ -442,7 +468,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
     // D: bucket lists (primes > big_min, squares > 2^17), dealt to warps from a
     //    shared counter so warps that finished A-C early take more lists
     if (a.nprod) {
-      const double Yd = (double)Yt;
+      const double Cd = (double)Ct;
       for (;;) {
         u32 b = 0;
         if (lane == 0) b = atomicAdd(&s_dnext, 1u);
@@ -477,16 +503,12 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
           if (lane == 0) atomicAdd(a.overflow, 1ull);
           for (u64 i = (u64)a.p_lo + b + (u64)lane * a.nprod; i < a.p_hi; i += 32ull * a.nprod) {
             const u32 p = a.primes[i];
-            u32 j = neg_mod(Yt, Yd, a.rprimes[i], p);
-            if (Yt == 0 && j == 0) j = p;
+            u32 j = first_hit<ODD>(Ct, Cd, a.rprimes[i], p);
             for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), (u32)a.logs[i] << ((j & 3) * 8));
           }
           for (u64 i = (u64)a.q_lo + b + (u64)lane * a.nprod; i < a.q_hi; i += 32ull * a.nprod) {
             const u64 p = a.primes[i];
-            const u64 q = p * p;
-            const u64 qq = qdiv64(Yd, __drcp_rn((double)q), Yt, q);
-            const u64 rem = Yt - qq * q;
-            const u64 j = rem ? q - rem : (Yt ? 0 : q);
+            const u64 j = first_hit_sq<ODD>(Ct, Cd, p * p);
             if (j < S2_T) red_or(sbase + ((u32)j & ~3u), 0x80u << (((u32)j & 3) * 8));
           }
         }
@@ -500,7 +522,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
     }
     // 3. classify (warp w: words [w*1024, (w+1)*1024), lane l: 4 words per step)
     {
-      const bool uniform = Yt >= S2_T;
+      const bool uniform = Yt >= SPAN;  // the tile's y lie in one binade
       const int thr_t = 62 - __clzll((long long)(Yt | 1));
       const u32 kthr = uniform ? (u32)(127 - thr_t) * 0x01010101u : 0u;
       uint4* st4 = (uint4*)st;
@@ -519,7 +541,8 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
           for (int k = 0; k < 4; k++) {
             u32 mw = 0;
             for (int bb = 0; bb < 4; bb++) {
-              const u64 y = Yt + (u64)(q * 4 + k) * 4 + bb;
+              const u64 cell = (u64)(q * 4 + k) * 4 + bb;
+              const u64 y = Yt + (ODD ? 2 * cell + 1 : cell);
               const int thr = (y ? 63 - __clzll((long long)y) : 0) - 1;
               const int mm = mu_cell((wv[k] >> (8 * bb)) & 0xff, thr);
               s += mm;
@@ -595,16 +618,29 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         for (int k = 0; k < 4; k++) dst[k] = o[k];
       }
     }
-    // 6. captures, tile-relative: Q_t[j] = M(floor(n_t/j)) - M(Yt - 1)
-    for (int t = 0; t < a.n_cap; t++) {
-      const CaptureTarget2& ct = a.caps[t];
-      u64 jhi = Yt ? udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt) : ~0ull;
-      u64 jlo = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt + S2_T) + 1;
-      if (jlo < ct.jq0) jlo = ct.jq0;
-      if (jhi > ct.jq1) jhi = ct.jq1;
+    // 6. captures, tile-relative: Q_t[j] = (prefix at floor(n_t/j)) - (prefix at Yt - 1),
+    //    the prefix being M (full mode) or the odd-y sum (odd mode).  The j range of
+    //    every target on this tile is computed once per tile by one thread each.
+    for (int t0 = 0; t0 < a.n_cap; t0 += S2_MAXCAP) {
+      const int nc = min(a.n_cap - t0, S2_MAXCAP);
+      __syncthreads();
+      if (tid < nc) {
+        const CaptureTarget2& ct = a.caps[t0 + tid];
+        u64 jhi = Yt ? udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt) : ~0ull;
+        u64 jlo = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt + SPAN) + 1;
+        s_cj[0][tid] = jlo < ct.jq0 ? ct.jq0 : jlo;
+        s_cj[1][tid] = jhi > ct.jq1 ? ct.jq1 : jhi;
+      }
+      __syncthreads();
+     for (int t = 0; t < nc; t++) {
+      const CaptureTarget2& ct = a.caps[t0 + t];
+      const u64 jlo = s_cj[0][t], jhi = s_cj[1][t];
       for (u64 j = jlo + tid; j <= jhi; j += S2_NT) {
         const u64 y = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, j);
-        const u32 o = (u32)(y - Yt);
+        // cells with y' <= y: o + 1 (full) or the odd y' in [Yt, y]: (o + 1) / 2 (odd)
+        const u32 ncell = ODD ? (u32)((y - Yt + 1) >> 1) : (u32)(y - Yt + 1);
+        if (ncell == 0) { ct.Q[j - ct.jq0] = 0; continue; }
+        const u32 o = ncell - 1;
         const int c = o >> 5;
         const u32* wp = st + (c << 3);
         int s = 0;
@@ -619,6 +655,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         }
         ct.Q[j - ct.jq0] = csum[c] + s;
       }
+     }
     }
   }
 }
@@ -631,7 +668,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
 __global__ void __launch_bounds__(256) k_s3_finish(const int* __restrict__ tile_sum, u32 ntiles, i64* running,
                                                    const int* __restrict__ bkrel, i64* __restrict__ bk,
                                                    const CaptureTarget2* __restrict__ caps, int n_cap, u64 Y0,
-                                                   unsigned long long* done) {
+                                                   u64 span, unsigned long long* done) {
   __shared__ i64 wred[8];
   __shared__ i64 s_base;
   const u32 t = blockIdx.x;
@@ -650,11 +687,11 @@ __global__ void __launch_bounds__(256) k_s3_finish(const int* __restrict__ tile_
   __syncthreads();
   const i64 base = s_base;
   if (bk && tid < 4) bk[(u64)t * 4 + tid] = base + bkrel[(u64)t * 4 + tid];
-  const u64 Yt = Y0 + (u64)t * S2_T;
+  const u64 Yt = Y0 + (u64)t * span;
   for (int c = 0; c < n_cap; c++) {
     const CaptureTarget2& ct = caps[c];
     u64 jhi = Yt ? udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt) : ~0ull;
-    u64 jlo = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt + S2_T) + 1;
+    u64 jlo = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt + span) + 1;
     if (jlo < ct.jq0) jlo = ct.jq0;
     if (jhi > ct.jq1) jhi = ct.jq1;
     for (u64 j = jlo + tid; j <= jhi; j += blockDim.x) ct.Q[j - ct.jq0] += (int)base;
@@ -674,11 +711,13 @@ __global__ void __launch_bounds__(256) k_s3_finish(const int* __restrict__ tile_
 // ------------------------------------------------------------------ host side
 int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
   Sieve2Args a = g.tile;
+  const bool odd = a.odd != 0;
   if (a.nprod) {
     Bucket2Args b = g.bucket;
     const size_t bs = (((3 * (size_t)b.ntiles + 1 + 3) & ~(size_t)3) + (size_t)b.ntiles * b.bin) * sizeof(u32);
     if (kt) kt->begin(KT_SIEVE_LARGE, st);
-    k_bucket_fill<<<b.nprod_grid, 1024, bs, st>>>(b);
+    if (odd) k_bucket_fill<true><<<b.nprod_grid, 1024, bs, st>>>(b);
+    else k_bucket_fill<false><<<b.nprod_grid, 1024, bs, st>>>(b);
     if (kt) kt->end(st);
     MT_CUDA_CHECK(cudaGetLastError());
   }
@@ -686,12 +725,13 @@ int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
   const size_t smem = S2_T + S2_CH * sizeof(int) + (size_t)(2 * nA + nBp + 2 * nC) * 4 + (size_t)nBp * 2 + 16;
   const u32 grid = (a.ntiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
   if (kt) kt->begin(KT_SIEVE_TILE, st);
-  k_sieve3<<<grid, S2_NT, smem, st>>>(a);
+  if (odd) k_sieve3<true><<<grid, S2_NT, smem, st>>>(a);
+  else k_sieve3<false><<<grid, S2_NT, smem, st>>>(a);
   if (kt) kt->end(st);
   MT_CUDA_CHECK(cudaGetLastError());
   if (kt) kt->begin(KT_OTHER, st);
   k_s3_finish<<<a.ntiles, 256, 0, st>>>(a.tile_sum, a.ntiles, a.running, a.bkrel, a.bk, a.caps, a.n_cap, a.Y0,
-                                        a.tstate);
+                                        odd ? 2ull * S2_T : (u64)S2_T, a.tstate);
   if (kt) kt->end(st);
   MT_CUDA_CHECK(cudaGetLastError());
   return MT_OK;
@@ -731,13 +771,16 @@ uint8_t logp(u64 p) {  // ceil(log2 p) | 1  (sieve.py:111-121)
   for (u64 x = p - 1; x; x >>= 1) bl++;
   return (uint8_t)(bl | 1);
 }
-// byte pattern of period P replicated over 4P + T bytes, as words
-std::vector<uint32_t> pattern_words(u64 P, const std::vector<u32>& logp_primes, const std::vector<u32>& sq) {
+// byte pattern of period P replicated over 4P + T bytes, as words.  Full mode:
+// cell j is y = j (multiples of p at j == 0 mod p); odd mode: cell j is
+// y = 2j + 1 (odd multiples of p at j == (p-1)/2 mod p)
+std::vector<uint32_t> pattern_words(u64 P, const std::vector<u32>& logp_primes, const std::vector<u32>& sq,
+                                    bool odd = false) {
   std::vector<uint8_t> one(P, 0);
   for (u32 p : logp_primes)
-    for (u64 j = 0; j < P; j += p) one[j] = (uint8_t)(one[j] + logp(p));
+    for (u64 j = odd ? p / 2 : 0; j < P; j += p) one[j] = (uint8_t)(one[j] + logp(p));
   for (u32 q : sq)
-    for (u64 j = 0; j < P; j += q) one[j] |= 0x80;
+    for (u64 j = odd ? q / 2 : 0; j < P; j += q) one[j] |= 0x80;
   const u64 nbytes = 4 * P + S2_T;
   std::vector<uint32_t> w(nbytes / 4);
   for (u64 i = 0; i < nbytes / 4; i++) {
@@ -750,9 +793,10 @@ std::vector<uint32_t> pattern_words(u64 P, const std::vector<u32>& logp_primes, 
 }  // namespace
 
 struct Sieve2Host {
-  Buf w1, w2, prm, rp, lg, buf, counts, tstate, ovf, tsum, tbase, bkrel;
+  Buf w1, w2, w1o, w2o, prm, rp, lg, buf, counts, tstate, ovf, tsum, tbase, bkrel;
   int nsm = 148;
   u64 P1 = 485100, P2 = 96577;  // 2^2 3^2 5^2 7^2 11, 13 17 19 23
+  u64 P1o = 121275;             // odd cells: 3^2 5^2 7^2 11 (P2 serves both modes)
   std::vector<u32> p;
   u32 nprod = 0, cap = 0, max_tiles = 0;
   u32 fill_smem = 0;  // dynamic shared memory available to k_bucket_fill
@@ -762,6 +806,7 @@ struct Sieve2Host {
   u32 kp = 0, kq = 0, P_lo = 0, Q_lo = 0;
   u32 big_min = S2_T / 2;  // primes above this go to the bucket lists (2^16: measured 1.2 % better than 2^17 at 1e19)
   uint64_t overflows_host = 0;
+  uint64_t launches = 0;  // kernels launched by mt_sieve2_run (fill + tile + finish per segment)
 };
 
 int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cudaStream_t st) {
@@ -795,6 +840,8 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
   };
   if (up(h->w1, pattern_words(h->P1, {2, 3, 5, 7, 11}, {4, 9, 25, 49}))) return MT_ERR_RESOURCE;
   if (up(h->w2, pattern_words(h->P2, {13, 17, 19, 23}, {}))) return MT_ERR_RESOURCE;
+  if (up(h->w1o, pattern_words(h->P1o, {3, 5, 7, 11}, {9, 25, 49}, true))) return MT_ERR_RESOURCE;
+  if (up(h->w2o, pattern_words(h->P2, {13, 17, 19, 23}, {}, true))) return MT_ERR_RESOURCE;
   if (const char* e = getenv("MT_S2_BIG_LOG2")) h->big_min = 1u << atoi(e);
   // bucket space: producers = SMs; capacity from the expected hits per (producer, tile)
   int dev, nsm;
@@ -846,13 +893,17 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
   {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa;
-    MT_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_sieve3));
-    MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       optin - (int)fa.sharedSizeBytes));
-    MT_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_bucket_fill));
-    h->fill_smem = (u32)(optin - (int)fa.sharedSizeBytes);
-    MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fill_smem));
+    cudaFuncAttributes fa, fb;
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_sieve3<false>));
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&fb, k_sieve3<true>));
+    const int s3 = optin - (int)std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s3));
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s3));
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_bucket_fill<false>));
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&fb, k_bucket_fill<true>));
+    h->fill_smem = (u32)(optin - (int)std::max(fa.sharedSizeBytes, fb.sharedSizeBytes));
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fill_smem));
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fill_smem));
   }
   if (max_tiles > 16384) { mt_set_error("too many tiles per segment (max 2^31 cells)"); return MT_ERR_VALUE; }
   MT_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -869,10 +920,12 @@ uint64_t mt_sieve2_overflows(Sieve2Host* h) {
 
 int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running, int8_t* mu_out,
                   int16_t* m16_out, int64_t* bk, uint8_t* states_out, const CaptureTarget2* caps,
-                  int n_cap, cudaStream_t st, KTimer* kt) {
+                  int n_cap, cudaStream_t st, KTimer* kt, bool odd) {
   if (ntiles == 0) return MT_OK;
-  if (ntiles > h->max_tiles || (Y0 % S2_T)) { mt_set_error("bad sieve segment"); return MT_ERR_VALUE; }
-  const u64 y2 = Y0 + (u64)ntiles * S2_T - 1;
+  const u64 span = odd ? 2ull * S2_T : (u64)S2_T;
+  if (ntiles > h->max_tiles || (Y0 % span)) { mt_set_error("bad sieve segment"); return MT_ERR_VALUE; }
+  if (odd && (m16_out || bk || Y0 < span)) { mt_set_error("odd-cell segments give mu and sums only (y >= 2^18)"); return MT_ERR_VALUE; }
+  const u64 y2 = Y0 + (u64)ntiles * span - 1;
   const std::vector<u32>& p = h->p;
   const u64 s = isqrt64(y2);  // p <= floor(sqrt(y2))  <=>  p*p <= y2
   auto idx_gt = [&](u64 v) { return (u32)(std::upper_bound(p.begin(), p.end(), (u32)std::min<u64>(v, 0xFFFFFFFFull)) - p.begin()); };
@@ -884,10 +937,11 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
   a.tstate = (unsigned long long*)h->tstate.p;
   a.ticket = (uint32_t*)((unsigned long long*)h->tstate.p + ntiles);
   a.running = running;
-  a.w1 = (const u32*)h->w1.p; a.w2 = (const u32*)h->w2.p;
-  a.w1_period4 = 4 * h->P1; a.w2_period4 = 4 * h->P2;
+  a.odd = odd ? 1u : 0u;
+  a.w1 = (const u32*)(odd ? h->w1o.p : h->w1.p); a.w2 = (const u32*)(odd ? h->w2o.p : h->w2.p);
+  a.w1_period4 = 4 * (odd ? h->P1o : h->P1); a.w2_period4 = 4 * h->P2;
   a.primes = (const u32*)h->prm.p; a.rprimes = (const double*)h->rp.p; a.logs = (const uint8_t*)h->lg.p;
-  a.p_first = std::min(idx_gt(28), end);  // A primes start at 29 (2..23 are presieved)
+  a.p_first = std::min(idx_gt(28), end);  // A primes start at 29 (2..23 are presieved; odd mode: 3..23)
   a.p_warp_end = std::max(a.p_first, std::min(idx_gt(S2_A_MAX - 1), end));
   a.p_small_end = std::max(a.p_warp_end, std::min(idx_gt(h->big_min), end));
   a.p_b2 = std::max(a.p_warp_end, std::min(idx_gt(S2_B2_MIN - 1), a.p_small_end));
@@ -922,5 +976,12 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
     return MT_ERR_VALUE;
   }
   b.buf = (u32*)h->buf.p; b.counts = (u32*)h->counts.p;
+  h->launches += (a.nprod ? 1 : 0) + 2;
   return mt_sieve2_segment(g, st, kt);
+}
+
+uint64_t mt_sieve2_launches(Sieve2Host* h, bool reset) {
+  const uint64_t n = h->launches;
+  if (reset) h->launches = 0;
+  return n;
 }

@@ -24,6 +24,9 @@
 #include "mt_common.cuh"
 #include "mt_internal.h"
 
+#include <algorithm>
+#include <vector>
+
 #define IPT 32  // items per lane per work chunk
 
 struct UpdateCtx {
@@ -34,6 +37,7 @@ struct UpdateCtx {
   const uint8_t* tile_vbits_max;
   uint64_t ntiles;
   TargetDev* tgts;  // device
+  std::vector<TargetDev> tgts_h;  // host copy (windows are set per Q-gather pass)
   int ntgt;
   // scratch
   uint64_t* units;   // [ntiles+1]
@@ -706,7 +710,11 @@ __global__ void k_qgather_plan(ElemDev E, const TargetDev* __restrict__ tgts, u6
   u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (e > E.n) return;
   if (e == E.n) { cnt[e] = 0; return; }
-  const u64 k = E.k[e], jq0 = tgts[E.tgt[e]].jq0;
+  const TargetDev& tg = tgts[E.tgt[e]];
+  const u64 k = E.k[e], jq0 = tg.jq0;
+  if (r0 < tg.wlo) r0 = tg.wlo;  // this pass's window of the target's table
+  if (r1 > tg.whi) r1 = tg.whi;
+  if (r0 >= r1) { cnt[e] = 0; dtop[e] = 0; return; }
   u64 hi = E.dq_hi[e], lo = E.lo[e];
   const u64 dl = (jq0 + r0 + k - 1) / k, dh = (jq0 + r1 - 1) / k;
   if (dl > lo) lo = dl;
@@ -724,7 +732,7 @@ static int scan_u64(UpdateCtx* c, const uint64_t* in, uint64_t* out, uint64_t n,
     c->cub_bytes = need;
   }
   MT_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, need, in, out, (int64_t)n, st));
-  c->launches += 1;
+  c->launches += 2;  // cub: tile-state init kernel + scan kernel
   return MT_OK;
 }
 
@@ -742,6 +750,7 @@ int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* 
   c->launches = 0;
   *out = c;
   MT_CUDA_CHECK(cudaMalloc(&c->tgts, sizeof(TargetDev) * (ntgt ? ntgt : 1)));
+  c->tgts_h.assign(tgts, tgts + ntgt);
   MT_CUDA_CHECK(cudaMemcpyAsync(c->tgts, tgts, sizeof(TargetDev) * ntgt, cudaMemcpyHostToDevice, st));
   MT_CUDA_CHECK(cudaMalloc(&c->units, sizeof(uint64_t) * (ntiles + 1) * 2));
   MT_CUDA_CHECK(cudaMalloc(&c->cnt, sizeof(uint64_t) * (E.n + 1)));
@@ -770,6 +779,7 @@ void mt_update_destroy(UpdateCtx* c) {
 }
 
 uint64_t mt_update_launches(UpdateCtx* c) { return c->launches; }
+void mt_update_reset_launches(UpdateCtx* c) { c->launches = 0; }
 
 int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const int16_t* M16,
                            const int64_t* bk, cudaStream_t st) {
@@ -829,18 +839,27 @@ int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const 
 // element.  Blocking the table index into L2-sized ranges and running every
 // element's items of one block before the next keeps the block in L2, so the
 // table is read from HBM about once (1e19: 1.78 TB of DRAM reads unblocked).
-int mt_update_qgather(UpdateCtx* c, u64 qmax, cudaStream_t st) {
+int mt_update_qgather(UpdateCtx* c, const uint64_t* wlo, const uint64_t* whi, bool interleave, cudaStream_t st) {
   const ElemDev& E = c->E;
   u64 B = 1ull << 24;  // 64 MB of int32 table per block
   if (const char* ev = getenv("MT_QBLOCK_LOG2")) B = 1ull << atoi(ev);
-  const u64 nb = qmax ? (qmax + B - 1) / B : 0;
-  for (u64 b = 0; b < nb; b++) {
+  u64 lo = ~0ull, hi = 0;
+  for (int t = 0; t < c->ntgt; t++) {
+    c->tgts_h[t].wlo = wlo[t];
+    c->tgts_h[t].whi = whi[t];
+    if (whi[t] > wlo[t]) { lo = std::min<u64>(lo, wlo[t]); hi = std::max<u64>(hi, whi[t]); }
+  }
+  if (hi == 0) return MT_OK;
+  MT_CUDA_CHECK(cudaMemcpyAsync(c->tgts, c->tgts_h.data(), sizeof(TargetDev) * c->ntgt, cudaMemcpyHostToDevice, st));
+  MT_CUDA_CHECK(cudaStreamSynchronize(st));  // tgts_h may change before the copy would run
+  const u32 rank = interleave ? c->sh.rank : 0u, world = interleave ? c->sh.world : 1u;
+  for (u64 b = lo / B; b * B < hi; b++) {
     k_qgather_plan<<<(unsigned)((E.n + 1 + 255) / 256), 256, 0, st>>>(E, c->tgts, b * B, (b + 1) * B, c->qcnt, c->dtop);
     c->launches++;
     int rc = scan_u64(c, c->qcnt, c->qoff, E.n + 1, st);
     if (rc) return rc;
     MT_CUDA_CHECK(cudaMemsetAsync(c->counter + 3, 0, sizeof(uint64_t), st));
-    QArgs a{E, c->acc, c->qoff, c->dtop, E.n, c->counter + 3, c->tgts, c->sh.rank, c->sh.world};
+    QArgs a{E, c->acc, c->qoff, c->dtop, E.n, c->counter + 3, c->tgts, rank, world};
     c->kt->begin(KT_QGATHER, st);
     k_qitems<<<c->nsm * 8, 256, 0, st>>>(a);
     c->kt->end(st);
@@ -874,7 +893,8 @@ __global__ void k_fin_level(const uint64_t* __restrict__ acc, const uint64_t* __
   if (lane == 0) fin[k - 1] = (int64_t)(1ull - acc[k - 1] - s);
 }
 
-int mt_finalize_dev(const uint64_t* acc, const uint64_t* D, uint64_t K, int64_t* fin, cudaStream_t st) {
+int mt_finalize_dev(const uint64_t* acc, const uint64_t* D, uint64_t K, int64_t* fin, cudaStream_t st,
+                    uint64_t* launches) {
   if (K == 0) return MT_OK;
   u64 khi = K;
   while (khi > 0) {
@@ -883,6 +903,7 @@ int mt_finalize_dev(const uint64_t* acc, const uint64_t* D, uint64_t K, int64_t*
     u64 threads = n * 32;
     k_fin_level<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(acc, D, fin, klo, khi);
     MT_CUDA_CHECK(cudaGetLastError());
+    if (launches) ++*launches;
     khi = klo;
   }
   return MT_OK;

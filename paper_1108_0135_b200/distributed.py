@@ -2,23 +2,30 @@
 (NCCL over NVLink/NVSwitch on the box; gloo in the CPU tests).
 
 The reference is single-process; the y-axis split is new work
-(SURVEY.md §8(e)).  The engine plan (include/mertens_sm100.h, "plan API") runs
-the job in four device phases; this module performs the three exchanges
-between them, and nothing else:
+(DESIGN.md §5).  The engine plan (include/mertens_sm100.h,
+"plan API") runs the job in four device phases; this module performs the
+exchanges between them, and nothing else:
 
+  0. fingerprint   all ranks must run the same job: an all_gather of a job
+                   fingerprint (targets, u, captures, flags) -> ContractViolationError
+                   on any mismatch, before any device work
   1. sieve_update  every rank sieves the head [0, Y_H) redundantly, takes every
-                   w-th work unit of the head update, and sieves its own
-                   contiguous share of the tail segments with a LOCAL prefix.
-     -> all_gather of the G tail totals T_h (int64, G values):
+                   w-th work unit of the head update, and sieves the odd y of
+                   its own tail range [a_r, b_r) and of its half [a_r/2, b_r/2)
+                   with a LOCAL prefix (M(x) = O(x) - O(x/2), O = odd-y sum).
+     -> all_gather of the G range totals T_h (int64, G values):
         offset_r = M(Y_H - 1) + sum_{h<r} T_h          (the deferred M offset)
-  2. tail_offset   Q[j] += offset_r on the quotient-table slice whose
-                   quotients floor(n/j) fall in rank r's tail.
-     -> broadcast of every rank's Q slice (int32, contiguous in j) so that each
-        rank holds the complete table M(floor(n/j)).
-  3. gather        every w-th chunk of the dense items k*d <= J from Q; rank 0
-                   adds the summation-by-parts term -M(mcut)*xcut.
+  2. tail_offset   Q[j] = M(floor(n/j)) on the quotient-table slice whose
+                   quotients fall in rank r's range.
+     -> only when quotient captures were requested: sum-reduction of the
+        capture window (each rank holds its own entries, zeros elsewhere), so
+        the M(floor(n/c)) outputs are complete on every rank
+  3. gather        the dense items k*d <= J whose table entry is in rank r's own
+                   slice, plus every w-th chunk of those in the replicated head
+                   part; rank 0 adds the summation-by-parts term -M(mcut)*xcut.
      -> all_reduce(sum) of the K-entry accumulator (int64 two's complement ==
-        the engine's mod-2^64 arithmetic).
+        the engine's mod-2^64 arithmetic).  This is the
+        only bulk collective of the job.
   4. resolve       level-parallel finalize on every rank; rank 0's outputs are
                    the job's outputs.
 
@@ -29,8 +36,6 @@ which rank adds which term of the same mod-2^64 sums.
 from __future__ import annotations
 
 import ctypes
-
-import numpy as np
 
 from . import _lib
 
@@ -77,6 +82,7 @@ class DevicePlan:
         _lib.check(self.L.mt_plan_create(ctypes.byref(job), ctypes.byref(self.h)))
         self.device = torch.device("cuda", torch.cuda.current_device() if job.device < 0 else job.device)
         self.n_targets = job.n_targets
+        self._fp = job_fingerprint(job)
 
     def sieve_update(self):
         mh, tt = ctypes.c_int64(), ctypes.c_int64()
@@ -85,6 +91,14 @@ class DevicePlan:
 
     def tail_offset(self, off: int):
         _lib.check(self.L.mt_plan_tail_offset(self.h, int(off)))
+
+    def fingerprint(self):
+        return self._fp
+
+    def cap_window(self):
+        p, c = ctypes.c_void_p(), ctypes.c_uint64()
+        _lib.check(self.L.mt_plan_cap_window(self.h, ctypes.byref(p), ctypes.byref(c)))
+        return _device_view(p.value, c.value, "<i4", self.device) if c.value else None
 
     def q_slice(self, target: int, rank: int):
         p, c = ctypes.c_void_p(), ctypes.c_uint64()
@@ -142,8 +156,37 @@ def _staged(t, fn, group):
         fn(t)
 
 
-def run_phases(plan, group=None, res=None):
-    """Drive one job through the plan's phases with the three exchanges.
+def job_fingerprint(job) -> list[int]:
+    """Eight int64 words that every rank of one sharded job must agree on."""
+    import hashlib
+
+    ns = [(int(job.n_hi[i]) << 64) | int(job.n_lo[i]) for i in range(job.n_targets)]
+    h = hashlib.sha256(",".join(map(str, ns)).encode()).digest()
+    words = [int.from_bytes(h[:7], "little"), int(job.u), int(job.n_targets), int(job.cap_c_lo), int(job.cap_c_hi),
+             int(job.cap_small), int(job.flags) & ~_lib.MT_FLAG_TIMING,
+             (int(job.seg_log2_head) << 32) | (int(job.seg_log2_tail) << 16) | int(job.shard_world)]
+    return [w & ((1 << 63) - 1) for w in words]
+
+
+def check_same_job(plan, group=None, device=None):
+    """All ranks must run the same job; a mismatch (e.g. every rank computing a
+    different n under torchrun) raises ContractViolationError on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    from .errors import ContractViolationError
+
+    size = dist.get_world_size(group)
+    fp = torch.tensor(plan.fingerprint(), dtype=torch.int64, device=device)
+    allfp = [torch.zeros_like(fp) for _ in range(size)]
+    dist.all_gather(allfp, fp, group=group)
+    if any(not torch.equal(a, allfp[0]) for a in allfp):
+        raise ContractViolationError("ranks of the process group run different exact jobs "
+                                     "(set EngineConfig(distributed=False) for independent per-rank jobs)")
+
+
+def run_phases(plan, group=None, res=None, verify=True):
+    """Drive one job through the plan's phases with the exchanges.
     `plan` is a DevicePlan (or the CPU stand-in of the tests) of THIS rank."""
     import torch
     import torch.distributed as dist
@@ -151,18 +194,18 @@ def run_phases(plan, group=None, res=None):
     rank, size = dist.get_rank(group), dist.get_world_size(group)
     gloo = dist.get_backend(group) == "gloo"
     dev = torch.device("cpu") if gloo else getattr(plan, "device", torch.device("cpu"))
+    if verify:
+        check_same_job(plan, group, dev)
     m_head, t_local = plan.sieve_update()
     tot = torch.tensor([t_local], dtype=torch.int64, device=dev)
     allt = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(size)]
     dist.all_gather(allt, tot, group=group)
     offs = tail_offsets(m_head, [int(t.item()) for t in allt])
     plan.tail_offset(offs[rank])
-    for t in range(plan.n_targets):
-        for r in range(size):
-            view = plan.q_slice(t, r)
-            if view is not None:
-                src = dist.get_global_rank(group, r) if group is not None else r
-                _staged(view, lambda x: dist.broadcast(x, src=src, group=group), group)
+    win = plan.cap_window()
+    if win is not None:
+        plan.sync()
+        _staged(win, lambda x: dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group), group)
     plan.sync()
     plan.gather()
     acc = plan.acc()

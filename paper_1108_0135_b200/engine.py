@@ -85,7 +85,10 @@ class EngineConfig:
     seg_log2_head: int = 0
     seg_log2_tail: int = 0
     engine_flags: int = 0          # MT_FLAG_FORCE_WIDE / _FORCE_SLOWDIV (tests), MT_FLAG_TIMING
-    distributed: bool = True       # shard over the default torch.distributed group when one is up
+    # shard ONE job over the default torch.distributed group (every rank must call
+    # with the same arguments; a job fingerprint is checked).  Off by default: under
+    # torchrun each rank then computes its own requests independently.
+    distributed: bool = False
     stream: int | None = None      # cudaStream_t (int) to run on; None: the engine's own
     checkpoint_seconds: float = 300.0  # with checkpoint_path: after the head, then at most this often
 
@@ -261,28 +264,42 @@ def make_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, rank=0, world
     return job
 
 
+def rank_checkpoint_path(path: str, rank: int, world: int) -> str:
+    """One checkpoint file per rank of a sharded job (the single-rank name is `path`)."""
+    return path if world <= 1 else f"{path}.r{rank}of{world}"
+
+
+def _sieve_checkpointed(L, h, config: EngineConfig, path: str | None, restore_from=None):
+    """Phase 1 of a plan in steps, checkpointed after the head and then at most
+    every `checkpoint_seconds` between tail segments (the reference writes after
+    every block, engine.py:391-392; at GPU rates that would be I/O bound).
+    Returns (M(head_end - 1), this rank's tail total)."""
+    import ctypes
+
+    if restore_from:
+        _lib.check(L.mt_plan_restore(h, restore_from.encode()))
+    done, mh, tt = ctypes.c_int(0), ctypes.c_int64(), ctypes.c_int64()
+    last = time.perf_counter()
+    first = not restore_from
+    bpath = (path or "").encode()
+    while not done.value:
+        _lib.check(L.mt_plan_sieve_step(h, 256, ctypes.byref(done), ctypes.byref(mh), ctypes.byref(tt)))
+        now = time.perf_counter()
+        if bpath and not done.value and (first or now - last >= config.checkpoint_seconds):
+            _lib.check(L.mt_plan_checkpoint(h, bpath))
+            last, first = now, False
+    return mh.value, tt.value
+
+
 def _run_checkpointed(L, job, res, config: EngineConfig, restore_from=None):
-    """Single-target job on the plan API, checkpointed after the head and then at
-    most every `checkpoint_seconds` between tail segments (the reference writes
-    after every block, engine.py:391-392; at GPU rates that would be I/O bound)."""
+    """Single-target, single-rank job on the plan API with checkpoints."""
     import ctypes
 
     h = ctypes.c_void_p()
     _lib.check(L.mt_plan_create(ctypes.byref(job), ctypes.byref(h)))
     try:
-        path = (config.checkpoint_path or "").encode()
-        if restore_from:
-            _lib.check(L.mt_plan_restore(h, restore_from.encode()))
-        done, mh, tt = ctypes.c_int(0), ctypes.c_int64(), ctypes.c_int64()
-        last = time.perf_counter()
-        first = not restore_from
-        while not done.value:
-            _lib.check(L.mt_plan_sieve_step(h, 256, ctypes.byref(done), ctypes.byref(mh), ctypes.byref(tt)))
-            now = time.perf_counter()
-            if path and not done.value and (first or now - last >= config.checkpoint_seconds):
-                _lib.check(L.mt_plan_checkpoint(h, path))
-                last, first = now, False
-        _lib.check(L.mt_plan_tail_offset(h, mh.value))
+        mh, _ = _sieve_checkpointed(L, h, config, config.checkpoint_path, restore_from)
+        _lib.check(L.mt_plan_tail_offset(h, mh))
         _lib.check(L.mt_plan_gather(h))
         _lib.check(L.mt_plan_resolve(h, ctypes.byref(res)))
     finally:
@@ -314,13 +331,20 @@ def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None,
         res.small_m_out = small_m.ctypes.data_as(_lib._pi64)
     if acc_out is not None:
         res.acc_out = acc_out.ctypes.data_as(_lib._pu64)
+    ckpt = bool(config.checkpoint_path or restore_from)
+    if ckpt and len(ns) != 1:  # the reference refuses multi-target checkpoints too (engine.py:664-665)
+        raise ContractViolationError("checkpoint/resume covers single-target jobs only")
     if world > 1:
         plan = distributed.DevicePlan(job)
         try:
+            if ckpt:
+                path = config.checkpoint_path and rank_checkpoint_path(config.checkpoint_path, rank, world)
+                rfrom = restore_from and rank_checkpoint_path(restore_from, rank, world)
+                plan.sieve_update = lambda: _sieve_checkpointed(L, plan.h, config, path, rfrom)
             distributed.run_phases(plan, None, res)
         finally:
             plan.close()
-    elif (config.checkpoint_path or restore_from) and len(ns) == 1:
+    elif ckpt:
         _run_checkpointed(L, job, res, config, restore_from)
     else:
         _lib.check(L.mt_run(job, res))
@@ -512,17 +536,25 @@ _CKPT_HEAD = struct.Struct("<8sII QQ Q Q Q q Q")  # engine.py:659
 
 def resume_exact(path: str, config: EngineConfig | None = None) -> MertensResult:
     """Continue a checkpointed run to completion (engine.py:731-741).  The file
-    carries the reference's MERTCKP1 header (version 2: this engine's state
-    follows it); u must match the one `config` derives (engine.py:697-698)."""
+    carries the reference's MERTCKP1 header (version 3: this engine's state
+    follows it); u must match the one `config` derives (engine.py:697-698).
+    A sharded job (config.distributed under a process group) resumes from the
+    per-rank files `path.r{rank}of{world}`."""
     config = config or EngineConfig()
-    with open(path, "rb") as f:
+    from . import distributed
+
+    rank, world = distributed.world() if config.distributed else (0, 1)
+    with open(rank_checkpoint_path(path, rank, world), "rb") as f:
         head = f.read(_CKPT_HEAD.size)
     if len(head) != _CKPT_HEAD.size:
         raise ContractViolationError("not a checkpoint file")
-    magic, version, _flags, n_lo, n_hi, u, _next_y1, _K, _m_running, _bl = _CKPT_HEAD.unpack(head)
-    if magic != b"MERTCKP1" or version != 2:
+    magic, version, flags, n_lo, n_hi, u, _next_y1, _K, _m_running, _bl = _CKPT_HEAD.unpack(head)
+    if magic != b"MERTCKP1" or version != 3:
         raise ContractViolationError("not an sm100 checkpoint file")
     n = (n_hi << 64) | n_lo
     if choose_u(n, 1, config.mem_budget, config.u_alpha) != u:
         raise ContractViolationError(f"checkpoint built with u={u}, config derives another u")
+    if flags != (rank | (world << 16)):
+        raise ContractViolationError(f"checkpoint written by rank {flags & 0xFFFF} of {flags >> 16}, "
+                                     f"this is rank {rank} of {world}")
     return _mertens_exact(n, config, restore_from=path)

@@ -4,14 +4,20 @@ real multi-rank driver (paper_1108_0135_b200/distributed.run_phases) and the
 sharding algebra can be exercised with world_size > 1 over gloo on CPU.
 
 It restates the device plan's decomposition (mt_engine.cu plan_setup /
-mt_plan_*; DESIGN.md §5):
+mt_plan_*; DESIGN.md §2.4, §5):
   acc_k = sum_{m<=mcut} mu(m) floor(v/m) - M(mcut) xcut        counted walk
         + sum_{d=lo_w}^{xcut} M(floor(v/d))                    windowed dense walk (head)
         + sum_{d=lo}^{dq_hi} Q[k d]                            Q-gather (any y)
-with Q[j] = M(floor(n/j)) captured while sieving; the head [0, Y_H) is sieved
-by every rank, the tail segments are split contiguously and prefixed locally.
-Work units are dealt to ranks by element index (the device deals them by
-work-unit index; either partition yields the same sums).
+with Q[j] = M(floor(n/j)).  The head [0, Y_H) is sieved by every rank and
+captures Q directly.  The tail [Y_H, E) is split into w ranges [a, b)
+balanced by sieve work (tail_partition); rank r sieves only the odd y of
+[a/2, b/2) U [a, b) with one running prefix P (P(a/2 - 1) = 0) and captures
+P at floor(n/j) and floor(n/(2j)) for its own slice j; then
+  M(floor(n/j)) = P(floor(n/j)) - P(floor(n/(2j))) - P(a - 1) + M(a - 1),
+because M(x) = O(x) - O(floor(x/2)) with O the odd-y Moebius sum.
+The Q-gather of rank r reads only its own slice and every w-th element's
+items in the head part.  Work units are dealt to ranks by element index (the
+device deals them by work-unit index; either partition yields the same sums).
 """
 
 from __future__ import annotations
@@ -22,10 +28,55 @@ import torch
 from oracle import engine_port as E
 
 
+def tail_cost(a, b):
+    """mt_engine.cu tail_cost: y covered by a rank owning [a, b)."""
+    if b <= a:
+        return 0
+    h0, h1 = a // 2, b // 2
+    c = (b - a) + (h1 - h0)
+    if h1 > a:
+        c -= h1 - a
+    return c
+
+
+def tail_partition(H, E_, w, align):
+    """mt_engine.cu tail_partition: boundaries on `align` balancing tail_cost."""
+    yb = [H] + [E_] * w
+    if w <= 1 or E_ <= H:
+        return yb
+
+    def cover(c, out=None):
+        a = H
+        for r in range(w - 1):
+            lo, hi = 0, (E_ - a) // align
+            while lo < hi:
+                mid = (lo + hi + 1) // 2
+                if tail_cost(a, a + mid * align) <= c:
+                    lo = mid
+                else:
+                    hi = mid - 1
+            a += lo * align
+            if out is not None:
+                out[r + 1] = a
+        return tail_cost(a, E_) <= c
+
+    lo, hi = 0, tail_cost(H, E_)
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if cover(mid):
+            hi = mid
+        else:
+            lo = mid + 1
+    cover(lo, yb)
+    yb[w] = E_
+    return yb
+
+
 class ShardedOraclePlan:
     device = torch.device("cpu")
+    SENTINEL = -(1 << 30)
 
-    def __init__(self, ns, u, rank, world, Rh=1 << 12, Rt=1 << 14):
+    def __init__(self, ns, u, rank, world, Rh=1 << 12, align=1 << 10, capture=False):
         self.ns, self.u, self.rank, self.world = list(ns), u, rank, world
         self.n_targets = len(self.ns)
         self.H = [E.HarmonicArray(n, u) for n in self.ns]
@@ -47,33 +98,58 @@ class ShardedOraclePlan:
             if act.any():
                 head_end = max(head_end, int((h.v[act] // lw[act]).max()))
         head_end = min(head_end, u)
-        self.Rh, self.Rt = Rh, Rt
-        self.head_lim = -(-(head_end + 1) // Rh) * Rh
-        self.tail_segs = max(0, -(-(u + 1 - self.head_lim) // Rt))
-        self.y_last = self.head_lim + self.tail_segs * Rt - 1
+        segs = -(-(head_end + 1) // Rh)
+        while (segs * Rh) % align:
+            segs += 1
+        self.head_lim = segs * Rh
+        self.tail_end = -(-(u + 1) // align) * align if u + 1 > self.head_lim else self.head_lim
+        self.ybound = tail_partition(self.head_lim, self.tail_end, world, align)
+        self.a, self.b = self.ybound[rank], self.ybound[rank + 1]
+        self.tail_segs = sum(1 for r in range(world) if self.ybound[r + 1] > self.ybound[r])
+        self.y_last = max(self.tail_end, self.head_lim) - 1
         self.M = E.mertens_table(self.y_last)  # M[y-1] = M(y)
-        self.Q = [np.full(max(0, self.J[t] - self.jq0[t] + 1), -(1 << 30), np.int32) for t in range(self.n_targets)]
+        mu = np.diff(np.concatenate([[0], self.M]))
+        odd = np.arange(1, self.y_last + 1) % 2 == 1
+        self.O = np.cumsum(np.where(odd, mu, 0))  # O[y-1] = sum of mu over odd y' <= y
+        self.Q = [np.full(max(0, self.J[t] - self.jq0[t] + 1), self.SENTINEL, np.int64) for t in range(self.n_targets)]
+        self.P2 = [None] * self.n_targets
         self._acc = [np.zeros(h.size, np.uint64) for h in self.H]
+        self.capture = capture
 
     def Mof(self, y):
         y = np.asarray(y, dtype=np.int64)
         return np.where(y >= 1, self.M[np.maximum(y, 1) - 1], 0)
 
-    def _tail_y(self, s):
-        return self.head_lim + s * self.Rt
+    def Oof(self, y):
+        y = np.asarray(y, dtype=np.int64)
+        return np.where(y >= 1, self.O[np.maximum(y, 1) - 1], 0)
+
+    def Pof(self, x):
+        """This rank's running odd prefix P(x) over [a/2, b/2) U [a, b), P(a/2 - 1) = 0."""
+        a, b = self.a, self.b
+        h0, h1 = a // 2, b // 2
+        x = np.asarray(x, dtype=np.int64)
+        base = self.Oof(h0 - 1)
+        if h1 > a:  # union [a/2, b): one continuous stretch
+            return self.Oof(np.minimum(x, b - 1)) - base
+        # disjoint: [a/2, b/2) then [a, b) with the gap skipped
+        p = self.Oof(np.minimum(x, h1 - 1)) - base
+        return p + np.where(x >= a, self.Oof(np.minimum(x, b - 1)) - self.Oof(a - 1), 0)
 
     def _slice(self, t, r):
-        """j range of target t captured in rank r's tail (mt_plan::q_slice)."""
-        s0, s1 = self.tail_segs * r // self.world, self.tail_segs * (r + 1) // self.world
-        if s0 >= s1 or self.J[t] < self.jq0[t]:
+        """j range of target t owned by rank r (mt_plan::q_slice)."""
+        a, b = self.ybound[r], self.ybound[r + 1]
+        if a >= b or self.J[t] < self.jq0[t]:
             return None
-        ya, yb = self._tail_y(s0), self._tail_y(s1) - 1
-        lo = max(self.ns[t] // (yb + 1) + 1, self.jq0[t])
-        hi = min(self.ns[t] // ya, self.J[t])
+        lo = max(self.ns[t] // b + 1, self.jq0[t])
+        hi = min(self.ns[t] // a, self.J[t])
         return (lo, hi) if lo <= hi else None
 
     def _mine(self, size):
         return np.arange(size) % self.world == self.rank
+
+    def fingerprint(self):
+        return [hash(tuple(self.ns)) & ((1 << 62) - 1), self.u, self.n_targets, 0, 0, 0, 0, self.world]
 
     def sieve_update(self):
         n_ = self.ns
@@ -88,29 +164,44 @@ class ShardedOraclePlan:
                 s += int(self.Mof(v // d).sum()) if len(d) else 0
                 acc[i] = np.uint64(s % (1 << 64))
             self._acc[t] = acc
-            # captures: head (absolute) and this rank's tail (local prefix)
             if len(self.Q[t]):
                 j = np.arange(self.jq0[t], self.J[t] + 1, dtype=np.int64)
                 y = n_[t] // j
                 head = y < self.head_lim
-                self.Q[t][head] = self.Mof(y[head])
+                self.Q[t][head] = self.Mof(y[head])  # head captures: absolute M
                 sl = self._slice(t, self.rank)
                 if sl:
-                    s0 = self.tail_segs * self.rank // self.world
-                    base = int(self.Mof(self._tail_y(s0) - 1))
-                    a, b = sl[0] - self.jq0[t], sl[1] - self.jq0[t] + 1
-                    self.Q[t][a:b] = self.Mof(y[a:b]) - base
-        s0 = self.tail_segs * self.rank // self.world
-        s1 = self.tail_segs * (self.rank + 1) // self.world
+                    i0, i1 = sl[0] - self.jq0[t], sl[1] - self.jq0[t] + 1
+                    self.Q[t][i0:i1] = self.Pof(y[i0:i1])        # P(floor(n/j))
+                    self.P2[t] = self.Pof((n_[t] // 2) // j[i0:i1])  # P(floor(n/(2j)))
         m_head = int(self.Mof(self.head_lim - 1))
-        t_local = int(self.Mof(self._tail_y(s1) - 1) - self.Mof(self._tail_y(s0) - 1)) if s1 > s0 else 0
-        return m_head, t_local
+        if self.b <= self.a:
+            self.s_a = 0
+            return m_head, 0
+        self.s_a = int(self.Pof(self.a - 1))
+        s_h = int(self.Pof(self.b // 2 - 1))
+        p_end = int(self.Pof(self.b - 1))
+        return m_head, (p_end - self.s_a) - s_h
 
     def tail_offset(self, off):
         for t in range(self.n_targets):
             sl = self._slice(t, self.rank)
             if sl:
-                self.Q[t][sl[0] - self.jq0[t]:sl[1] - self.jq0[t] + 1] += np.int32(off)
+                i0, i1 = sl[0] - self.jq0[t], sl[1] - self.jq0[t] + 1
+                self.Q[t][i0:i1] = self.Q[t][i0:i1] - self.P2[t] + (int(off) - self.s_a)
+        if self.capture and len(self.Q[0]):  # mask the window to the entries this rank owns
+            j = np.arange(self.jq0[0], self.J[0] + 1, dtype=np.int64)
+            sl = self._slice(0, self.rank)
+            mine = np.zeros(len(j), bool)
+            if sl:
+                mine |= (j >= sl[0]) & (j <= sl[1])
+            if self.rank == 0:
+                mine |= j >= self.ns[0] // self.head_lim + 1
+            self.Q[0][~mine] = 0
+            self._win = torch.from_numpy(self.Q[0].astype(np.int32))
+
+    def cap_window(self):
+        return self._win if self.capture and len(self.Q[0]) else None
 
     def q_slice(self, t, r):
         sl = self._slice(t, r)
@@ -119,17 +210,22 @@ class ShardedOraclePlan:
         return torch.from_numpy(self.Q[t][sl[0] - self.jq0[t]:sl[1] - self.jq0[t] + 1])
 
     def sync(self):
-        pass
+        if self.capture and len(self.Q[0]):
+            self.Q[0] = self._win.numpy().astype(np.int64)
 
     def gather(self):
         for t, h in enumerate(self.H):
-            assert (self.Q[t] != -(1 << 30)).all(), "a quotient-table slice was never filled"
+            sl = self._slice(t, self.rank)
+            jh = self.ns[t] // self.head_lim + 1
             for i in range(h.size):
-                s = 0
-                if i % self.world == self.rank:
-                    k = i + 1
-                    d = np.arange(int(h.lo[i]), int(self.dq[t][i]) + 1, dtype=np.int64)
-                    s = int(self.Q[t][k * d - self.jq0[t]].astype(np.int64).sum()) if len(d) else 0
+                k = i + 1
+                d = np.arange(int(h.lo[i]), int(self.dq[t][i]) + 1, dtype=np.int64)
+                j = k * d
+                own = (j >= sl[0]) & (j <= sl[1]) if sl else np.zeros(len(j), bool)
+                take = own | ((j >= jh) & (i % self.world == self.rank))
+                q = self.Q[t][j[take] - self.jq0[t]]
+                assert (q != self.SENTINEL).all(), "read a quotient-table entry this rank does not own"
+                s = int(q.sum())
                 if self.rank == 0:  # summation-by-parts term, once per element (k_acc_finish)
                     s -= int(self.Mof(int(h.mcut[i]))) * int(h.xcut[i])
                 self._acc[t][i] = np.uint64((int(self._acc[t][i]) + s) % (1 << 64))
@@ -146,3 +242,5 @@ class ShardedOraclePlan:
             out.append(kc.finalize_recursion(np.ascontiguousarray(a), h.D))
             o += h.size
         res["finals"] = out
+        if self.capture and len(self.Q[0]):
+            res["window"] = self.Q[0].copy()

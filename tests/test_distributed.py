@@ -1,6 +1,8 @@
 """CPU (gloo, world_size 2 and 3): the multi-rank driver run_phases with the
-oracle-backed plan stand-in — tail offsets, Q-slice broadcasts and the int64
-all-reduce reproduce the single-process finals bit for bit."""
+oracle-backed plan stand-in — odd-y tail ranges with deferred offsets, the
+capture-window reduction and the int64 all-reduce reproduce the
+single-process finals bit for bit, no rank reads a quotient-table entry it
+does not own, and ranks running different jobs are refused."""
 import os
 import socket
 import time
@@ -21,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, ns, u, q):
+def _worker(rank, world, port, ns, u, q, capture, skew):
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
@@ -33,19 +35,26 @@ def _worker(rank, world, port, ns, u, q):
     try:
         from sharded_oracle import ShardedOraclePlan
 
-        plan = ShardedOraclePlan(ns, u, rank, world)
+        my_ns = [n + (rank if skew else 0) for n in ns]
+        plan = ShardedOraclePlan(my_ns, u, rank, world, capture=capture)
         res = {}
-        offs = D.run_phases(plan, None, res)
-        q.put((rank, [f.tolist() for f in res["finals"]], offs, plan.tail_segs))
+        try:
+            offs = D.run_phases(plan, None, res)
+        except Exception as ex:  # noqa: BLE001 - reported to the parent
+            q.put((rank, type(ex).__name__, str(ex), None, None))
+            return
+        win = res.get("window")
+        q.put((rank, [f.tolist() for f in res["finals"]], offs, plan.ybound,
+               None if win is None else win.tolist()))
     finally:
         dist.destroy_process_group()
 
 
-def _run(ns, u, world):
+def _run(ns, u, world, capture=False, skew=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, ns, u, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, ns, u, q, capture, skew)) for r in range(world)]
     for p in ps:
         p.start()
     out = []
@@ -67,15 +76,52 @@ def test_tail_offsets():
     assert D.tail_offsets(0, []) == []
 
 
+def test_tail_partition_balanced():
+    from sharded_oracle import tail_cost, tail_partition
+
+    H, E, al = 1 << 20, 1 << 30, 1 << 12
+    for w in (1, 2, 3, 8):
+        yb = tail_partition(H, E, w, al)
+        assert yb[0] == H and yb[-1] == E and all(b >= a for a, b in zip(yb, yb[1:]))
+        assert all(y % al == 0 for y in yb)
+        costs = [tail_cost(a, b) for a, b in zip(yb, yb[1:])]
+        assert max(costs) - min(costs) <= 1.5 * al * w, costs
+        # every y of [H, E) is owned by exactly one range; rank r also covers [a/2, b/2)
+        assert sum(b - a for a, b in zip(yb, yb[1:])) == E - H
+    # one rank: the odd cells of [H/2, E), i.e. about half of what a full sieve of [H, E) touches
+    assert tail_cost(H, E) == E - H // 2
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_job_matches_single_process(oracle, world):
     ns = [10**8, 10**8 + 7]
     u = oracle.choose_u(max(ns), len(ns))
     ref = oracle.mertens_exact_multi(ns)
     out = _run(ns, u, world)
-    for rank, finals, offs, tail_segs in out:
-        assert tail_segs >= world  # every rank owns tail segments
+    for rank, finals, offs, ybound, _ in out:
+        assert sum(1 for a, b in zip(ybound, ybound[1:]) if b > a) == world  # every rank owns a tail range
         for n, f in zip(ns, finals):
             assert np.array_equal(np.array(f, np.int64), ref[n].final), (rank, n)
     # the offsets are the same on every rank
     assert len({tuple(o[2]) for o in out}) == 1
+
+
+def test_sharded_capture_window(oracle):
+    """The capture window (the M(floor(n/c)) outputs) is assembled by one sum-reduction."""
+    ns = [10**8 + 3]
+    u = oracle.choose_u(ns[0])
+    out = _run(ns, u, 2, capture=True)
+    from sharded_oracle import ShardedOraclePlan
+
+    p = ShardedOraclePlan(ns, u, 0, 1)
+    j = np.arange(p.jq0[0], p.J[0] + 1, dtype=np.int64)
+    want = p.Mof(ns[0] // j)
+    for rank, finals, _, _, win in out:
+        assert np.array_equal(np.array(win, np.int64), want), rank
+
+
+def test_sharded_job_refuses_mismatched_ranks(oracle):
+    ns = [10**7]
+    u = oracle.choose_u(ns[0])
+    out = _run(ns, u, 2, skew=True)
+    assert all(o[1] == "ContractViolationError" for o in out), out

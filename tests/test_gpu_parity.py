@@ -277,6 +277,36 @@ def test_production_sieve_stress_paths(engine, oracle, monkeypatch, env):
     assert np.array_equal(mu, ref), int((mu != ref).sum())
 
 
+@pytest.mark.parametrize("y1,length", [(1 << 18, 3 << 20), (10**9 - 123457, 3 << 20), (2**32 - 70000, 300001),
+                                       (4_641_588_833_612 - 10**6, 2 * 10**6),
+                                       (82_036_050_574_571 - 10**6, 10**6), (464_158_883_361_277 - 10**6, 10**6)])
+def test_odd_tail_sieve_mu(engine, oracle, y1, length):
+    """The tail's odd-cell sieve (cell c = y 2c + 1: presieve patterns and every
+    prime stream re-phased to (p-1)/2 mod p) gives the reference's mu at every
+    odd y, on ranges up to the 1e22 job's u."""
+    from paper_1108_0135_b200 import _lib
+
+    y2 = y1 + length - 1
+    y0 = y1 | 1
+    mu = np.zeros((y2 - y0) // 2 + 1, np.int8)
+    _lib.check(_lib.lib().mt_sieve_odd(y1, y2, _lib.ptr(mu)))
+    ref = oracle.mu_range(oracle.get_kernels("c"), y0, y2)[::2]
+    assert np.array_equal(mu, ref), int((mu != ref).sum())
+
+
+@pytest.mark.parametrize("env", [{"MT_FILL_BIN": "16"}, {"MT_S2_CAP": "64"}])
+def test_odd_tail_sieve_stress_paths(engine, oracle, monkeypatch, env):
+    from paper_1108_0135_b200 import _lib
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    y1, length = 4_641_588_833_612 - 10**6, 2 * 10**6
+    mu = np.zeros(length // 2, np.int8)
+    _lib.check(_lib.lib().mt_sieve_odd(y1, y1 + length - 1, _lib.ptr(mu)))
+    ref = oracle.mu_range(oracle.get_kernels("c"), y1 | 1, y1 + length - 1)[::2]
+    assert np.array_equal(mu, ref), int((mu != ref).sum())
+
+
 def test_production_sieve_prefix(engine, oracle):
     from paper_1108_0135_b200 import _lib
 
@@ -314,16 +344,21 @@ def _two_rank_worker(rank, world, port, n, q):
         distributed.run_phases(plan, None, res)
         st = _lib.stats_dict(res.stats)
         plan.close()
-        q.put((rank, fin.tolist(), st["tail_seg_begin"], st["tail_seg_end"]))
+        # the public API over the process group: quotient captures assembled by the
+        # capture-window reduction
+        r = P.mertens_exact(n, P.EngineConfig(device=0, seg_log2_head=20, seg_log2_tail=20, distributed=True))
+        q.put((rank, fin.tolist(), st["tail_seg_begin"], st["tail_seg_end"], r.value, r._final.tolist(),
+               r._cp_m.tolist()))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_ranks_on_one_gpu(engine, golden, world):
-    """The multi-GPU path (plan API + run_phases: interleaved head units, split
-    tail, offsets, Q-slice broadcasts, int64 allreduce) with `world` ranks sharing
-    cuda:0 over gloo: finals identical to the single-rank job."""
+    """The multi-GPU path (plan API + run_phases: interleaved head units, odd-y
+    tail ranges, deferred offsets, rank-local Q-gather, int64 allreduce) with
+    `world` ranks sharing cuda:0 over gloo: finals identical to the single-rank
+    job; mertens_exact(distributed=True) also assembles the 4M quotient captures."""
     import socket
     import time
 
@@ -349,10 +384,13 @@ def test_sharded_ranks_on_one_gpu(engine, golden, world):
             assert time.time() - t0 < 600
     for p in ps:
         p.join(timeout=60)
-    segs = sorted((o[2], o[3]) for o in out)
-    assert segs[0][0] == 0 and all(segs[i][1] == segs[i + 1][0] for i in range(world - 1)) and segs[0][1] > 0
-    for rank, fin, _, _ in out:
+    segs = sorted((o[2], o[3]) for o in out)  # tail ranges [ya, yb) tile [head_end, tail_end)
+    assert segs[0][0] > 0 and all(segs[i][1] == segs[i + 1][0] for i in range(world - 1))
+    assert all(a < b for a, b in segs) and segs[-1][1] > ref.u
+    for rank, fin, _, _, val, fin2, cpm in out:
         assert np.array_equal(np.array(fin, np.int64), ref._final), rank
+        assert val == ref.value and np.array_equal(np.array(fin2, np.int64), ref._final), rank
+        assert np.array_equal(np.array(cpm, np.int64), ref._cp_m), rank
 
 
 @pytest.mark.slow
@@ -377,6 +415,43 @@ def test_batch_extreme_1161e19(engine):
     # u-invariance: a different shared sieve (4 targets) gives the same values
     sub = engine.mertens_exact_multi(ns[2:6])
     assert all(sub[n].value == mm[n].value for n in ns[2:6])
+
+
+@pytest.mark.slow
+def test_c3_64_targets_1161e19(engine):
+    """C3 as specified (BASELINE configs[2]): 64 close targets
+    x + j*10^10, j = -32..31, around the paper's extreme, one shared sieve with
+    u = choose_u(max, 64).  j = 0 is pinned to the paper; all 64 values agree with
+    a second shared-sieve layout (two 32-target jobs, each with its own u) and
+    three sampled targets agree with their single-target runs."""
+    import json
+    import os
+    import time
+
+    x = 11609864264058592345
+    ns = [x + j * 10**10 for j in range(-32, 32)]
+    t0 = time.perf_counter()
+    mm = engine.mertens_exact_multi(ns)
+    wall = time.perf_counter() - t0
+    u = engine.choose_u(max(ns), 64)
+    assert u == 82_036_050_574_571 and mm[x].u == u
+    assert mm[x].value == -1995900927
+    assert round(mm[x].ratio, 9) == -0.585767684
+    lo = engine.mertens_exact_multi(ns[:32])
+    hi = engine.mertens_exact_multi(ns[32:])
+    assert lo[ns[0]].u != u
+    for n in ns:
+        assert (lo.get(n) or hi.get(n)).value == mm[n].value, n
+    for n in (ns[0], ns[40], ns[-1]):  # and three single-target runs (u = choose_u(n))
+        assert engine.mertens_exact(n).value == mm[n].value, n
+    out = os.environ.get("MT_RESULTS_DIR")
+    if out:
+        st = mm[x].stats.device
+        json.dump({"ns": [str(n) for n in ns], "u": u, "wall_s": wall,
+                   "values": {str(n): mm[n].value for n in ns},
+                   "kernel_ms": st.get("kernel_ms"), "phases_ms": {k: st[k] for k in (
+                       "ms_update_head", "ms_sieve_tail", "ms_qgather", "ms_finalize", "ms_setup")}},
+                  open(os.path.join(out, "c3_64.json"), "w"), indent=1)
 
 
 def test_dense_full_quotient_map(engine, oracle):
@@ -410,20 +485,20 @@ def test_checkpoint_resume(engine, golden, tmp_path):
 
     n = 10**13
     path = str(tmp_path / "ck.bin")
-    cfg = engine.EngineConfig(checkpoint_path=path, checkpoint_seconds=0.0, seg_log2_tail=20)
+    cfg = engine.EngineConfig(checkpoint_path=path, checkpoint_seconds=0.0, seg_log2_tail=18)
     full = engine.mertens_exact(n, cfg)
     assert full.value == 599582
     head = open(path, "rb").read(72)
     magic, version, flags, n_lo, n_hi, u, next_y1, K, m_running, bl = struct.unpack("<8sII QQ Q Q Q q Q", head)
-    assert (magic, version, n_lo, u, K) == (b"MERTCKP1", 2, n, full.u, len(full._final))
+    assert (magic, version, flags, n_lo, u, K) == (b"MERTCKP1", 3, 1 << 16, n, full.u, len(full._final))
     # resume from the last checkpoint of that run (somewhere in the tail)
-    r = engine.resume_exact(path, engine.EngineConfig(seg_log2_tail=20))
+    r = engine.resume_exact(path, engine.EngineConfig(seg_log2_tail=18))
     assert r.value == full.value and np.array_equal(r._final, full._final)
     assert np.array_equal(r._cp_m, full._cp_m)
     from paper_1108_0135_b200.errors import ContractViolationError
 
     with pytest.raises(ContractViolationError):
-        engine.resume_exact(path, engine.EngineConfig(u_alpha=2.0, seg_log2_tail=20))
+        engine.resume_exact(path, engine.EngineConfig(u_alpha=2.0, seg_log2_tail=18))
     bad = str(tmp_path / "bad.bin")
     open(bad, "wb").write(b"x" * 100)
     with pytest.raises(Exception):
