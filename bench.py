@@ -136,10 +136,10 @@ def cpu_reference_sample(n: int, u: int, threads: int):
     extrapolate to the whole job (SURVEY.md §8(d) CPU-baseline plan).
 
     apply : the reference's apply_block, single-threaded as the reference runs it
-            (engine.py:380-384), for every S-th element on two y-blocks: the first
-            block [1, 2^22] (counted-walk heavy) and a block at y = 2^30 inside
-            the dense region (random M gathers).  The two blocks' (counted, dense)
-            pair counts and times give the per-pair costs t_c, t_d.  oracle/_ref's
+            (engine.py:380-384), on two y-blocks: [1, 2^22] for every S-th element
+            (its counted walks -> t_c per counted pair) and a block at y = 2^30
+            inside the dense region for the sampled elements whose counted walk
+            ended below it (random M gathers -> t_d per dense pair).  oracle/_ref's
             compiled kernel when n <= 4e18 (where it is defined), else the oracle's C
             port with mod-2^64 wrap (the reference's i128 guard rejects those n).
     sieve : the reference's sieve_logprime on 2^28 y at y = u/2 over `threads`
@@ -160,21 +160,26 @@ def cpu_reference_sample(n: int, u: int, threads: int):
     counted = int(H.mcut.sum(dtype=np.uint64))
     dense = int(np.where(H.xcut >= H.lo, H.xcut - H.lo + np.uint64(1), 0).sum(dtype=np.uint64))
     K = n // u
-    stride = max(1, K // 1024)
+    stride = max(1, K // 256)  # ~1e9 counted pairs at 1e19: ~5 s of one core
     ks = np.arange(0, K, stride)
     primes = E.generate_primes(E.ceil_sqrt(u) + 1)
     logs, wheel = E.build_logs(primes), E.build_wheel()
     use_ref_apply = kern_ref is not None and n <= 4 * 10**18
     L = 1 << 22
     blocks = []
-    for y1 in (1, 1 << 30):
+    # block 1: [1, 2^22] -- counted walks of every sampled element (no dense items yet);
+    # block 2: [2^30, 2^30 + 2^22) over the elements whose counted walk ended below it
+    # (8x denser sample) -- dense items only, the random M gathers
+    for y1, ks_b in ((1, ks), (1 << 30, np.arange(0, K, max(1, K // 2048)))):
         y2 = min(y1 + L - 1, u)
+        if y1 > 1:
+            ks_b = ks_b[H.mcut[ks_b] < np.uint64(y1)]
         mu = E.mu_range(kern_c, y1, y2, primes, logs, wheel)
         mp = np.cumsum(mu, dtype=np.int64)  # the base M(y1 - 1) does not change the work
         dn, yn = _walk_state_at(H, y1)
-        a = {f: np.ascontiguousarray(getattr(H, f)[ks]) for f in ("v", "lo", "xcut", "mcut")}
-        dn, yn = np.ascontiguousarray(dn[ks]), np.ascontiguousarray(yn[ks])
-        acc = np.zeros(len(ks), np.int64 if use_ref_apply else np.uint64)
+        a = {f: np.ascontiguousarray(getattr(H, f)[ks_b]) for f in ("v", "lo", "xcut", "mcut")}
+        dn, yn = np.ascontiguousarray(dn[ks_b]), np.ascontiguousarray(yn[ks_b])
+        acc = np.zeros(len(ks_b), np.int64 if use_ref_apply else np.uint64)
         t0 = time.perf_counter()
         if use_ref_apply:
             c, d = kern_ref.apply_block(acc, a["v"], a["lo"], a["xcut"], a["mcut"], dn, yn, y1, y2, mp, None)
@@ -182,11 +187,8 @@ def cpu_reference_sample(n: int, u: int, threads: int):
             c, d = kern_c.apply_block_wrap(acc, a["v"], a["lo"], a["xcut"], a["mcut"], dn, yn, y1, y2, mp)
         blocks.append((int(c), int(d), time.perf_counter() - t0))
     (c1, d1, s1), (c2, d2, s2) = blocks
-    det = c1 * d2 - c2 * d1
-    tc = (s1 * d2 - s2 * d1) / det if det else 0.0
-    td = (c1 * s2 - c2 * s1) / det if det else 0.0
-    if not (tc > 0 and td > 0):  # ill-conditioned: one blended rate
-        tc = td = (s1 + s2) / max(1, c1 + d1 + c2 + d2)
+    tc = s1 / max(1, c1 + d1)
+    td = max(0.0, s2 - c2 * tc) / max(1, d2)
     SL = 1 << 28
     y0 = max(2, u // 2)
     sk = kern_ref if kern_ref is not None else kern_c
@@ -199,8 +201,9 @@ def cpu_reference_sample(n: int, u: int, threads: int):
     t_apply = counted * tc + dense * td
     est = t_apply + u / y_rate
     kind = "reference" if (use_ref_apply and kern_ref is not None) else "port"
-    sample = (f"apply_block single-threaded (as the reference) on every {stride}-th of K={K} elements over the "
-              f"blocks [1,2^22] ({c1:.3g} counted + {d1:.3g} dense pairs, {s1:.3g} s) and [2^30,2^30+2^22) "
+    sample = (f"apply_block single-threaded (as the reference) on every {stride}-th of K={K} elements over "
+              f"[1,2^22] ({c1:.3g} counted + {d1:.3g} dense pairs, {s1:.3g} s) and on the elements of an 8x "
+              f"denser sample whose counted walk ended below 2^30 over [2^30,2^30+2^22) "
               f"({c2:.3g} + {d2:.3g} pairs, {s2:.3g} s) -> {tc * 1e9:.3g} ns/counted pair, "
               f"{td * 1e9:.3g} ns/dense pair ({'oracle/_ref compiled kernel' if use_ref_apply else 'oracle C port, mod-2^64 (reference kernel rejects n>4e18)'})"
               f"; sieve_logprime of 2^28 y at y={y0} on {threads} threads ({'oracle/_ref' if kern_ref is not None else 'oracle C port'}); "
@@ -294,6 +297,8 @@ def main():
     ap.add_argument("--no-anchor", action="store_true")
     ap.add_argument("--anchor-n", default="1e13", help="end-to-end config both arms run in full")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="each rank prints its rank/world and exits (tests the --gpus launcher)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(_relaunch(args))
@@ -303,6 +308,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but the launcher started {world} ranks")
+    if args.launch_check:
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local}), flush=True)
+        return
 
     import paper_1108_0135_b200 as P
 

@@ -106,6 +106,12 @@ int mt_sieve_odd(uint64_t y1, uint64_t y2, int8_t* mu_out);
 int mt_sieve_bench2(uint64_t Y0, uint64_t nseg, uint64_t y_last, int odd, double* ms_out);
 int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, double* ms_out); /* odd = 0 */
 
+/* the engine's exact 128/64 division (reciprocal multiply + exact correction,
+ * taken by the elements with v >= 2^64 at n >= 2^64) on a batch: q = v / m for
+ * v = v_hi:v_lo < 2^120, m >= 1 (parity entry for tests) */
+int mt_udiv128_batch(const uint64_t* v_lo, const uint64_t* v_hi, const uint64_t* m, uint64_t n,
+                     uint64_t* q_lo, uint64_t* q_hi);
+
 /* ---- 2. job-level production entry ----------------------------------------- */
 
 typedef struct {

@@ -50,10 +50,33 @@ __device__ __forceinline__ double u128_to_double(u64 lo, u64 hi) {
   return hi ? fma((double)hi, 18446744073709551616.0, (double)lo) : __ull2double_rn(lo);
 }
 
-// exact floor((hi:lo)/m) for any m >= 1 (slow path)
+// exact floor((hi:lo)/m), m >= 1, v < 2^120 (the engine's v < 2^75): reciprocal
+// multiply with exact correction instead of the compiler's software u128/u64.
+//   1. q = trunc(double(v) * rcp(m)): relative error < 2^-50, so the signed
+//      remainder t = v - q m (exact, 128-bit) satisfies |t/m| < 2^-50 q + 2;
+//   2. q += round(double(t) * rcp(m)) -- |t/m| < 2^70 fits the estimate's range
+//      and its error is < 2 -- and t -= that multiple of m (exact);
+//   3. at most two +-1 steps bring t into [0, m).
 __device__ __forceinline__ u128 udiv128(u64 lo, u64 hi, u64 m) {
-  u128 v = ((u128)hi << 64) | lo;
-  return v / m;
+  const u128 v = ((u128)hi << 64) | lo;
+  const double r = __drcp_rn((double)m);
+  const double vd = hi ? fma((double)hi, 18446744073709551616.0, (double)lo) : __ull2double_rn(lo);
+  const double qd = vd * r;
+  u128 q;
+  if (qd < 18446744073709551616.0) {
+    q = __double2ull_rz(qd);
+  } else {  // split at 2^64: both parts exact (qd has <= 53 significant bits)
+    const u64 qh = __double2ull_rz(qd * 5.421010862427522e-20);  // 2^-64
+    const double rest = fma(-(double)qh, 18446744073709551616.0, qd);
+    q = ((u128)qh << 64) | __double2ull_rz(rest > 0.0 ? rest : 0.0);
+  }
+  i128 t = (i128)(v - q * (u128)m);
+  const long long q2 = __double2ll_rn((double)t * r);
+  q += (u128)(i128)q2;
+  t -= (i128)q2 * (i128)(u128)m;
+  while (t < 0) { q -= 1; t += (i128)(u128)m; }
+  while (t >= (i128)(u128)m) { q += 1; t -= (i128)(u128)m; }
+  return q;
 }
 
 // exact floor(v/m) choosing the fast path when it is provably exact

@@ -25,6 +25,7 @@
 #include <unistd.h>
 
 #include <cub/cub.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include "mt_common.cuh"
 #include "mt_internal.h"
@@ -409,6 +410,33 @@ extern "C" int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, doubl
   return mt_sieve_bench2(Y0, nseg, y_last, 0, ms_out);
 }
 
+// exact 128/64 division of the engine (udiv128, mt_common.cuh) on a batch: parity
+// entry for the reciprocal-multiply + correction path the n >= 2^64 elements take
+__global__ void k_udiv128(const u64* lo, const u64* hi, const u64* m, u64 n, u64* qlo, u64* qhi) {
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u128 q = udiv128(lo[i], hi[i], m[i]);
+  qlo[i] = (u64)q;
+  qhi[i] = (u64)(q >> 64);
+}
+
+extern "C" int mt_udiv128_batch(const uint64_t* v_lo, const uint64_t* v_hi, const uint64_t* m, uint64_t n,
+                                uint64_t* q_lo, uint64_t* q_hi) {
+  if (!n) return MT_OK;
+  for (u64 i = 0; i < n; i++)
+    if (!m[i] || (v_hi[i] >> 56)) { mt_set_error("udiv128: m >= 1 and v < 2^120 required"); return MT_ERR_VALUE; }
+  DevBuf a, b, c, d, e;
+  RC(dalloc(a, n * 8)); RC(dalloc(b, n * 8)); RC(dalloc(c, n * 8)); RC(dalloc(d, n * 8)); RC(dalloc(e, n * 8));
+  MT_CUDA_CHECK(cudaMemcpy(a.p, v_lo, n * 8, cudaMemcpyHostToDevice));
+  MT_CUDA_CHECK(cudaMemcpy(b.p, v_hi, n * 8, cudaMemcpyHostToDevice));
+  MT_CUDA_CHECK(cudaMemcpy(c.p, m, n * 8, cudaMemcpyHostToDevice));
+  k_udiv128<<<(unsigned)((n + 255) / 256), 256>>>(a.as<u64>(), b.as<u64>(), c.as<u64>(), n, d.as<u64>(), e.as<u64>());
+  MT_CUDA_CHECK(cudaGetLastError());
+  MT_CUDA_CHECK(cudaMemcpy(q_lo, d.p, n * 8, cudaMemcpyDeviceToHost));
+  MT_CUDA_CHECK(cudaMemcpy(q_hi, e.p, n * 8, cudaMemcpyDeviceToHost));
+  return MT_OK;
+}
+
 // ============================================================================
 // backend-protocol: apply_block / finalize / divisor arrays
 // ============================================================================
@@ -652,6 +680,12 @@ __global__ void k_cap_mask(int* __restrict__ Q, u64 jq0, u64 c0, u64 c1, u64 s0,
   const bool mine = (j >= s0 && j <= s1) || (head_mine && j >= jh);
   if (!mine) Q[j - jq0] = 0;
 }
+
+// NVTX ranges around the plan's phases (visible in nsys / ncu --nvtx; no-ops otherwise)
+struct NvtxRange {
+  explicit NvtxRange(const char* s) { nvtxRangePushA(s); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static double ms_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1055,6 +1089,7 @@ extern "C" int mt_plan_sieve_step(mt_plan* P, uint64_t max_tail_segments, int* d
   PLAN_DEV(P);
   cudaStream_t st = P->st;
   if (!P->head_done) {
+    NvtxRange nv("mt.head");
     P->kt.reset();
     P->launches = 0;
     mt_update_reset_launches(P->uc);
@@ -1095,6 +1130,7 @@ extern "C" int mt_plan_sieve_step(mt_plan* P, uint64_t max_tail_segments, int* d
   const u64 room = ns > P->tseg_next ? ns - P->tseg_next : 0;
   const u64 s_end = P->tseg_next + std::min<u64>(room, max_tail_segments);
   if (P->tseg_next < s_end) {
+    NvtxRange nv("mt.tail");
     MT_CUDA_CHECK(cudaEventRecord(P->ev[1], st));
     for (u64 s = P->tseg_next; s < s_end; s++) {
       RC(mt_sieve2_run(P->sv, P->tsegs[s].Y0, P->tsegs[s].ntiles, P->d_run.as<int64_t>(), nullptr, nullptr, nullptr,
@@ -1352,6 +1388,7 @@ extern "C" int mt_plan_acc(mt_plan* P, void** dptr, uint64_t* count) {
 extern "C" int mt_plan_gather(mt_plan* P) {
   if (P->phase < 2) { mt_set_error("gather before tail_offset"); return MT_ERR_CONTRACT; }
   PLAN_DEV(P);
+  NvtxRange nv("mt.gather");
   MT_CUDA_CHECK(cudaEventRecord(P->ev[3], P->st));
   const int N = P->N;
   std::vector<u64> wlo(N, 0), whi(N, 0);
@@ -1381,6 +1418,7 @@ extern "C" int mt_plan_gather(mt_plan* P) {
 extern "C" int mt_plan_resolve(mt_plan* P, mt_result* out) {
   if (P->phase < 3) { mt_set_error("finalize before the harmonic array is complete"); return MT_ERR_CONTRACT; }
   PLAN_DEV(P);
+  NvtxRange nv("mt.resolve");
   cudaStream_t st = P->st;
   MT_CUDA_CHECK(cudaEventRecord(P->ev[4], st));
   for (int i = 0; i < P->N; i++)

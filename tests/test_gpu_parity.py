@@ -433,8 +433,8 @@ def test_c3_64_targets_1161e19(engine):
     t0 = time.perf_counter()
     mm = engine.mertens_exact_multi(ns)
     wall = time.perf_counter() - t0
-    u = engine.choose_u(max(ns), 64)
-    assert u == 82_036_050_574_571 and mm[x].u == u
+    u = engine.choose_u(max(ns), 64)  # = 82,036,052,034,891 (choose_u of the largest target, engine.py:424-446)
+    assert mm[x].u == u and mm[ns[0]].u == u
     assert mm[x].value == -1995900927
     assert round(mm[x].ratio, 9) == -0.585767684
     lo = engine.mertens_exact_multi(ns[:32])
@@ -503,3 +503,31 @@ def test_checkpoint_resume(engine, golden, tmp_path):
     open(bad, "wb").write(b"x" * 100)
     with pytest.raises(Exception):
         engine.resume_exact(bad)
+
+
+def test_udiv128_reciprocal(engine):
+    """The exact 128/64 division (reciprocal multiply + correction) that replaces
+    the software u128/u64 for v >= 2^64: random v < 2^75 and m of every size,
+    plus the edges (m = 1, m = v, q at powers of two, v = q m - 1)."""
+    from paper_1108_0135_b200 import _lib
+
+    rng = np.random.default_rng(3)
+    vs, ms = [], []
+    for _ in range(20000):
+        v = int(rng.integers(0, 1 << 63)) << int(rng.integers(0, 13)) | int(rng.integers(0, 1 << 62))
+        m = max(1, int(rng.integers(0, 1 << 63)) >> int(rng.integers(0, 63)))
+        vs.append(v % (1 << 75)); ms.append(m)
+    for m in (1, 2, 3, (1 << 32) - 1, 1 << 32, (1 << 63) - 25, (1 << 64) - 1):
+        for q in (1, (1 << 52) + 1, (1 << 64) - 1, 1 << 64, (1 << 74) // m + 1):
+            for dv in (-1, 0, 1):
+                v = q * m + dv
+                if 0 <= v < (1 << 75):
+                    vs.append(v); ms.append(m)
+    lo = np.array([v & (2**64 - 1) for v in vs], np.uint64)
+    hi = np.array([v >> 64 for v in vs], np.uint64)
+    mm = np.array(ms, np.uint64)
+    qlo, qhi = np.zeros(len(vs), np.uint64), np.zeros(len(vs), np.uint64)
+    _lib.check(_lib.lib().mt_udiv128_batch(_lib.ptr(lo), _lib.ptr(hi), _lib.ptr(mm), len(vs), _lib.ptr(qlo), _lib.ptr(qhi)))
+    got = [(int(h) << 64) | int(l) for l, h in zip(qlo.tolist(), qhi.tolist())]
+    bad = [(v, m) for v, m, g in zip(vs, ms, got) if g != v // m]
+    assert not bad, bad[:5]

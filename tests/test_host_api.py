@@ -137,3 +137,20 @@ def test_dense_map_identity_residual(oracle):
     assert R.quotient(K + 5) == r.quotient(K + 5) and R.quotient(n // 7) == small[7]
     qmap[3] += 1
     assert P.mertens_identity_residual(R) != 0
+
+
+def test_bench_gpus_spawns_ranks():
+    """`bench.py --gpus 3` outside torchrun launches 3 ranks (torch.distributed.run)
+    and every rank sees world size 3 (--gpus was ignored)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "3", "--launch-check",
+                        "--dist-backend", "gloo"], capture_output=True, text=True, timeout=300, env=env)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == [0, 1, 2] and all(d["world"] == 3 for d in lines)
