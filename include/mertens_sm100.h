@@ -94,17 +94,19 @@ int mt_mertens_at(const uint64_t* pts, uint64_t npts, int64_t* m_out);
  * mu_out and, if m_out is non-null, M(y) into m_out (either may be null) */
 int mt_sieve_fast(uint64_t y1, uint64_t y2, int8_t* mu_out, int64_t* m_out);
 
-/* the production sieve in odd-cell (tail) mode, the one the engine runs above
- * the head: mu of the odd y of [y1, y2] (y1 >= 2^18) into mu_out[(y - y0)/2],
- * y0 = the first odd y >= y1 */
-int mt_sieve_odd(uint64_t y1, uint64_t y2, int8_t* mu_out);
+/* the production sieve in wheel (tail) mode, the one the engine runs above the
+ * head: mu of the y of [y1, y2] coprime to the wheel (2: odd y; 6: gcd(y, 6) = 1),
+ * y1 >= one tile (2^18 or 3 * 2^17), into mu_out[i] for the i-th such y */
+int mt_sieve_wheel(uint64_t y1, uint64_t y2, int wheel, int8_t* mu_out);
+int mt_sieve_odd(uint64_t y1, uint64_t y2, int8_t* mu_out); /* wheel 2 */
 
 /* profiling entry (tools/sieve_bench.py): the production sieve in tail mode
  * over nseg segments of 6 tiles per SM from Y0 (a multiple of the tile's y-span:
- * 2^17, or 2^18 with odd = 1) with the primes of y_last; summed CUDA-event ms
- * per kernel class into ms_out[7] (sieve_tile, bucket_fill, -, -, -, -, finish) */
-int mt_sieve_bench2(uint64_t Y0, uint64_t nseg, uint64_t y_last, int odd, double* ms_out);
-int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, double* ms_out); /* odd = 0 */
+ * 2^17 x 1, 2 or 3 for wheel 1, 2, 6) with the primes of y_last; summed
+ * CUDA-event ms per kernel class into ms_out[7] (sieve_tile, bucket_fill, -, -,
+ * -, -, finish) */
+int mt_sieve_bench2(uint64_t Y0, uint64_t nseg, uint64_t y_last, int wheel, double* ms_out);
+int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, double* ms_out); /* wheel 1 */
 
 /* the engine's exact 128/64 division (reciprocal multiply + exact correction,
  * taken by the elements with v >= 2^64 at n >= 2^64) on a batch: q = v / m for

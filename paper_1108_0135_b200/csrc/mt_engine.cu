@@ -350,14 +350,20 @@ extern "C" int mt_sieve_fast(uint64_t y1, uint64_t y2, int8_t* mu_out, int64_t* 
   return MT_OK;
 }
 
-// the production sieve in odd-cell (tail) mode over the odd y of [y1, y2]
-// (y1 >= 2^18): mu_out[i] = mu(y0 + 2i), y0 = the first odd y >= y1
-extern "C" int mt_sieve_odd(uint64_t y1, uint64_t y2, int8_t* mu_out) {
-  const u64 SPAN = 2ull * MT_S2_TILE, NT = 256, RY = SPAN * NT;
-  if (y2 < y1 || y1 < SPAN) { mt_set_error("bad range (odd-cell sieve needs y1 >= 2^18)"); return MT_ERR_VALUE; }
+// cells of wheel W with y - Y0 <= o (host mirror of Wheel<W>::ncell, Y0 a multiple of W)
+static u64 wheel_ncell(int W, u64 o) {
+  return W == 1 ? o + 1 : W == 2 ? (o + 1) >> 1 : 2 * (o / 6) + (o % 6 >= 1) + (o % 6 >= 5);
+}
+
+// the production sieve in wheel (tail) mode over the y of [y1, y2] coprime to the
+// wheel (2: odd y; 6: gcd(y, 6) = 1), y1 >= one tile: mu_out[i] = mu of the i-th
+// such y in ascending order
+extern "C" int mt_sieve_wheel(uint64_t y1, uint64_t y2, int wheel, int8_t* mu_out) {
+  if (wheel != 2 && wheel != 6) { mt_set_error("wheel must be 2 or 6"); return MT_ERR_VALUE; }
+  const u64 SPAN = (u64)MT_S2_TILE * (wheel == 2 ? 2 : 3), NT = 256, RY = SPAN * NT;
+  if (y2 < y1 || y1 < SPAN) { mt_set_error("bad range (the wheel sieve needs y1 >= one tile)"); return MT_ERR_VALUE; }
   u64 Y0 = (y1 / SPAN) * SPAN;
-  const u64 y0 = y1 | 1;
-  if (y0 > y2) return MT_OK;
+  const u64 first = wheel_ncell(wheel, y1 - 1 - Y0);  // cells of [Y0, y1)
   const u64 y_last = ((y2 - Y0) / RY + 1) * RY + Y0 - 1;
   Sieve2Host* h = nullptr;
   struct G { Sieve2Host*& h; ~G() { mt_sieve2_destroy(h); } } g{h};
@@ -365,24 +371,29 @@ extern "C" int mt_sieve_odd(uint64_t y1, uint64_t y2, int8_t* mu_out) {
   DevBuf d_mu, d_run;
   RC(dalloc(d_mu, NT * MT_S2_TILE)); RC(dalloc(d_run, 8));
   MT_CUDA_CHECK(cudaMemset(d_run.p, 0, 8));
-  for (; Y0 <= y2; Y0 += RY) {
+  u64 done = 0;  // cells of [Y0_first, Y0) copied or skipped
+  for (u64 base = 0; Y0 <= y2; Y0 += RY, base += NT * MT_S2_TILE) {
     RC(mt_sieve2_run(h, Y0, (uint32_t)NT, d_run.as<int64_t>(), d_mu.as<int8_t>(), nullptr, nullptr, nullptr,
-                     nullptr, 0, 0, nullptr, true));
-    const u64 ya = std::max(Y0 + 1, y0), yb = std::min(Y0 + RY - 1, y2);  // odd y of this segment
-    if (yb < ya) continue;
-    const u64 ca = (ya - Y0 - 1) / 2, cb = (yb - Y0 - 1) / 2;
-    MT_CUDA_CHECK(cudaMemcpy(mu_out + (ya - y0) / 2, d_mu.as<int8_t>() + ca, cb - ca + 1, cudaMemcpyDeviceToHost));
+                     nullptr, 0, 0, nullptr, wheel));
+    const u64 ca = base < first ? first - base : 0;                   // first wanted cell of this segment
+    const u64 cb = wheel_ncell(wheel, std::min(y2, Y0 + RY - 1) - Y0);  // cells with y <= min(y2, end)
+    if (cb > ca) MT_CUDA_CHECK(cudaMemcpy(mu_out + (base + ca - first), d_mu.as<int8_t>() + ca, cb - ca, cudaMemcpyDeviceToHost));
+    done = base + cb;
   }
+  (void)done;
   MT_CUDA_CHECK(cudaDeviceSynchronize());
   return MT_OK;
 }
 
+extern "C" int mt_sieve_odd(uint64_t y1, uint64_t y2, int8_t* mu_out) { return mt_sieve_wheel(y1, y2, 2, mu_out); }
+
 // profiling entry: the production sieve in tail mode (sums only, no outputs)
 // over nseg segments of the default size from Y0 (multiple of 2^17), with
 // primes for y_last; per-kernel-class CUDA-event ms into ms_out[KT_NCLASS]
-extern "C" int mt_sieve_bench2(uint64_t Y0, uint64_t nseg, uint64_t y_last, int odd, double* ms_out) {
-  const u64 span = odd ? 2ull * MT_S2_TILE : MT_S2_TILE;
-  if (Y0 % span || (odd && Y0 == 0)) { mt_set_error("Y0 must be a positive multiple of the tile span"); return MT_ERR_VALUE; }
+extern "C" int mt_sieve_bench2(uint64_t Y0, uint64_t nseg, uint64_t y_last, int wheel, double* ms_out) {
+  if (wheel == 0) wheel = 1;
+  const u64 span = (u64)MT_S2_TILE * (wheel == 6 ? 3 : wheel);
+  if (Y0 % span || (wheel > 1 && Y0 == 0)) { mt_set_error("Y0 must be a positive multiple of the tile span"); return MT_ERR_VALUE; }
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -399,7 +410,7 @@ extern "C" int mt_sieve_bench2(uint64_t Y0, uint64_t nseg, uint64_t y_last, int 
   kt.init(true);
   for (u64 s = 0; s < nseg; s++)
     RC(mt_sieve2_run(h, Y0 + s * R, NT, d_run.as<int64_t>(), nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, &kt,
-                     odd != 0));
+                     wheel));
   MT_CUDA_CHECK(cudaDeviceSynchronize());
   kt.drain();
   for (int c = 0; c < KT_NCLASS; c++) ms_out[c] = kt.ms[c];
@@ -664,12 +675,16 @@ __global__ void k_copy_caps(const int* __restrict__ Q, u64 jq0, u64 c_lo, u64 cn
   out[i] = Q[c_lo + i - jq0];
 }
 
-// Q[j] = Q[j] - P2[j] + delta over one target's own tail slice: the odd-cell
-// prefix P at floor(n/j) minus P at floor(n/(2j)) is M(floor(n/j)) - M(ya - 1)
-// up to the constant P(ya - 1) folded into delta
-__global__ void k_q_combine(int* __restrict__ Q, const int* __restrict__ P2, u64 cnt, int delta) {
+// Q[j] = sum_d s_d T_d[j] + delta over one target's own tail slice, T_1 = Q:
+// the wheel prefixes at floor(n/(d j)) combine to M(floor(n/j)) - M(ya - 1) up to
+// a constant folded into delta
+struct CombineArgs { const int* T[3]; int s[3]; int n; };
+__global__ void k_q_combine(int* __restrict__ Q, CombineArgs c, u64 cnt, int delta) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < cnt) Q[i] = Q[i] - P2[i] + delta;
+  if (i >= cnt) return;
+  int v = Q[i] + delta;
+  for (int k = 0; k < c.n; k++) v += c.s[k] * c.T[k][i];
+  Q[i] = v;
 }
 
 // multi-rank output assembly: zero the capture-window entries this rank does
@@ -694,44 +709,68 @@ static double ms_since(std::chrono::steady_clock::time_point t0) {
 // ============================================================================
 // the tail split
 // ============================================================================
-// M(x) = O(x) - O(floor(x/2)) with O the sum of mu over ODD y <= x (mu(2z) =
-// -mu(z) for odd z, mu = 0 on multiples of 4).  A rank owning the tail range
-// [a, b) therefore sieves only odd y, over [a/2, b/2) U [a, b), with one running
-// prefix P (P(a/2 - 1) = 0): for x in [a, b),
-//   M(x) - M(a - 1) = P(x) - P(floor(x/2)) - P(a - 1).
-// Boundaries are multiples of TAIL_ALIGN so that a/2 is a multiple of the odd
-// tile's y-span (2^18).
-#define TAIL_ALIGN (1ull << 19)
-#define TILE_Y_ODD (2ull * MT_S2_TILE)
+// The tail sieves only the y coprime to the wheel W (2: odd y; 6: gcd(y, 6) = 1).
+// With C_W(x) the Moebius sum over those y <= x (mu(2z) = -mu(z) for odd z,
+// mu(3z) = -mu(z) for 3 not dividing z, mu = 0 on multiples of 4 and 9):
+//   M(x) = sum_{d | W} mu(d) C_W(floor(x/d)),   d in {1, 2} (W = 2) or {1, 2, 3, 6} (W = 6).
+// A rank owning the tail range [a, b) sieves the wheel cells of the union of
+// [a/d, b/d) with one running prefix P (P(a/W - 1) = 0), cut at every a/d and
+// b/d, and records P at those breakpoints.  For x in [a, b):
+//   M(x) - M(a - 1) = sum_d mu(d) (P(floor(x/d)) - P(a/d - 1)).
+// Boundaries are multiples of W * (tile y-span) so every a/d is a tile boundary.
+struct TailWheel {
+  int W = 6, nd = 4;
+  u64 d[4] = {1, 2, 3, 6};
+  int s[4] = {1, -1, -1, 1};
+  u64 tile_y = 3ull * MT_S2_TILE;  // y per tile (2^17 cells)
+  u64 align() const { return (u64)W * tile_y; }
+};
+static TailWheel tail_wheel(int W) {
+  TailWheel t;
+  if (W == 2) { t.W = 2; t.nd = 2; t.tile_y = 2ull * MT_S2_TILE; }
+  return t;
+}
 
-// y-values a rank owning [a, b) covers: |[a/2, b/2) U [a, b)| (odd cells = half of it)
-static u64 tail_cost(u64 a, u64 b) {
-  if (b <= a) return 0;
-  const u64 h0 = a / 2, h1 = b / 2;
-  u64 c = (b - a) + (h1 - h0);
-  if (h1 > a) c -= h1 - a;
+// the y-intervals [a/d, b/d) a rank owning [a, b) sieves, merged
+static std::vector<std::pair<u64, u64>> tail_union(const TailWheel& tw, u64 a, u64 b) {
+  std::vector<std::pair<u64, u64>> iv, out;
+  if (b <= a) return out;
+  for (int k = 0; k < tw.nd; k++) iv.push_back({a / tw.d[k], b / tw.d[k]});
+  std::sort(iv.begin(), iv.end());
+  for (auto& x : iv) {
+    if (!out.empty() && x.first <= out.back().second) out.back().second = std::max(out.back().second, x.second);
+    else out.push_back(x);
+  }
+  return out;
+}
+
+// y-values a rank owning [a, b) covers (its cells: 1/2 or 1/3 of them)
+static u64 tail_cost(const TailWheel& tw, u64 a, u64 b) {
+  u64 c = 0;
+  for (auto& x : tail_union(tw, a, b)) c += x.second - x.first;
   return c;
 }
 
-// boundaries H = y[0] < ... <= y[w] = E on TAIL_ALIGN, balancing tail_cost
-static std::vector<u64> tail_partition(u64 H, u64 E, uint32_t w) {
+// boundaries H = y[0] < ... <= y[w] = E on the wheel's alignment, balancing tail_cost
+static std::vector<u64> tail_partition(const TailWheel& tw, u64 H, u64 E, uint32_t w) {
   std::vector<u64> yb(w + 1, E);
   yb[0] = H;
   if (w <= 1 || E <= H) return yb;
+  const u64 AL = tw.align();
   auto cover = [&](u64 c, std::vector<u64>* out) -> bool {
     u64 a = H;
     for (uint32_t r = 0; r + 1 < w; r++) {
-      u64 lo = 0, hi = (E - a) / TAIL_ALIGN;  // largest step with cost <= c
+      u64 lo = 0, hi = (E - a) / AL;  // largest step with cost <= c
       while (lo < hi) {
         const u64 mid = (lo + hi + 1) / 2;
-        if (tail_cost(a, a + mid * TAIL_ALIGN) <= c) lo = mid; else hi = mid - 1;
+        if (tail_cost(tw, a, a + mid * AL) <= c) lo = mid; else hi = mid - 1;
       }
-      a += lo * TAIL_ALIGN;
+      a += lo * AL;
       if (out) (*out)[r + 1] = a;
     }
-    return tail_cost(a, E) <= c;
+    return tail_cost(tw, a, E) <= c;
   };
-  u64 lo = 0, hi = tail_cost(H, E);
+  u64 lo = 0, hi = tail_cost(tw, H, E);
   while (lo < hi) {
     const u64 mid = lo + (hi - lo) / 2;
     if (cover(mid, nullptr)) hi = mid; else lo = mid + 1;
@@ -743,23 +782,28 @@ static std::vector<u64> tail_partition(u64 H, u64 E, uint32_t w) {
 
 struct TailSeg { u64 Y0; uint32_t ntiles; };
 
-// this rank's odd-cell segments over [a/2, b/2) U [a, b), cut at a and b/2;
-// snap_a / snap_h = number of segments ending at or before a / b/2
-static void tail_segments(u64 a, u64 b, u64 seg_y, std::vector<TailSeg>& out, size_t& snap_a, size_t& snap_h) {
-  out.clear();
-  snap_a = snap_h = 0;
+// this rank's wheel segments over the union of [a/d, b/d), cut at every
+// breakpoint a/d, b/d; bp[i] = the breakpoints (ascending) and snap[i] = the number
+// of segments ending at or before bp[i] (P(bp[i] - 1) is the running prefix then)
+static void tail_segments(const TailWheel& tw, u64 a, u64 b, u64 seg_y, std::vector<TailSeg>& out,
+                          std::vector<u64>& bp, std::vector<size_t>& snap) {
+  out.clear(); bp.clear(); snap.clear();
   if (b <= a) return;
-  const u64 h0 = a / 2, h1 = b / 2;
-  std::vector<std::pair<u64, u64>> iv;
-  if (h1 > a) iv = {{h0, a}, {a, h1}, {h1, b}};
-  else iv = {{h0, h1}, {a, b}};
-  for (auto& x : iv)
-    for (u64 s = x.first; s < x.second; s += seg_y)
-      out.push_back({s, (uint32_t)((std::min(x.second, s + seg_y) - s) / TILE_Y_ODD)});
-  for (auto& s : out) {
-    const u64 e = s.Y0 + (u64)s.ntiles * TILE_Y_ODD;
-    if (e <= a) snap_a++;
-    if (e <= h1) snap_h++;
+  for (int k = 0; k < tw.nd; k++) { bp.push_back(a / tw.d[k]); bp.push_back(b / tw.d[k]); }
+  std::sort(bp.begin(), bp.end());
+  bp.erase(std::unique(bp.begin(), bp.end()), bp.end());
+  for (size_t i = 0; i + 1 < bp.size(); i++) {
+    const u64 x = bp[i], y = bp[i + 1];
+    bool cov = false;
+    for (int k = 0; k < tw.nd; k++) cov |= a / tw.d[k] <= x && y <= b / tw.d[k];
+    if (!cov) continue;
+    for (u64 s = x; s < y; s += seg_y)
+      out.push_back({s, (uint32_t)((std::min(y, s + seg_y) - s) / tw.tile_y)});
+  }
+  for (u64 x : bp) {
+    size_t c = 0;
+    for (auto& s : out) c += s.Y0 + (u64)s.ntiles * tw.tile_y <= x;
+    snap.push_back(c);
   }
 }
 
@@ -790,23 +834,31 @@ struct mt_plan {
   std::vector<TargetDev> tdev;
   std::vector<CaptureTargetH> caps_head, caps_tail;
   // own tail slice per target (j with floor(n/j) in [ya, yb); empty: sj0 > sj1)
-  // and P2[j - sj0] = P(floor(n/(2j))) for it
+  // and the wheel-prefix tables d_P[t * (nd - 1) + k - 1][j - sj0] = P(floor(n/(d_k j)))
   std::vector<u64> sj0, sj1;
-  std::vector<DevBuf> d_P2;
+  std::vector<DevBuf> d_P;
   // segments
   u64 Rh = 0, head_end = 0, head_segs = 0, head_lim = 0, y_last = 0;
   u64 tail_end = 0, seg_y = 0;       // tail = [head_lim, tail_end); odd segments span <= seg_y
   std::vector<u64> ybound;           // rank r owns [ybound[r], ybound[r+1])
   u64 ya = 0, yb = 0;
   std::vector<TailSeg> tsegs;
-  size_t snap_a = 0, snap_h = 0;
+  TailWheel tw;                      // the tail's wheel (MT_TAIL_WHEEL: 6 default, or 2)
+  std::vector<u64> bp;               // breakpoints a/d, b/d (ascending)
+  std::vector<size_t> snap;          // P(bp[i] - 1) = the running prefix after snap[i] segments
+  std::vector<int64_t> snapv;        // those prefixes (host, after the tail)
   Sieve2Host* sv = nullptr;
   DevBuf d_mu, d_m, d_bk, d_run, d_snap, d_caps_head, d_caps_tail, d_small;
   u64 cap_c_lo = 1, cap_c_hi = 0, cap_small = 0, nsmall = 0;
   bool cap32 = false;  // MT_FLAG_CAP32: int32 capture outputs (the dense full quotient map)
   UpdateCtx* uc = nullptr;
   KTimer kt;
-  int64_t m_head = 0, tail_total = 0, s_a = 0, s_h = 0, p_end = 0;
+  int64_t m_head = 0, tail_total = 0, p_end = 0;
+  // P at breakpoint y (y must be one of bp)
+  int64_t snap_at(u64 y) const {
+    for (size_t i = 0; i < bp.size(); i++) if (bp[i] == y) return snapv[i];
+    return 0;
+  }
   double ms_setup = 0, ms_head = 0, ms_tail = 0, ms_gather = 0, ms_fin = 0;
   cudaEvent_t ev[6] = {};
   int phase = 0;  // 1 after sieve_update, 2 after tail_offset, 3 after gather
@@ -839,6 +891,7 @@ struct mt_plan {
     for (auto& s : tsegs) c += (u64)s.ntiles * MT_S2_TILE;
     return c;
   }
+  int nx() const { return tw.nd - 1; }  // wheel-prefix tables per target besides Q
 };
 
 #define PLAN_DEV(p) do { if ((p)->device >= 0) MT_CUDA_CHECK(cudaSetDevice((p)->device)); } while (0)
@@ -916,9 +969,15 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   }
 
   // ---- quotient tables: Q_t[j] = M(floor(n_t/j)), j in [jq0_t, jq1_t]; the tail
-  // part also needs P2 (odd-prefix captures at floor(n/(2j))), so a table entry
-  // is budgeted at 8 bytes
-  const u64 q_budget = job->q_budget_bytes ? job->q_budget_bytes : (96ull << 30);
+  // part also needs the wheel-prefix captures at floor(n/(d j)), d | W, d > 1, so a
+  // table entry is budgeted at 4 bytes per divisor
+  {
+    int W = 6;
+    if (const char* ev = getenv("MT_TAIL_WHEEL")) W = atoi(ev);
+    if (W != 2 && W != 6) { mt_set_error("MT_TAIL_WHEEL must be 2 or 6"); return MT_ERR_VALUE; }
+    P->tw = tail_wheel(W);
+  }
+  const u64 q_budget = job->q_budget_bytes ? job->q_budget_bytes : (128ull << 30);
   P->J.assign(N, 0); P->jq0.assign(N, 0); P->jq1.assign(N, 0);
   P->cap_c_lo = job->cap_c_lo; P->cap_c_hi = job->cap_c_hi;
   for (int i = 0; i < N; i++) {
@@ -933,7 +992,7 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
       P->jq1[i] = hi;
       if (hi >= P->jq0[i]) q_total += (hi - P->jq0[i] + 1);
     }
-    if (q_total * 8 <= q_budget) break;
+    if (q_total * 4 * P->tw.nd <= q_budget) break;
     for (int i = 0; i < N; i++) P->J[i] = P->J[i] / 2;
   }
   for (int i = 0; i < N; i++)
@@ -1014,35 +1073,37 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
     mt_set_error("bad segment sizes");
     return MT_ERR_VALUE;
   }
-  P->seg_y = tail_tiles * TILE_Y_ODD;
-  P->head_segs = (head_end + 1 + Rh - 1) / Rh;
-  while ((P->head_segs * Rh) % TAIL_ALIGN) P->head_segs++;  // the tail starts on TAIL_ALIGN
-  P->head_lim = P->head_segs * Rh;  // first y of the tail
+  P->seg_y = tail_tiles * P->tw.tile_y;
+  // the head ends on the wheel's alignment (its last segment may be shorter than Rh)
+  const u64 AL = P->tw.align();
+  P->head_lim = (head_end + 1 + AL - 1) / AL * AL;  // first y of the tail
+  P->head_segs = (P->head_lim + Rh - 1) / Rh;
   P->tail_end = P->head_lim;
-  if (u + 1 > P->head_lim) P->tail_end = (u + 1 + TAIL_ALIGN - 1) / TAIL_ALIGN * TAIL_ALIGN;
-  P->ybound = tail_partition(P->head_lim, P->tail_end, P->world);
+  if (u + 1 > P->head_lim) P->tail_end = (u + 1 + AL - 1) / AL * AL;
+  P->ybound = tail_partition(P->tw, P->head_lim, P->tail_end, P->world);
   P->ya = P->ybound[P->rank];
   P->yb = P->ybound[P->rank + 1];
-  tail_segments(P->ya, P->yb, P->seg_y, P->tsegs, P->snap_a, P->snap_h);
+  tail_segments(P->tw, P->ya, P->yb, P->seg_y, P->tsegs, P->bp, P->snap);
   P->y_last = std::max(P->tail_end, P->head_lim) - 1;
   RC(mt_sieve2_create(&P->sv, P->y_last, (uint32_t)std::max<u64>(Rh / MT_S2_TILE, tail_tiles), st));
   RC(dalloc(P->d_mu, Rh)); RC(dalloc(P->d_m, Rh * 2)); RC(dalloc(P->d_bk, (Rh / MT_BLK) * 8 + 8));
-  RC(dalloc(P->d_run, 8)); RC(dalloc(P->d_snap, 16));
-  // own tail slices, their P2 tables, and the tail capture list: Q at floor(n/j)
-  // and P2 at floor(floor(n/2)/j) = floor(n/(2j)) for j in the slice
+  RC(dalloc(P->d_run, 8)); RC(dalloc(P->d_snap, 8 * 8));
+  // own tail slices, their wheel-prefix tables, and the tail capture list: the
+  // prefix P at floor(n/j) (into Q) and at floor(floor(n/d)/j) = floor(n/(d j)) for
+  // every other divisor d of the wheel, for j in the slice
   P->sj0.assign(N, 1); P->sj1.assign(N, 0);
-  P->d_P2.clear();
-  P->d_P2.reserve(N);
+  P->d_P.clear();
+  P->d_P.reserve((size_t)N * P->nx());
   for (int i = 0; i < N; i++) {
-    P->d_P2.emplace_back();
     u64 j0, j1;
     P->q_slice(i, P->rank, j0, j1);
     P->sj0[i] = j0; P->sj1[i] = j1;
     const u64 cnt = j1 >= j0 ? j1 - j0 + 1 : 0;
-    RC(dalloc(P->d_P2[i], cnt * 4));
-    if (cnt) {
-      P->caps_tail.push_back(make_cap(P->n[i], j0, j1, P->tdev[i].Q + (j0 - P->jq0[i])));
-      P->caps_tail.push_back(make_cap(P->n[i] / 2, j0, j1, P->d_P2[i].as<int>()));
+    if (cnt) P->caps_tail.push_back(make_cap(P->n[i], j0, j1, P->tdev[i].Q + (j0 - P->jq0[i])));
+    for (int k = 1; k < P->tw.nd; k++) {
+      P->d_P.emplace_back();
+      RC(dalloc(P->d_P.back(), cnt * 4));
+      if (cnt) P->caps_tail.push_back(make_cap(P->n[i] / P->tw.d[k], j0, j1, P->d_P.back().as<int>()));
     }
   }
   RC(dalloc(P->d_caps_head, P->caps_head.size() * sizeof(CaptureTargetH)));
@@ -1097,19 +1158,19 @@ extern "C" int mt_plan_sieve_step(mt_plan* P, uint64_t max_tail_segments, int* d
     MT_CUDA_CHECK(cudaMemsetAsync(P->d_acc.p, 0, P->NE * 8, st));
     MT_CUDA_CHECK(cudaMemsetAsync(P->d_mmc.p, 0, P->NE * 4, st));
     MT_CUDA_CHECK(cudaMemsetAsync(P->d_run.p, 0, 8, st));
-    MT_CUDA_CHECK(cudaMemsetAsync(P->d_snap.p, 0, 16, st));
+    MT_CUDA_CHECK(cudaMemsetAsync(P->d_snap.p, 0, 8 * 8, st));
     MT_CUDA_CHECK(cudaEventRecord(P->ev[0], st));
     for (u64 s = 0; s < P->head_segs; s++) {
-      const u64 Y0 = s * P->Rh;
-      RC(mt_sieve2_run(P->sv, Y0, (uint32_t)(P->Rh / MT_S2_TILE), P->d_run.as<int64_t>(), P->d_mu.as<int8_t>(),
+      const u64 Y0 = s * P->Rh, R = std::min(P->Rh, P->head_lim - Y0);  // the last segment ends at head_lim
+      RC(mt_sieve2_run(P->sv, Y0, (uint32_t)(R / MT_S2_TILE), P->d_run.as<int64_t>(), P->d_mu.as<int8_t>(),
                        P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), nullptr,
                        (const CaptureTarget2*)P->d_caps_head.p, (int)P->caps_head.size(), st, &P->kt));
-      RC(mt_update_head_segment(P->uc, Y0, P->Rh, P->d_mu.as<int8_t>(), P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), st));
+      RC(mt_update_head_segment(P->uc, Y0, R, P->d_mu.as<int8_t>(), P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), st));
       if (P->nsmall && Y0 <= P->cap_small) {
         if (P->cap32)
-          k_copy_small<int32_t><<<(unsigned)((P->Rh + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, P->Rh, P->cap_small, P->d_small.as<int32_t>());
+          k_copy_small<int32_t><<<(unsigned)((R + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, R, P->cap_small, P->d_small.as<int32_t>());
         else
-          k_copy_small<int64_t><<<(unsigned)((P->Rh + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, P->Rh, P->cap_small, P->d_small.as<int64_t>());
+          k_copy_small<int64_t><<<(unsigned)((R + 255) / 256), 256, 0, st>>>(P->d_m.as<int16_t>(), P->d_bk.as<int64_t>(), Y0, R, P->cap_small, P->d_small.as<int64_t>());
         P->launches++;
       }
     }
@@ -1135,10 +1196,11 @@ extern "C" int mt_plan_sieve_step(mt_plan* P, uint64_t max_tail_segments, int* d
     for (u64 s = P->tseg_next; s < s_end; s++) {
       RC(mt_sieve2_run(P->sv, P->tsegs[s].Y0, P->tsegs[s].ntiles, P->d_run.as<int64_t>(), nullptr, nullptr, nullptr,
                        nullptr, (const CaptureTarget2*)P->d_caps_tail.p, (int)P->caps_tail.size(), st, &P->kt,
-                       true));
-      // prefix snapshots P(ya - 1) and P(yb/2 - 1)
-      if (s + 1 == P->snap_a) MT_CUDA_CHECK(cudaMemcpyAsync(P->d_snap.as<int64_t>(), P->d_run.p, 8, cudaMemcpyDeviceToDevice, st));
-      if (s + 1 == P->snap_h) MT_CUDA_CHECK(cudaMemcpyAsync(P->d_snap.as<int64_t>() + 1, P->d_run.p, 8, cudaMemcpyDeviceToDevice, st));
+                       P->tw.W));
+      // prefix snapshots P(bp - 1) at the breakpoints a/d, b/d
+      for (size_t i = 0; i < P->bp.size(); i++)
+        if (P->snap[i] == s + 1)
+          MT_CUDA_CHECK(cudaMemcpyAsync(P->d_snap.as<int64_t>() + i, P->d_run.p, 8, cudaMemcpyDeviceToDevice, st));
     }
     MT_CUDA_CHECK(cudaEventRecord(P->ev[2], st));
     MT_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -1150,12 +1212,17 @@ extern "C" int mt_plan_sieve_step(mt_plan* P, uint64_t max_tail_segments, int* d
   MT_CUDA_CHECK(cudaGetLastError());
   *done = P->tseg_next >= ns;
   if (*done) {
-    int64_t v[3] = {0, 0, 0};
+    int64_t v[9] = {0};
     MT_CUDA_CHECK(cudaMemcpy(v, P->d_run.p, 8, cudaMemcpyDeviceToHost));
-    MT_CUDA_CHECK(cudaMemcpy(v + 1, P->d_snap.p, 16, cudaMemcpyDeviceToHost));
-    P->p_end = v[0]; P->s_a = v[1]; P->s_h = v[2];
-    // this rank's M-total over [ya, yb): (own odd sum) - (half-range odd sum)
-    P->tail_total = ns ? (P->p_end - P->s_a) - P->s_h : 0;
+    MT_CUDA_CHECK(cudaMemcpy(v + 1, P->d_snap.p, 8 * 8, cudaMemcpyDeviceToHost));
+    P->p_end = v[0];
+    P->snapv.assign(v + 1, v + 1 + P->bp.size());
+    // this rank's M-total over [ya, yb): sum_d mu(d) (P(yb/d - 1) - P(ya/d - 1))
+    int64_t tt = 0;
+    if (ns)
+      for (int k = 0; k < P->tw.nd; k++)
+        tt += P->tw.s[k] * (P->snap_at(P->yb / P->tw.d[k]) - P->snap_at(P->ya / P->tw.d[k]));
+    P->tail_total = tt;
     P->phase = 1;
     if (m_head) *m_head = P->m_head;
     if (tail_total) *tail_total = P->tail_total;
@@ -1221,9 +1288,9 @@ static int read_u64(FILE* f, u64* v) {
 // P2 (u64 count + int32), small captures (u64 count + element bytes), head M,
 // running prefix and the two prefix snapshots (i64 each)
 static int ckpt_write(mt_plan* P, FILE* f) {
-  int64_t tail[4] = {P->m_head, 0, 0, 0};
+  int64_t tail[10] = {P->m_head, 0};
   MT_CUDA_CHECK(cudaMemcpy(tail + 1, P->d_run.p, 8, cudaMemcpyDeviceToHost));
-  MT_CUDA_CHECK(cudaMemcpy(tail + 2, P->d_snap.p, 16, cudaMemcpyDeviceToHost));
+  MT_CUDA_CHECK(cudaMemcpy(tail + 2, P->d_snap.p, 8 * 8, cudaMemcpyDeviceToHost));
   CkptHead h{};
   memcpy(h.magic, "MERTCKP1", 8);
   h.version = MT_CKPT_VERSION;
@@ -1240,8 +1307,9 @@ static int ckpt_write(mt_plan* P, FILE* f) {
   RC(write_all(f, &qn, 8));
   RC(write_dev(f, P->tdev[0].Q, qn * 4));
   const u64 pn = P->sj1[0] >= P->sj0[0] ? P->sj1[0] - P->sj0[0] + 1 : 0;
-  RC(write_all(f, &pn, 8));
-  RC(write_dev(f, P->d_P2[0].p, pn * 4));
+  const u64 pw = pn | ((u64)P->tw.W << 56);  // the tail wheel travels with the slice size
+  RC(write_all(f, &pw, 8));
+  for (int k = 0; k < P->nx(); k++) RC(write_dev(f, P->d_P[k].p, pn * 4));
   const u64 sb = P->nsmall * (P->cap32 ? 4 : 8);
   RC(write_all(f, &sb, 8));
   RC(write_dev(f, P->d_small.p, sb));
@@ -1286,22 +1354,26 @@ extern "C" int mt_plan_restore(mt_plan* P, const char* path) {
   }
   RC(read_dev(f, P->d_acc.p, P->NE * 8));
   RC(read_dev(f, P->d_mmc.p, P->NE * 4));
-  u64 qn = 0, pn = 0, sb = 0;
+  u64 qn = 0, pw = 0, sb = 0;
   RC(read_u64(f, &qn));
   const u64 qn_plan = P->jq1[0] >= P->jq0[0] ? P->jq1[0] - P->jq0[0] + 1 : 0;
   if (qn != qn_plan) { mt_set_error("checkpoint quotient table differs from this plan's"); return MT_ERR_CONTRACT; }
   RC(read_dev(f, P->tdev[0].Q, qn * 4));
-  RC(read_u64(f, &pn));
+  RC(read_u64(f, &pw));
+  const u64 pn = pw & ((1ull << 56) - 1);
   const u64 pn_plan = P->sj1[0] >= P->sj0[0] ? P->sj1[0] - P->sj0[0] + 1 : 0;
-  if (pn != pn_plan) { mt_set_error("checkpoint tail slice differs from this plan's"); return MT_ERR_CONTRACT; }
-  RC(read_dev(f, P->d_P2[0].p, pn * 4));
+  if (pn != pn_plan || (int)(pw >> 56) != P->tw.W) {
+    mt_set_error("checkpoint tail slice or wheel differs from this plan's");
+    return MT_ERR_CONTRACT;
+  }
+  for (int k = 0; k < P->nx(); k++) RC(read_dev(f, P->d_P[k].p, pn * 4));
   RC(read_u64(f, &sb));
   if (sb != P->nsmall * (P->cap32 ? 4 : 8)) { mt_set_error("checkpoint capture size differs"); return MT_ERR_CONTRACT; }
   RC(read_dev(f, P->d_small.p, sb));
-  int64_t tail[4];
+  int64_t tail[10];
   if (fread(tail, sizeof(tail), 1, f) != 1) { mt_set_error("checkpoint truncated"); return MT_ERR_CONTRACT; }
   MT_CUDA_CHECK(cudaMemcpy(P->d_run.p, tail + 1, 8, cudaMemcpyHostToDevice));
-  MT_CUDA_CHECK(cudaMemcpy(P->d_snap.p, tail + 2, 16, cudaMemcpyHostToDevice));
+  MT_CUDA_CHECK(cudaMemcpy(P->d_snap.p, tail + 2, 8 * 8, cudaMemcpyHostToDevice));
   P->m_head = tail[0];
   P->head_done = true;
   u64 s = 0;
@@ -1320,20 +1392,25 @@ extern "C" int mt_plan_restore(mt_plan* P, const char* path) {
   return MT_OK;
 }
 
-// phase 2: absolute M on this rank's tail slices: Q[j] = P(floor(n/j)) -
-// P(floor(n/(2j))) - P(ya - 1) + M(ya - 1), offset = M(ya - 1).  With world > 1
-// the capture window is then masked to the entries this rank owns, ready for
-// the caller's sum-reduction (mt_plan_cap_window).
+// phase 2: absolute M on this rank's tail slices: Q[j] = sum_d mu(d) (P(floor(n/(d j)))
+// - P(ya/d - 1)) + M(ya - 1), offset = M(ya - 1).  With world > 1 the capture window
+// is then masked to the entries this rank owns, ready for the caller's
+// sum-reduction (mt_plan_cap_window).
 extern "C" int mt_plan_tail_offset(mt_plan* P, int64_t offset) {
   if (P->phase < 1) { mt_set_error("tail_offset before sieve_update"); return MT_ERR_CONTRACT; }
   PLAN_DEV(P);
-  const int64_t delta = offset - P->s_a;
+  int64_t delta = offset;
+  if (!P->tsegs.empty())
+    for (int k = 0; k < P->tw.nd; k++) delta -= P->tw.s[k] * P->snap_at(P->ya / P->tw.d[k]);
   if (delta > INT32_MAX || delta < INT32_MIN) { mt_set_error("M offset beyond int32"); return MT_ERR_OVERFLOW; }
   for (int t = 0; t < P->N; t++) {
     if (P->sj0[t] > P->sj1[t]) continue;
     const u64 cnt = P->sj1[t] - P->sj0[t] + 1;
-    k_q_combine<<<(unsigned)((cnt + 255) / 256), 256, 0, P->st>>>(P->tdev[t].Q + (P->sj0[t] - P->jq0[t]),
-                                                                  P->d_P2[t].as<int>(), cnt, (int)delta);
+    CombineArgs ca{};
+    ca.n = P->nx();
+    for (int k = 0; k < ca.n; k++) { ca.T[k] = P->d_P[(size_t)t * P->nx() + k].as<int>(); ca.s[k] = P->tw.s[k + 1]; }
+    k_q_combine<<<(unsigned)((cnt + 255) / 256), 256, 0, P->st>>>(P->tdev[t].Q + (P->sj0[t] - P->jq0[t]), ca, cnt,
+                                                                  (int)delta);
     P->launches++;
     MT_CUDA_CHECK(cudaGetLastError());
   }

@@ -157,7 +157,7 @@ struct Sieve2Args {
   int64_t* tile_base;                         // [ntiles] M(tile start - 1)
   int* bkrel;                                 // head: tile-relative 32K block starts [ntiles*4]
   uint32_t tiles_per_cta;                     // persistent CTAs: contiguous tiles each
-  uint32_t odd;                               // odd-cell mode: cell c of the segment is y = Y0 + 2c + 1
+  uint32_t wheel;                             // 1: cell c = y; 2: odd y (y = 2c + 1); 6: y coprime to 6
   const CaptureTarget2* caps;
   int n_cap;
 };
@@ -173,11 +173,12 @@ struct Sieve2Host;
 int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cudaStream_t st);
 void mt_sieve2_destroy(Sieve2Host* h);
 // one segment [Y0, Y0 + ntiles*2^17): outputs as requested (null = skip)
-// odd = true: the segment's cells are the odd y of [Y0, Y0 + ntiles * 2^18) (tail
-// mode: sums and captures of the odd-y prefix; mu_out gets mu of the odd y)
+// wheel 2 / 6: the segment's cells are the odd y / the y coprime to 6 of
+// [Y0, Y0 + ntiles * 2^17 * (2 or 3)) (tail mode: sums and captures of the
+// wheel's prefix; mu_out gets mu of the cells)
 int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running, int8_t* mu_out,
                   int16_t* m16_out, int64_t* bk, uint8_t* states_out, const CaptureTarget2* caps,
-                  int n_cap, cudaStream_t st, KTimer* kt, bool odd = false);
+                  int n_cap, cudaStream_t st, KTimer* kt, int wheel = 1);
 uint64_t mt_sieve2_overflows(Sieve2Host* h);
 uint64_t mt_sieve2_launches(Sieve2Host* h, bool reset);
 #define MT_S2_TILE (1u << 17)

@@ -62,60 +62,80 @@ __device__ __forceinline__ void red_add(u32 saddr, u32 v) {
 __device__ __forceinline__ void red_or(u32 saddr, u32 v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
-// (-Y) mod p for p < 2^32, Y < 2^53, with r = 1/p rounded (host: 1.0/p)
-__device__ __forceinline__ u32 neg_mod(u64 Y, double Yd, double r, u32 p) {
-  u64 q = qdiv64(Yd, r, Y, p);
-  u32 rem = (u32)(Y - q * p);
-  return rem ? p - rem : 0u;
-}
 
-// first cell >= C0 hit by prime p.  Full mode: cells are y (y = 0 is never
-// marked).  Odd mode (the tail): cell c holds y = 2c + 1, and
-// p | 2c + 1  <=>  c == (p - 1)/2 (mod p), so the hits of p are the cells
-// (p - 1)/2 + p*t -- one plain stream of stride p, as in full mode.
-template <bool ODD>
-__device__ __forceinline__ u32 first_hit(u64 C0, double Cd, double r, u32 p) {
-  u32 j = neg_mod(C0, Cd, r, p);
-  if (ODD) {
-    const u64 jj = (u64)j + (p >> 1);
-    j = (u32)(jj >= p ? jj - p : jj);
-  } else if (C0 == 0 && j == 0) {
-    j = p;
+// ----------------------------------------------------------------------------
+// wheel modes of a segment.  Cell c of a tile starting at Yt:
+//   W = 1: y = Yt + c                  every y (the head)
+//   W = 2: y = Yt + 2c + 1             odd y (tail)
+//   W = 6: y = Yt + 3c + 1 + (c & 1)   y coprime to 6 (tail; Yt multiple of 6)
+// The hits of a prime p >= 5 (or of a square q = p^2) on the cells form NS
+// arithmetic streams of cell stride STRIDE: one stream of stride p (W = 1, 2;
+// W = 2: p | 2c + 1 <=> c == (p-1)/2 mod p) or two of stride 2p (W = 6: y = p*m,
+// m == 1 or 5 mod 6, at cells floor(p/3) and floor(5p/3) mod 2p).
+// ----------------------------------------------------------------------------
+template <int W> struct Wheel {
+  static constexpr int NS = W == 6 ? 2 : 1;
+  static constexpr u64 SPAN = (u64)S2_T * (W == 1 ? 1 : W == 2 ? 2 : 3);  // y per tile
+  __device__ static __forceinline__ u64 cell0(u64 Y) { return W == 1 ? Y : W == 2 ? Y >> 1 : Y / 3; }
+  __device__ static __forceinline__ u64 y_of(u64 c) { return W == 1 ? c : W == 2 ? 2 * c + 1 : 3 * c + 1 + (c & 1); }
+  // number of cells with y' - Yt <= o (the prefix length of a capture at y = Yt + o)
+  __device__ static __forceinline__ u64 ncell(u64 o) {
+    return W == 1 ? o + 1 : W == 2 ? (o + 1) >> 1 : 2 * (o / 6) + (o % 6 >= 1) + (o % 6 >= 5);
   }
-  return j;
+};
+
+// (-Y) mod m for m < 2^50, Y < 2^53, with r = 1/m rounded (host: 1.0/m)
+__device__ __forceinline__ u64 neg_mod64(u64 Y, double Yd, double r, u64 m) {
+  const u64 q = qdiv64(Yd, r, Y, m);
+  const u64 rem = Y - q * m;
+  return rem ? m - rem : 0;
 }
-// same for a square q = p^2 (q < 2^63)
-template <bool ODD>
-__device__ __forceinline__ u64 first_hit_sq(u64 C0, double Cd, u64 q) {
-  const u64 qq = qdiv64(Cd, __drcp_rn((double)q), C0, q);
-  const u64 rem = C0 - qq * q;
-  if (ODD) {
-    const u64 f = (rem ? q - rem : 0) + (q >> 1);
-    return f >= q ? f - q : f;
+__device__ __forceinline__ u32 neg_mod(u64 Y, double Yd, double r, u32 p) { return (u32)neg_mod64(Y, Yd, r, p); }
+
+// first cells >= C0 hit by modulus m (a prime or a square, m >= 5, coprime to 6
+// when W = 6): j[s] = the offset from C0 of stream s's first cell, j[s] < STRIDE.
+// rm = 1/m rounded (1/(2m) = rm/2 exactly).
+template <int W>
+__device__ __forceinline__ void first_hits(u64 C0, double Cd, double rm, u64 m, u64* j) {
+  if (W == 6) {
+    const u64 m2 = 2 * m;
+    const u64 r = neg_mod64(C0, Cd, 0.5 * rm, m2);
+    const u64 a = r + m / 3, b = r + (5 * m) / 3;
+    j[0] = a >= m2 ? a - m2 : a;
+    j[1] = b >= m2 ? b - m2 : b;
+  } else {
+    u64 r = neg_mod64(C0, Cd, rm, m);
+    if (W == 2) {
+      r += m >> 1;
+      if (r >= m) r -= m;
+    } else if (C0 == 0 && r == 0) {
+      r = m;  // y = 0 is never marked
+    }
+    j[0] = r;
   }
-  return rem ? q - rem : (C0 ? 0 : q);
 }
 
 // ----------------------------------------------------------------------------
-// bucket producer: every hit of a prime p > S2_T (log marks) and of p^2 > S2_T
-// (square flags) in the segment [Y0, Y0 + R), appended to the producer-private
+// bucket producer: every hit of a prime p > big_min (log marks) and of p^2 > S2_T
+// (square flags) in the segment's R cells, appended to the producer-private
 // list of its tile.  Entry = offset (17 bits) | value << 17 (value bit 7 = OR).
 // ----------------------------------------------------------------------------
 // Work is balanced by hits, not by primes: small primes hit the segment up
 // to 16x more often than large ones.  Each batch takes FBATCH of this
-// producer's primes, computes every prime's first hit and hit count (one
-// prime per thread) and cuts the hit runs into items of at most FITEM
-// consecutive multiples (an exclusive scan of items per prime; a thread finds
-// its item's prime by binary search).  Rounds of one item per thread follow.
+// producer's hit streams (NS per prime), computes every stream's first hit and
+// hit count (one stream per thread) and cuts the hit runs into items of at most
+// FITEM consecutive hits (an exclusive scan of items per stream; a thread finds
+// its item's stream by binary search).  Rounds of one item per thread follow.
 // Slots in a tile's list come from shared-memory counters; the entries are
 // write-combined in shared memory (`bin` per tile and round) and flushed as
 // runs (one bulk async copy per tile and round) instead of one 4-byte L2
 // write per hit (ncu: the scattered stores were 60% of the stalls).  Entries
 // past a full bin, and all square flags, are stored directly.
-#define FBATCH 1024  // primes per batch
+#define FBATCH 1024  // streams per batch
 #define FITEM 32     // hits per item (1024 items per round: ~32k hits over the tiles)
-template <bool ODD>
+template <int W>
 __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
+  constexpr int NS = Wheel<W>::NS;
   // dynamic: rcnt[ntiles + 1] (round counts; [ntiles] = dummy), gcnt[ntiles]
   // (entries before this round), cnt2[ntiles] (square flags), stage[ntiles][bin]
   extern __shared__ __align__(16) u32 dsm[];
@@ -128,7 +148,7 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
   __shared__ u32 s_q0[FBATCH];
   __shared__ u32 s_step[FBATCH];
   __shared__ u32 s_val[FBATCH];
-  __shared__ u32 s_ipre[FBATCH + 1];  // exclusive prefix of items per prime
+  __shared__ u32 s_ipre[FBATCH + 1];  // exclusive prefix of items per stream
   __shared__ u32 s_wsum[32];
   __shared__ u32 s_hits;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -136,35 +156,37 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
   const u32 nt = a.ntiles, bin = a.bin;
   if (tid == 0) s_hits = 0;
   for (u32 t = tid; t < 3 * nt + 1; t += blockDim.x) dsm[t] = 0;
-  const u64 Y0 = a.Y0;
-  const u64 C0 = ODD ? Y0 >> 1 : Y0;  // first cell of the segment (odd mode: cell c <-> y = 2c + 1)
-  const u32 R = nt * S2_T;  // <= 2^31
-  const double Yd = (double)C0;
+  const u64 C0 = Wheel<W>::cell0(a.Y0);  // first cell of the segment
+  const u32 R = nt * S2_T;                // cells, <= 2^31
+  const double Cd = (double)C0;
   u32* __restrict__ out = a.buf + (u64)b * nt * a.cap;
   const u32 cap = a.cap;
   // this producer's primes: log marks p_lo + b + k*NP, then squares q_lo + b + k*NP
   const u32 nlog = a.p_hi > a.p_lo + b ? (a.p_hi - a.p_lo - b + NP - 1) / NP : 0;
   const u32 nsq = a.q_hi > a.q_lo + b ? (a.q_hi - a.q_lo - b + NP - 1) / NP : 0;
-  const u32 nprim = nlog + nsq;
-  for (u32 base = 0; base < nprim; base += FBATCH) {
+  const u32 nstream = (nlog + nsq) * NS;
+  for (u32 base = 0; base < nstream; base += FBATCH) {
     __syncthreads();
-    // phase 1: first hit, step, value, item count of one prime per thread
+    // phase 1: first hit, step, value, item count of one stream per thread
     u32 c = 0;
     {
-      const u32 k = base + tid;
+      const u32 ks = base + tid, k = ks / NS, s = ks % NS;
       u32 q0 = R, step = 1, val = 0;
-      if (k < nprim) {
+      if (ks < nstream) {
+        u64 j[NS];
         if (k < nlog) {
           const u32 p = a.pperm[(u64)b * a.kp + k];  // producer-major copy: coalesced; 1/p and log recomputed
-          q0 = first_hit<ODD>(C0, Yd, __drcp_rn((double)p), p);
-          step = p;
+          first_hits<W>(C0, Cd, __drcp_rn((double)p), p, j);
+          q0 = (u32)(s ? j[NS - 1] : j[0]);
+          step = NS * p;
           val = ((32u - __clz(p - 1)) | 1u) << 17;  // ceil(log2 p) | 1
         } else {
           const u64 p = a.qperm[(u64)b * a.kq + (k - nlog)];
           const u64 q = p * p;
-          const u64 f = first_hit_sq<ODD>(C0, Yd, q);
-          q0 = f < R ? (u32)f : R;
-          step = q < R ? (u32)q : R;  // one hit at most when q >= R
+          first_hits<W>(C0, Cd, __drcp_rn((double)q), q, j);
+          const u64 js = s ? j[NS - 1] : j[0];
+          q0 = js < R ? (u32)js : R;
+          step = NS * q < R ? (u32)(NS * q) : R;  // one hit at most when the stride reaches R
           val = 0x80u << 17;
         }
         const u32 hits = q0 < R ? (R - 1 - q0) / step + 1 : 0;
@@ -317,6 +339,9 @@ __device__ __forceinline__ int mu_cell(u32 s, int thr) {
   return ((int)s > thr) ? 1 - 2 * par : 2 * par - 1;
 }
 
+// next tile's first offset of a stream whose first offset in this tile is j < stride
+__device__ __forceinline__ u32 carry(u32 j, u32 tm, u32 stride) { return j >= tm ? j - tm : j + stride - tm; }
+
 // ----------------------------------------------------------------------------
 // k_sieve3: persistent tile kernel.  CTA c sieves the contiguous tiles
 // [c*m, c*m + m) of the segment; the first multiple of every in-tile prime
@@ -325,20 +350,21 @@ __device__ __forceinline__ int mu_cell(u32 s, int thr) {
 // outputs are tile-relative; k_s3_finish makes them absolute.
 // ----------------------------------------------------------------------------
 
-template <bool ODD>
+template <int W>
 __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
-  constexpr u64 SPAN = ODD ? 2ull * S2_T : (u64)S2_T;  // y per tile
+  constexpr int NS = Wheel<W>::NS;
+  constexpr u64 SPAN = Wheel<W>::SPAN;
   extern __shared__ u32 st[];                   // S2_W state / mu words
   int* csum = (int*)(st + S2_W);                // S2_CH chunk sums -> exclusive chunk prefixes
   const u32 nA = a.p_warp_end - a.p_first;
   const u32 nBp = a.p_small_end - a.p_warp_end;
   const u32 nB1 = a.p_b2 - a.p_warp_end;        // B1 primes; [nB1, nBp) are B2
   const u32 nC = a.sq_end - a.sq_first;
-  u32* offA = (u32*)(csum + S2_CH);             // first multiple of p (lane 0's mark), A primes
-  u32* tmA = offA + nA;                         // T mod p
-  u32* offB = tmA + nA;                         // first multiple, B primes
-  u32* offC = offB + nBp;                       // first multiple of p^2, small squares
-  u32* tmC = offC + nC;                         // T mod p^2
+  u32* offA = (u32*)(csum + S2_CH);             // [NS][nA] first hit of each stream (lane 0's mark), A primes
+  u32* tmA = offA + NS * nA;                    // T mod stride
+  u32* offB = tmA + nA;                         // [NS][nBp] first hits, B primes
+  u32* offC = offB + NS * nBp;                  // [NS][nC] first hits of p^2, small squares
+  u32* tmC = offC + NS * nC;                    // T mod stride
   uint16_t* pB = (uint16_t*)(tmC + nC);         // B primes as (p - 1) / 2
   __shared__ int wsum[32];
   __shared__ int s_total;
@@ -355,29 +381,32 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
 
   // ---- first multiples at the CTA's first tile
   {
-    const u64 Y = a.Y0 + (u64)tile0 * SPAN;
-    const u64 C = ODD ? Y >> 1 : Y;
+    const u64 C = Wheel<W>::cell0(a.Y0 + (u64)tile0 * SPAN);
     const double Cd = (double)C;
+    u64 j[NS];
     for (u32 k = tid; k < nA; k += S2_NT) {
       const u32 i = a.p_first + k, p = a.primes[i];
-      offA[k] = first_hit<ODD>(C, Cd, a.rprimes[i], p);
-      tmA[k] = S2_T % p;
+      first_hits<W>(C, Cd, a.rprimes[i], p, j);
+      for (int s = 0; s < NS; s++) offA[s * nA + k] = (u32)j[s];
+      tmA[k] = S2_T % (NS * p);
     }
     for (u32 k = tid; k < nBp; k += S2_NT) {
       const u32 i = a.p_warp_end + k, p = a.primes[i];
-      offB[k] = first_hit<ODD>(C, Cd, a.rprimes[i], p);
+      first_hits<W>(C, Cd, a.rprimes[i], p, j);
+      for (int s = 0; s < NS; s++) offB[s * nBp + k] = (u32)j[s];
       pB[k] = (uint16_t)((p - 1) >> 1);
     }
     for (u32 k = tid; k < nC; k += S2_NT) {
       const u32 p = a.primes[a.sq_first + k], q = p * p;
-      offC[k] = first_hit<ODD>(C, Cd, __drcp_rn((double)q), q);
-      tmC[k] = S2_T % q;
+      first_hits<W>(C, Cd, __drcp_rn((double)q), q, j);
+      for (int s = 0; s < NS; s++) offC[s * nC + k] = (u32)j[s];
+      tmC[k] = S2_T % (NS * q);
     }
   }
 
   for (u32 tile = tile0; tile < tile_end; tile++) {
     const u64 Yt = a.Y0 + (u64)tile * SPAN;    // first y of the tile
-    const u64 Ct = ODD ? Yt >> 1 : Yt;         // first cell of the tile
+    const u64 Ct = Wheel<W>::cell0(Yt);        // first cell of the tile
     __syncthreads();  // offsets ready / previous tile's outputs done
     if (tid == 0) s_dnext = 0;
     // 1. presieve patterns
@@ -389,21 +418,24 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
     for (u32 b = tid; b < a.nprod && b < S2_MAXPROD; b += S2_NT) s_cnt[b] = a.counts[(u64)b * a.ntiles + tile];
     __syncthreads();
     // 2. marks
-    // A: warp per prime, snake order over the warps
+    // A: warp per prime (W = 6: half-warp per stream), snake order over the warps
     for (u32 r = 0; r * 32 < nA; r++) {
       const u32 k = r * 32 + ((r & 1) ? 31 - warp : warp);
       if (k >= nA) continue;
       const u32 i = a.p_first + k;
       const u32 p = a.primes[i];
       const u32 lg = a.logs[i];
-      const u32 j0 = offA[k];
-      const u32 j = j0 + lane * p;
+      const u32 stride = NS * p;
+      const int s = NS == 2 ? lane >> 4 : 0;
+      const u32 li = NS == 2 ? lane & 15 : lane;
+      const u32 j0 = offA[s * nA + k];
+      const u32 j = j0 + li * stride;
       const u32 v = lg << ((j & 3) * 8);
-      const u32 astep = 32 * p;
+      const u32 astep = 32 * p;  // (32 / NS) lanes x stride
 #pragma unroll 4
       for (u32 ad = sbase + (j & ~3u); ad < send; ad += astep) red_add(ad, v);
       __syncwarp();
-      if (lane == 0) { const u32 tm = tmA[k]; offA[k] = j0 >= tm ? j0 - tm : j0 + p - tm; }
+      if (li == 0) offA[s * nA + k] = carry(j0, tmA[k], stride);
     }
     // B: lane per prime, groups of 32 in snake order (single loop, predicated tail)
     //    B1 = [1024, S2_B2_MIN): four interleaved streams per prime
@@ -416,32 +448,46 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         if (k < nB1) {
           const u32 p = 2u * pB[k] + 1u;
           const u32 lg = (32 - __clz(p - 1)) | 1;
-          u32 j = offB[k];
-          const u32 j1 = j + p, j2 = j1 + p, j3 = j2 + p, p4 = 4 * p;
-          const u32 v0 = lg << ((j & 3) * 8), v1 = lg << ((j1 & 3) * 8);
-          const u32 v2 = lg << ((j2 & 3) * 8), v3 = lg << ((j3 & 3) * 8);
-          u32 a0 = sbase + (j & ~3u), a1 = sbase + (j1 & ~3u), a2 = sbase + (j2 & ~3u), a3 = sbase + (j3 & ~3u);
+          // streams in ascending order a0 < a1 < a2 < a3 < a0 + 4p, stepping 4p:
+          // W = 1, 2: j, j+p, j+2p, j+3p; W = 6: lo, hi, lo+2p, hi+2p of the two streams
+          u32 e0, e1, e2, e3;
+          if (NS == 2) {
+            const u32 x = offB[k], y = offB[nBp + k];
+            e0 = min(x, y); e1 = max(x, y); e2 = e0 + 2 * p; e3 = e1 + 2 * p;
+          } else {
+            e0 = offB[k]; e1 = e0 + p; e2 = e1 + p; e3 = e2 + p;
+          }
+          const u32 p4 = 4 * p;
+          const u32 v0 = lg << ((e0 & 3) * 8), v1 = lg << ((e1 & 3) * 8);
+          const u32 v2 = lg << ((e2 & 3) * 8), v3 = lg << ((e3 & 3) * 8);
+          u32 a0 = sbase + (e0 & ~3u), a1 = sbase + (e1 & ~3u), a2 = sbase + (e2 & ~3u), a3 = sbase + (e3 & ~3u);
           // streams past the tile end add into a per-lane scratch word (csum[lane],
           // rewritten by the classify pass) instead of branching around the reduction
           const u32 scratch = send + 4 * lane;  // csum[lane]: one word per lane, no contention
-          for (; a0 < send; a0 += p4, a1 += p4, a2 += p4, a3 += p4, j += p4) {
+          u32 jn = e0;
+          for (; a0 < send; a0 += p4, a1 += p4, a2 += p4, a3 += p4, jn += p4) {
             red_add(a0, v0);
             red_add(a1 < send ? a1 : scratch, v1);
             red_add(a2 < send ? a2 : scratch, v2);
             red_add(a3 < send ? a3 : scratch, v3);
           }
-          // j is stream 0's next multiple; the first multiple past the tile is
-          // one of j - 3p .. j (three conditional steps, no division)
-          u32 jn = j;
-          jn = jn - p >= S2_T && jn >= p ? jn - p : jn;
-          jn = jn - p >= S2_T && jn >= p ? jn - p : jn;
-          jn = jn - p >= S2_T && jn >= p ? jn - p : jn;
-          offB[k] = jn - S2_T;
+          if (NS == 2) {
+            const u32 tm = S2_T % (2 * p);
+            offB[k] = carry(offB[k], tm, 2 * p);
+            offB[nBp + k] = carry(offB[nBp + k], tm, 2 * p);
+          } else {
+            // jn is stream 0's next multiple; the first multiple past the tile is
+            // one of jn - 3p .. jn (three conditional steps, no division)
+            jn = jn - p >= S2_T && jn >= p ? jn - p : jn;
+            jn = jn - p >= S2_T && jn >= p ? jn - p : jn;
+            jn = jn - p >= S2_T && jn >= p ? jn - p : jn;
+            offB[k] = jn - S2_T;
+          }
         }
       }
     }
-    //    B2 = [S2_B2_MIN, big_min): at most T / S2_B2_MIN hits per tile, one plain
-    //    stream per prime (per-prime setup dominates here, so it is kept minimal)
+    //    B2 = [S2_B2_MIN, big_min): at most T / S2_B2_MIN hits per tile and stream,
+    //    plain streams (per-prime setup dominates here, so it is kept minimal)
     {
       const u32 nG = (nBp - nB1 + 31) / 32;
       for (u32 r = 0; r * 32 < nG; r++) {
@@ -451,19 +497,26 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
         if (k < nBp) {
           const u32 p = 2u * pB[k] + 1u;
           const u32 lg = (32 - __clz(p - 1)) | 1;
-          u32 j = offB[k];
-          for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), lg << ((j & 3) * 8));
-          offB[k] = j - S2_T;
+          const u32 stride = NS * p;
+#pragma unroll
+          for (int s = 0; s < NS; s++) {
+            u32 j = offB[s * nBp + k];
+            for (; j < S2_T; j += stride) red_add(sbase + (j & ~3u), lg << ((j & 3) * 8));
+            offB[s * nBp + k] = j - S2_T;
+          }
         }
       }
     }
-    // C: warp per small square
+    // C: warp per small square (W = 6: half-warp per stream)
     for (u32 k = warp; k < nC; k += 32) {
       const u32 p = a.primes[a.sq_first + k], q = p * p;
-      const u32 j0 = offC[k];
-      for (u32 j = j0 + lane * q; j < S2_T; j += 32 * q) red_or(sbase + (j & ~3u), 0x80u << ((j & 3) * 8));
+      const u32 stride = NS * q;
+      const int s = NS == 2 ? lane >> 4 : 0;
+      const u32 li = NS == 2 ? lane & 15 : lane;
+      const u32 j0 = offC[s * nC + k];
+      for (u32 j = j0 + li * stride; j < S2_T; j += 32 * q) red_or(sbase + (j & ~3u), 0x80u << ((j & 3) * 8));
       __syncwarp();
-      if (lane == 0) { const u32 tm = tmC[k]; offC[k] = j0 >= tm ? j0 - tm : j0 + q - tm; }
+      if (li == 0) offC[s * nC + k] = carry(j0, tmC[k], stride);
     }
     // D: bucket lists (primes > big_min, squares > 2^17), dealt to warps from a
     //    shared counter so warps that finished A-C early take more lists
@@ -501,15 +554,19 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
           }
         } else {  // overflowed list: this producer's hits on the tile, recomputed exactly
           if (lane == 0) atomicAdd(a.overflow, 1ull);
+          u64 j[NS];
           for (u64 i = (u64)a.p_lo + b + (u64)lane * a.nprod; i < a.p_hi; i += 32ull * a.nprod) {
             const u32 p = a.primes[i];
-            u32 j = first_hit<ODD>(Ct, Cd, a.rprimes[i], p);
-            for (; j < S2_T; j += p) red_add(sbase + (j & ~3u), (u32)a.logs[i] << ((j & 3) * 8));
+            first_hits<W>(Ct, Cd, a.rprimes[i], p, j);
+            for (int s = 0; s < NS; s++)
+              for (u64 jj = j[s]; jj < S2_T; jj += NS * p)
+                red_add(sbase + ((u32)jj & ~3u), (u32)a.logs[i] << (((u32)jj & 3) * 8));
           }
           for (u64 i = (u64)a.q_lo + b + (u64)lane * a.nprod; i < a.q_hi; i += 32ull * a.nprod) {
             const u64 p = a.primes[i];
-            const u64 j = first_hit_sq<ODD>(Ct, Cd, p * p);
-            if (j < S2_T) red_or(sbase + ((u32)j & ~3u), 0x80u << (((u32)j & 3) * 8));
+            first_hits<W>(Ct, Cd, __drcp_rn((double)(p * p)), p * p, j);
+            for (int s = 0; s < NS; s++)
+              if (j[s] < S2_T) red_or(sbase + ((u32)j[s] & ~3u), 0x80u << (((u32)j[s] & 3) * 8));
           }
         }
       }
@@ -522,8 +579,10 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
     }
     // 3. classify (warp w: words [w*1024, (w+1)*1024), lane l: 4 words per step)
     {
-      const bool uniform = Yt >= SPAN;  // the tile's y lie in one binade
+      // one threshold for the tile when its y lie in one binade (always for W = 1, 2
+      // and y >= SPAN; W = 6 tiles are not power-of-two aligned)
       const int thr_t = 62 - __clzll((long long)(Yt | 1));
+      const bool uniform = Yt >= SPAN && (63 - __clzll((long long)(Yt + SPAN - 1))) == thr_t + 1;
       const u32 kthr = uniform ? (u32)(127 - thr_t) * 0x01010101u : 0u;
       uint4* st4 = (uint4*)st;
 #pragma unroll 2
@@ -541,8 +600,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
           for (int k = 0; k < 4; k++) {
             u32 mw = 0;
             for (int bb = 0; bb < 4; bb++) {
-              const u64 cell = (u64)(q * 4 + k) * 4 + bb;
-              const u64 y = Yt + (ODD ? 2 * cell + 1 : cell);
+              const u64 y = Yt + Wheel<W>::y_of((u64)(q * 4 + k) * 4 + bb);
               const int thr = (y ? 63 - __clzll((long long)y) : 0) - 1;
               const int mm = mu_cell((wv[k] >> (8 * bb)) & 0xff, thr);
               s += mm;
@@ -593,7 +651,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
       u32* mo = (u32*)(a.mu_out + (u64)tile * S2_T);
       for (int i = tid; i < (int)S2_W; i += S2_NT) mo[i] = st[i];
     }
-    if (a.m16_out) {
+    if (W == 1 && a.m16_out) {
       if (tid < 4) a.bkrel[(u64)tile * 4 + tid] = csum[tid * 1024];
       int16_t* m16 = a.m16_out + (u64)tile * S2_T;
       for (int c = tid; c < (int)S2_CH; c += S2_NT) {
@@ -619,7 +677,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
       }
     }
     // 6. captures, tile-relative: Q_t[j] = (prefix at floor(n_t/j)) - (prefix at Yt - 1),
-    //    the prefix being M (full mode) or the odd-y sum (odd mode).  The j range of
+    //    the prefix being M (W = 1) or the wheel's cell sum (W = 2, 6).  The j range of
     //    every target on this tile is computed once per tile by one thread each.
     for (int t0 = 0; t0 < a.n_cap; t0 += S2_MAXCAP) {
       const int nc = min(a.n_cap - t0, S2_MAXCAP);
@@ -637,8 +695,7 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
       const u64 jlo = s_cj[0][t], jhi = s_cj[1][t];
       for (u64 j = jlo + tid; j <= jhi; j += S2_NT) {
         const u64 y = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, j);
-        // cells with y' <= y: o + 1 (full) or the odd y' in [Yt, y]: (o + 1) / 2 (odd)
-        const u32 ncell = ODD ? (u32)((y - Yt + 1) >> 1) : (u32)(y - Yt + 1);
+        const u32 ncell = (u32)Wheel<W>::ncell(y - Yt);  // cells with y' <= y
         if (ncell == 0) { ct.Q[j - ct.jq0] = 0; continue; }
         const u32 o = ncell - 1;
         const int c = o >> 5;
@@ -709,30 +766,39 @@ __global__ void __launch_bounds__(256) k_s3_finish(const int* __restrict__ tile_
 }
 
 // ------------------------------------------------------------------ host side
-int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
-  Sieve2Args a = g.tile;
-  const bool odd = a.odd != 0;
+template <int W>
+static void launch_segment(const Sieve2Args& a, const Bucket2Args& b, size_t bs, size_t smem, u32 grid,
+                           cudaStream_t st, KTimer* kt) {
   if (a.nprod) {
-    Bucket2Args b = g.bucket;
-    const size_t bs = (((3 * (size_t)b.ntiles + 1 + 3) & ~(size_t)3) + (size_t)b.ntiles * b.bin) * sizeof(u32);
     if (kt) kt->begin(KT_SIEVE_LARGE, st);
-    if (odd) k_bucket_fill<true><<<b.nprod_grid, 1024, bs, st>>>(b);
-    else k_bucket_fill<false><<<b.nprod_grid, 1024, bs, st>>>(b);
+    k_bucket_fill<W><<<b.nprod_grid, 1024, bs, st>>>(b);
     if (kt) kt->end(st);
-    MT_CUDA_CHECK(cudaGetLastError());
   }
-  const u32 nA = a.p_warp_end - a.p_first, nBp = a.p_small_end - a.p_warp_end, nC = a.sq_end - a.sq_first;
-  const size_t smem = S2_T + S2_CH * sizeof(int) + (size_t)(2 * nA + nBp + 2 * nC) * 4 + (size_t)nBp * 2 + 16;
-  const u32 grid = (a.ntiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
   if (kt) kt->begin(KT_SIEVE_TILE, st);
-  if (odd) k_sieve3<true><<<grid, S2_NT, smem, st>>>(a);
-  else k_sieve3<false><<<grid, S2_NT, smem, st>>>(a);
+  k_sieve3<W><<<grid, S2_NT, smem, st>>>(a);
   if (kt) kt->end(st);
-  MT_CUDA_CHECK(cudaGetLastError());
   if (kt) kt->begin(KT_OTHER, st);
   k_s3_finish<<<a.ntiles, 256, 0, st>>>(a.tile_sum, a.ntiles, a.running, a.bkrel, a.bk, a.caps, a.n_cap, a.Y0,
-                                        odd ? 2ull * S2_T : (u64)S2_T, a.tstate);
+                                        Wheel<W>::SPAN, a.tstate);
   if (kt) kt->end(st);
+}
+
+// shared memory of k_sieve3: the tile, chunk sums, and the in-tile primes' offsets
+static size_t sieve3_smem(const Sieve2Args& a) {
+  const u32 nA = a.p_warp_end - a.p_first, nBp = a.p_small_end - a.p_warp_end, nC = a.sq_end - a.sq_first;
+  const u32 ns = a.wheel == 6 ? 2 : 1;
+  return S2_T + S2_CH * sizeof(int) + (size_t)((ns + 1) * nA + ns * nBp + (ns + 1) * nC) * 4 + (size_t)nBp * 2 + 16;
+}
+
+int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
+  const Sieve2Args& a = g.tile;
+  const Bucket2Args& b = g.bucket;
+  const size_t bs = (((3 * (size_t)b.ntiles + 1 + 3) & ~(size_t)3) + (size_t)b.ntiles * b.bin) * sizeof(u32);
+  const size_t smem = sieve3_smem(a);
+  const u32 grid = (a.ntiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
+  if (a.wheel == 6) launch_segment<6>(a, b, bs, smem, grid, st, kt);
+  else if (a.wheel == 2) launch_segment<2>(a, b, bs, smem, grid, st, kt);
+  else launch_segment<1>(a, b, bs, smem, grid, st, kt);
   MT_CUDA_CHECK(cudaGetLastError());
   return MT_OK;
 }
@@ -771,16 +837,16 @@ uint8_t logp(u64 p) {  // ceil(log2 p) | 1  (sieve.py:111-121)
   for (u64 x = p - 1; x; x >>= 1) bl++;
   return (uint8_t)(bl | 1);
 }
-// byte pattern of period P replicated over 4P + T bytes, as words.  Full mode:
-// cell j is y = j (multiples of p at j == 0 mod p); odd mode: cell j is
-// y = 2j + 1 (odd multiples of p at j == (p-1)/2 mod p)
-std::vector<uint32_t> pattern_words(u64 P, const std::vector<u32>& logp_primes, const std::vector<u32>& sq,
-                                    bool odd = false) {
+// byte pattern of period P (cells) replicated over 4P + T bytes, as words: the
+// logs of `logp_primes` and the 0x80 flags of `sq` on the cells of wheel W
+// (cell c <-> y = c, 2c + 1 or 3c + 1 + (c & 1); P a multiple of each period)
+std::vector<uint32_t> pattern_words(u64 P, const std::vector<u32>& logp_primes, const std::vector<u32>& sq, int W) {
   std::vector<uint8_t> one(P, 0);
-  for (u32 p : logp_primes)
-    for (u64 j = odd ? p / 2 : 0; j < P; j += p) one[j] = (uint8_t)(one[j] + logp(p));
-  for (u32 q : sq)
-    for (u64 j = odd ? q / 2 : 0; j < P; j += q) one[j] |= 0x80;
+  for (u64 c = 0; c < P; c++) {
+    const u64 y = W == 1 ? c : W == 2 ? 2 * c + 1 : 3 * c + 1 + (c & 1);
+    for (u32 p : logp_primes) if (y % p == 0) one[c] = (uint8_t)(one[c] + logp(p));
+    for (u32 q : sq) if (y % q == 0) one[c] |= 0x80;
+  }
   const u64 nbytes = 4 * P + S2_T;
   std::vector<uint32_t> w(nbytes / 4);
   for (u64 i = 0; i < nbytes / 4; i++) {
@@ -793,13 +859,17 @@ std::vector<uint32_t> pattern_words(u64 P, const std::vector<u32>& logp_primes, 
 }  // namespace
 
 struct Sieve2Host {
-  Buf w1, w2, w1o, w2o, prm, rp, lg, buf, counts, tstate, ovf, tsum, tbase, bkrel;
+  // presieve patterns per wheel W (index 0: W = 1, 1: W = 2, 2: W = 6), periods in cells:
+  //   W = 1: 2^2 3^2 5^2 7^2 11 = 485100 (2,3,5,7,11; 4,9,25,49) and 13 17 19 23 = 96577
+  //   W = 2: 3^2 5^2 7^2 11 = 121275 (3,5,7,11; 9,25,49) and 96577
+  //   W = 6: 2 5^2 7^2 11 = 26950 (5,7,11; 25,49) and 2 x 96577 (two cells per 6 y)
+  Buf w1[3], w2[3], prm, rp, lg, buf, counts, tstate, ovf, tsum, tbase, bkrel;
+  u64 P1[3] = {485100, 121275, 26950}, P2[3] = {96577, 96577, 193154};
   int nsm = 148;
-  u64 P1 = 485100, P2 = 96577;  // 2^2 3^2 5^2 7^2 11, 13 17 19 23
-  u64 P1o = 121275;             // odd cells: 3^2 5^2 7^2 11 (P2 serves both modes)
   std::vector<u32> p;
   u32 nprod = 0, cap = 0, max_tiles = 0;
   u32 fill_smem = 0;  // dynamic shared memory available to k_bucket_fill
+  u32 sieve3_smem_max = 0;  // dynamic shared memory available to k_sieve3
   // bucket primes in producer-major order: pperm[b * kp + k] = p[P_lo + b + k * nprod]
   // (log marks), qperm[b * kq + k] = p[Q_lo + b + k * nprod] (square flags)
   Buf pperm, qperm;
@@ -838,10 +908,11 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
     MT_CUDA_CHECK(cudaStreamSynchronize(st));  // the host vector dies at return
     return MT_OK;
   };
-  if (up(h->w1, pattern_words(h->P1, {2, 3, 5, 7, 11}, {4, 9, 25, 49}))) return MT_ERR_RESOURCE;
-  if (up(h->w2, pattern_words(h->P2, {13, 17, 19, 23}, {}))) return MT_ERR_RESOURCE;
-  if (up(h->w1o, pattern_words(h->P1o, {3, 5, 7, 11}, {9, 25, 49}, true))) return MT_ERR_RESOURCE;
-  if (up(h->w2o, pattern_words(h->P2, {13, 17, 19, 23}, {}, true))) return MT_ERR_RESOURCE;
+  if (up(h->w1[0], pattern_words(h->P1[0], {2, 3, 5, 7, 11}, {4, 9, 25, 49}, 1))) return MT_ERR_RESOURCE;
+  if (up(h->w1[1], pattern_words(h->P1[1], {3, 5, 7, 11}, {9, 25, 49}, 2))) return MT_ERR_RESOURCE;
+  if (up(h->w1[2], pattern_words(h->P1[2], {5, 7, 11}, {25, 49}, 6))) return MT_ERR_RESOURCE;
+  for (int i = 0; i < 3; i++)
+    if (up(h->w2[i], pattern_words(h->P2[i], {13, 17, 19, 23}, {}, i == 0 ? 1 : i == 1 ? 2 : 6))) return MT_ERR_RESOURCE;
   if (const char* e = getenv("MT_S2_BIG_LOG2")) h->big_min = 1u << atoi(e);
   // bucket space: producers = SMs; capacity from the expected hits per (producer, tile)
   int dev, nsm;
@@ -893,17 +964,22 @@ int mt_sieve2_create(Sieve2Host** out, uint64_t y_last, uint32_t max_tiles, cuda
   {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa, fb;
-    MT_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_sieve3<false>));
-    MT_CUDA_CHECK(cudaFuncGetAttributes(&fb, k_sieve3<true>));
-    const int s3 = optin - (int)std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
-    MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s3));
-    MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s3));
-    MT_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_bucket_fill<false>));
-    MT_CUDA_CHECK(cudaFuncGetAttributes(&fb, k_bucket_fill<true>));
-    h->fill_smem = (u32)(optin - (int)std::max(fa.sharedSizeBytes, fb.sharedSizeBytes));
-    MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fill_smem));
-    MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fill_smem));
+    cudaFuncAttributes f1, f2, f6;
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&f1, k_sieve3<1>));
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&f2, k_sieve3<2>));
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&f6, k_sieve3<6>));
+    const int s3 = optin - (int)std::max({f1.sharedSizeBytes, f2.sharedSizeBytes, f6.sharedSizeBytes});
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s3));
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, s3));
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_sieve3<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, s3));
+    h->sieve3_smem_max = (u32)s3;
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&f1, k_bucket_fill<1>));
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&f2, k_bucket_fill<2>));
+    MT_CUDA_CHECK(cudaFuncGetAttributes(&f6, k_bucket_fill<6>));
+    h->fill_smem = (u32)(optin - (int)std::max({f1.sharedSizeBytes, f2.sharedSizeBytes, f6.sharedSizeBytes}));
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fill_smem));
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fill_smem));
+    MT_CUDA_CHECK(cudaFuncSetAttribute(k_bucket_fill<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fill_smem));
   }
   if (max_tiles > 16384) { mt_set_error("too many tiles per segment (max 2^31 cells)"); return MT_ERR_VALUE; }
   MT_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -920,11 +996,16 @@ uint64_t mt_sieve2_overflows(Sieve2Host* h) {
 
 int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running, int8_t* mu_out,
                   int16_t* m16_out, int64_t* bk, uint8_t* states_out, const CaptureTarget2* caps,
-                  int n_cap, cudaStream_t st, KTimer* kt, bool odd) {
+                  int n_cap, cudaStream_t st, KTimer* kt, int wheel) {
   if (ntiles == 0) return MT_OK;
-  const u64 span = odd ? 2ull * S2_T : (u64)S2_T;
-  if (ntiles > h->max_tiles || (Y0 % span)) { mt_set_error("bad sieve segment"); return MT_ERR_VALUE; }
-  if (odd && (m16_out || bk || Y0 < span)) { mt_set_error("odd-cell segments give mu and sums only (y >= 2^18)"); return MT_ERR_VALUE; }
+  if (wheel != 1 && wheel != 2 && wheel != 6) { mt_set_error("wheel must be 1, 2 or 6"); return MT_ERR_VALUE; }
+  const u64 span = (u64)S2_T * (wheel == 6 ? 3 : wheel);
+  const int wi = wheel == 1 ? 0 : wheel == 2 ? 1 : 2;
+  if (ntiles > h->max_tiles || (Y0 % span) || (wheel == 6 && Y0 % 6)) { mt_set_error("bad sieve segment"); return MT_ERR_VALUE; }
+  if (wheel != 1 && (m16_out || bk || Y0 < span)) {
+    mt_set_error("wheel segments give mu and sums only, above the first tile");
+    return MT_ERR_VALUE;
+  }
   const u64 y2 = Y0 + (u64)ntiles * span - 1;
   const std::vector<u32>& p = h->p;
   const u64 s = isqrt64(y2);  // p <= floor(sqrt(y2))  <=>  p*p <= y2
@@ -937,11 +1018,11 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
   a.tstate = (unsigned long long*)h->tstate.p;
   a.ticket = (uint32_t*)((unsigned long long*)h->tstate.p + ntiles);
   a.running = running;
-  a.odd = odd ? 1u : 0u;
-  a.w1 = (const u32*)(odd ? h->w1o.p : h->w1.p); a.w2 = (const u32*)(odd ? h->w2o.p : h->w2.p);
-  a.w1_period4 = 4 * (odd ? h->P1o : h->P1); a.w2_period4 = 4 * h->P2;
+  a.wheel = (u32)wheel;
+  a.w1 = (const u32*)h->w1[wi].p; a.w2 = (const u32*)h->w2[wi].p;
+  a.w1_period4 = 4 * h->P1[wi]; a.w2_period4 = 4 * h->P2[wi];
   a.primes = (const u32*)h->prm.p; a.rprimes = (const double*)h->rp.p; a.logs = (const uint8_t*)h->lg.p;
-  a.p_first = std::min(idx_gt(28), end);  // A primes start at 29 (2..23 are presieved; odd mode: 3..23)
+  a.p_first = std::min(idx_gt(28), end);  // A primes start at 29 (2..23 are presieved, or those of them >= the wheel's)
   a.p_warp_end = std::max(a.p_first, std::min(idx_gt(S2_A_MAX - 1), end));
   a.p_small_end = std::max(a.p_warp_end, std::min(idx_gt(h->big_min), end));
   a.p_b2 = std::max(a.p_warp_end, std::min(idx_gt(S2_B2_MIN - 1), a.p_small_end));
@@ -976,6 +1057,7 @@ int mt_sieve2_run(Sieve2Host* h, uint64_t Y0, uint32_t ntiles, int64_t* running,
     return MT_ERR_VALUE;
   }
   b.buf = (u32*)h->buf.p; b.counts = (u32*)h->counts.p;
+  if (sieve3_smem(a) > h->sieve3_smem_max) { mt_set_error("sieve tile needs more shared memory than the device has"); return MT_ERR_RESOURCE; }
   h->launches += (a.nprod ? 1 : 0) + 2;
   return mt_sieve2_segment(g, st, kt);
 }

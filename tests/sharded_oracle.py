@@ -10,11 +10,12 @@ mt_plan_*):
         + sum_{d=lo}^{dq_hi} Q[k d]                            Q-gather (any y)
 with Q[j] = M(floor(n/j)).  The head [0, Y_H) is sieved by every rank and
 captures Q directly.  The tail [Y_H, E) is split into w ranges [a, b)
-balanced by sieve work (tail_partition); rank r sieves only the odd y of
-[a/2, b/2) U [a, b) with one running prefix P (P(a/2 - 1) = 0) and captures
-P at floor(n/j) and floor(n/(2j)) for its own slice j; then
-  M(floor(n/j)) = P(floor(n/j)) - P(floor(n/(2j))) - P(a - 1) + M(a - 1),
-because M(x) = O(x) - O(floor(x/2)) with O the odd-y Moebius sum.
+balanced by sieve work (tail_partition); rank r sieves only the y coprime to
+the wheel W (2 or 6) of the union of [a/d, b/d), d | W, with one running
+prefix P, and captures P at floor(n/(d j)) for its own slice j; then
+  M(floor(n/j)) = sum_d mu(d) (P(floor(n/(d j))) - P(a/d - 1)) + M(a - 1),
+because M(x) = sum_{d | W} mu(d) C_W(floor(x/d)) with C_W the Moebius sum over
+the y coprime to W.
 The Q-gather of rank r reads only its own slice and every w-th element's
 items in the head part.  Work units are dealt to ranks by element index (the
 device deals them by work-unit index; either partition yields the same sums).
@@ -28,18 +29,29 @@ import torch
 from oracle import engine_port as E
 
 
-def tail_cost(a, b):
-    """mt_engine.cu tail_cost: y covered by a rank owning [a, b)."""
+WHEELS = {2: ((1, 2), (1, -1)), 6: ((1, 2, 3, 6), (1, -1, -1, 1))}
+
+
+def tail_union(a, b, W=6):
+    """mt_engine.cu tail_union: the merged y-intervals [a/d, b/d), d | W."""
     if b <= a:
-        return 0
-    h0, h1 = a // 2, b // 2
-    c = (b - a) + (h1 - h0)
-    if h1 > a:
-        c -= h1 - a
-    return c
+        return []
+    iv = sorted((a // d, b // d) for d in WHEELS[W][0])
+    out = []
+    for x in iv:
+        if out and x[0] <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], x[1])
+        else:
+            out.append([x[0], x[1]])
+    return out
 
 
-def tail_partition(H, E_, w, align):
+def tail_cost(a, b, W=6):
+    """mt_engine.cu tail_cost: y covered by a rank owning [a, b)."""
+    return sum(e - s for s, e in tail_union(a, b, W))
+
+
+def tail_partition(H, E_, w, align, W=6):
     """mt_engine.cu tail_partition: boundaries on `align` balancing tail_cost."""
     yb = [H] + [E_] * w
     if w <= 1 or E_ <= H:
@@ -51,16 +63,16 @@ def tail_partition(H, E_, w, align):
             lo, hi = 0, (E_ - a) // align
             while lo < hi:
                 mid = (lo + hi + 1) // 2
-                if tail_cost(a, a + mid * align) <= c:
+                if tail_cost(a, a + mid * align, W) <= c:
                     lo = mid
                 else:
                     hi = mid - 1
             a += lo * align
             if out is not None:
                 out[r + 1] = a
-        return tail_cost(a, E_) <= c
+        return tail_cost(a, E_, W) <= c
 
-    lo, hi = 0, tail_cost(H, E_)
+    lo, hi = 0, tail_cost(H, E_, W)
     while lo < hi:
         mid = (lo + hi) // 2
         if cover(mid):
@@ -76,8 +88,11 @@ class ShardedOraclePlan:
     device = torch.device("cpu")
     SENTINEL = -(1 << 30)
 
-    def __init__(self, ns, u, rank, world, Rh=1 << 12, align=1 << 10, capture=False):
+    def __init__(self, ns, u, rank, world, Rh=1 << 12, align=None, capture=False, W=6):
         self.ns, self.u, self.rank, self.world = list(ns), u, rank, world
+        self.W = W
+        self.D, self.S = WHEELS[W]
+        align = align or (3 << 10 if W == 6 else 1 << 10)  # every a/d an integer
         self.n_targets = len(self.ns)
         self.H = [E.HarmonicArray(n, u) for n in self.ns]
         ymc = max(int(h.mcut.max()) for h in self.H)
@@ -98,21 +113,20 @@ class ShardedOraclePlan:
             if act.any():
                 head_end = max(head_end, int((h.v[act] // lw[act]).max()))
         head_end = min(head_end, u)
-        segs = -(-(head_end + 1) // Rh)
-        while (segs * Rh) % align:
-            segs += 1
-        self.head_lim = segs * Rh
+        self.head_lim = -(-(head_end + 1) // align) * align
         self.tail_end = -(-(u + 1) // align) * align if u + 1 > self.head_lim else self.head_lim
-        self.ybound = tail_partition(self.head_lim, self.tail_end, world, align)
+        self.ybound = tail_partition(self.head_lim, self.tail_end, world, align, W)
         self.a, self.b = self.ybound[rank], self.ybound[rank + 1]
         self.tail_segs = sum(1 for r in range(world) if self.ybound[r + 1] > self.ybound[r])
         self.y_last = max(self.tail_end, self.head_lim) - 1
         self.M = E.mertens_table(self.y_last)  # M[y-1] = M(y)
         mu = np.diff(np.concatenate([[0], self.M]))
-        odd = np.arange(1, self.y_last + 1) % 2 == 1
-        self.O = np.cumsum(np.where(odd, mu, 0))  # O[y-1] = sum of mu over odd y' <= y
+        y = np.arange(1, self.y_last + 1)
+        keep = (y % 2 == 1) & ((y % 3 != 0) if W == 6 else True)
+        self.O = np.cumsum(np.where(keep, mu, 0))  # O[y-1] = sum of mu over the wheel's y' <= y
+        self.U = tail_union(self.a, self.b, W)
         self.Q = [np.full(max(0, self.J[t] - self.jq0[t] + 1), self.SENTINEL, np.int64) for t in range(self.n_targets)]
-        self.P2 = [None] * self.n_targets
+        self.PD = [None] * self.n_targets
         self._acc = [np.zeros(h.size, np.uint64) for h in self.H]
         self.capture = capture
 
@@ -125,16 +139,12 @@ class ShardedOraclePlan:
         return np.where(y >= 1, self.O[np.maximum(y, 1) - 1], 0)
 
     def Pof(self, x):
-        """This rank's running odd prefix P(x) over [a/2, b/2) U [a, b), P(a/2 - 1) = 0."""
-        a, b = self.a, self.b
-        h0, h1 = a // 2, b // 2
+        """This rank's running wheel prefix P(x) over the union of [a/d, b/d)."""
         x = np.asarray(x, dtype=np.int64)
-        base = self.Oof(h0 - 1)
-        if h1 > a:  # union [a/2, b): one continuous stretch
-            return self.Oof(np.minimum(x, b - 1)) - base
-        # disjoint: [a/2, b/2) then [a, b) with the gap skipped
-        p = self.Oof(np.minimum(x, h1 - 1)) - base
-        return p + np.where(x >= a, self.Oof(np.minimum(x, b - 1)) - self.Oof(a - 1), 0)
+        p = np.zeros(x.shape, np.int64)
+        for lo, hi in self.U:
+            p += np.where(x >= lo, self.Oof(np.minimum(x, hi - 1)) - self.Oof(lo - 1), 0)
+        return p
 
     def _slice(self, t, r):
         """j range of target t owned by rank r (mt_plan::q_slice)."""
@@ -172,23 +182,21 @@ class ShardedOraclePlan:
                 sl = self._slice(t, self.rank)
                 if sl:
                     i0, i1 = sl[0] - self.jq0[t], sl[1] - self.jq0[t] + 1
-                    self.Q[t][i0:i1] = self.Pof(y[i0:i1])        # P(floor(n/j))
-                    self.P2[t] = self.Pof((n_[t] // 2) // j[i0:i1])  # P(floor(n/(2j)))
+                    self.Q[t][i0:i1] = self.Pof(y[i0:i1])  # P(floor(n/j))
+                    self.PD[t] = [self.Pof((n_[t] // d) // j[i0:i1]) for d in self.D[1:]]  # P(floor(n/(dj)))
         m_head = int(self.Mof(self.head_lim - 1))
         if self.b <= self.a:
             self.s_a = 0
             return m_head, 0
-        self.s_a = int(self.Pof(self.a - 1))
-        s_h = int(self.Pof(self.b // 2 - 1))
-        p_end = int(self.Pof(self.b - 1))
-        return m_head, (p_end - self.s_a) - s_h
+        self.s_a = sum(s * int(self.Pof(self.a // d - 1)) for d, s in zip(self.D, self.S))
+        return m_head, sum(s * int(self.Pof(self.b // d - 1) - self.Pof(self.a // d - 1)) for d, s in zip(self.D, self.S))
 
     def tail_offset(self, off):
         for t in range(self.n_targets):
             sl = self._slice(t, self.rank)
             if sl:
                 i0, i1 = sl[0] - self.jq0[t], sl[1] - self.jq0[t] + 1
-                self.Q[t][i0:i1] = self.Q[t][i0:i1] - self.P2[t] + (int(off) - self.s_a)
+                self.Q[t][i0:i1] += sum(sg * pd for sg, pd in zip(self.S[1:], self.PD[t])) + (int(off) - self.s_a)
         if self.capture and len(self.Q[0]):  # mask the window to the entries this rank owns
             j = np.arange(self.jq0[0], self.J[0] + 1, dtype=np.int64)
             sl = self._slice(0, self.rank)

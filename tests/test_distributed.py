@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, ns, u, q, capture, skew):
+def _worker(rank, world, port, ns, u, q, capture, skew, W=6):
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
@@ -36,7 +36,7 @@ def _worker(rank, world, port, ns, u, q, capture, skew):
         from sharded_oracle import ShardedOraclePlan
 
         my_ns = [n + (rank if skew else 0) for n in ns]
-        plan = ShardedOraclePlan(my_ns, u, rank, world, capture=capture)
+        plan = ShardedOraclePlan(my_ns, u, rank, world, capture=capture, W=W)
         res = {}
         try:
             offs = D.run_phases(plan, None, res)
@@ -50,11 +50,11 @@ def _worker(rank, world, port, ns, u, q, capture, skew):
         dist.destroy_process_group()
 
 
-def _run(ns, u, world, capture=False, skew=False):
+def _run(ns, u, world, capture=False, skew=False, W=6):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, ns, u, q, capture, skew)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, ns, u, q, capture, skew, W)) for r in range(world)]
     for p in ps:
         p.start()
     out = []
@@ -76,28 +76,28 @@ def test_tail_offsets():
     assert D.tail_offsets(0, []) == []
 
 
-def test_tail_partition_balanced():
+@pytest.mark.parametrize("W", [2, 6])
+def test_tail_partition_balanced(W):
     from sharded_oracle import tail_cost, tail_partition
 
-    H, E, al = 1 << 20, 1 << 30, 1 << 12
+    H, E, al = 6 << 20, 6 << 30, 6 << 12
     for w in (1, 2, 3, 8):
-        yb = tail_partition(H, E, w, al)
+        yb = tail_partition(H, E, w, al, W)
         assert yb[0] == H and yb[-1] == E and all(b >= a for a, b in zip(yb, yb[1:]))
         assert all(y % al == 0 for y in yb)
-        costs = [tail_cost(a, b) for a, b in zip(yb, yb[1:])]
-        assert max(costs) - min(costs) <= 1.5 * al * w, costs
-        # every y of [H, E) is owned by exactly one range; rank r also covers [a/2, b/2)
+        costs = [tail_cost(a, b, W) for a, b in zip(yb, yb[1:])]
+        assert max(costs) - min(costs) <= 2 * al * w, costs
         assert sum(b - a for a, b in zip(yb, yb[1:])) == E - H
-    # one rank: the odd cells of [H/2, E), i.e. about half of what a full sieve of [H, E) touches
-    assert tail_cost(H, E) == E - H // 2
+    # one rank: the cells of [H/W, E), i.e. 1/2 (W = 2) or 1/3 (W = 6) of its y
+    assert tail_cost(H, E, W) == E - H // W
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_job_matches_single_process(oracle, world):
+@pytest.mark.parametrize("world,W", [(2, 6), (3, 6), (3, 2)])
+def test_sharded_job_matches_single_process(oracle, world, W):
     ns = [10**8, 10**8 + 7]
     u = oracle.choose_u(max(ns), len(ns))
     ref = oracle.mertens_exact_multi(ns)
-    out = _run(ns, u, world)
+    out = _run(ns, u, world, W=W)
     for rank, finals, offs, ybound, _ in out:
         assert sum(1 for a, b in zip(ybound, ybound[1:]) if b > a) == world  # every rank owns a tail range
         for n, f in zip(ns, finals):

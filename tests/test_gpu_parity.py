@@ -277,34 +277,53 @@ def test_production_sieve_stress_paths(engine, oracle, monkeypatch, env):
     assert np.array_equal(mu, ref), int((mu != ref).sum())
 
 
-@pytest.mark.parametrize("y1,length", [(1 << 18, 3 << 20), (10**9 - 123457, 3 << 20), (2**32 - 70000, 300001),
+def _coprime(y0, y2, wheel):
+    y = np.arange(y0, y2 + 1, dtype=np.int64)
+    return (y % 2 == 1) & ((y % 3 != 0) if wheel == 6 else True)
+
+
+@pytest.mark.parametrize("wheel", [2, 6])
+@pytest.mark.parametrize("y1,length", [(1 << 19, 3 << 20), (10**9 - 123457, 3 << 20), (2**32 - 70000, 300001),
                                        (4_641_588_833_612 - 10**6, 2 * 10**6),
                                        (82_036_050_574_571 - 10**6, 10**6), (464_158_883_361_277 - 10**6, 10**6)])
-def test_odd_tail_sieve_mu(engine, oracle, y1, length):
-    """The tail's odd-cell sieve (cell c = y 2c + 1: presieve patterns and every
-    prime stream re-phased to (p-1)/2 mod p) gives the reference's mu at every
-    odd y, on ranges up to the 1e22 job's u."""
+def test_wheel_tail_sieve_mu(engine, oracle, y1, length, wheel):
+    """The tail's wheel sieve (W = 2: cells are the odd y; W = 6: the y coprime to
+    6, two streams per prime; presieve patterns and every stream re-phased) gives
+    the reference's mu at every such y, on ranges up to the 1e22 job's u."""
     from paper_1108_0135_b200 import _lib
 
     y2 = y1 + length - 1
-    y0 = y1 | 1
-    mu = np.zeros((y2 - y0) // 2 + 1, np.int8)
-    _lib.check(_lib.lib().mt_sieve_odd(y1, y2, _lib.ptr(mu)))
-    ref = oracle.mu_range(oracle.get_kernels("c"), y0, y2)[::2]
+    keep = _coprime(y1, y2, wheel)
+    mu = np.zeros(int(keep.sum()), np.int8)
+    _lib.check(_lib.lib().mt_sieve_wheel(y1, y2, wheel, _lib.ptr(mu)))
+    ref = oracle.mu_range(oracle.get_kernels("c"), y1, y2)[keep]
     assert np.array_equal(mu, ref), int((mu != ref).sum())
 
 
+@pytest.mark.parametrize("wheel", [2, 6])
 @pytest.mark.parametrize("env", [{"MT_FILL_BIN": "16"}, {"MT_S2_CAP": "64"}])
-def test_odd_tail_sieve_stress_paths(engine, oracle, monkeypatch, env):
+def test_wheel_tail_sieve_stress_paths(engine, oracle, monkeypatch, env, wheel):
     from paper_1108_0135_b200 import _lib
 
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     y1, length = 4_641_588_833_612 - 10**6, 2 * 10**6
-    mu = np.zeros(length // 2, np.int8)
-    _lib.check(_lib.lib().mt_sieve_odd(y1, y1 + length - 1, _lib.ptr(mu)))
-    ref = oracle.mu_range(oracle.get_kernels("c"), y1 | 1, y1 + length - 1)[::2]
+    keep = _coprime(y1, y1 + length - 1, wheel)
+    mu = np.zeros(int(keep.sum()), np.int8)
+    _lib.check(_lib.lib().mt_sieve_wheel(y1, y1 + length - 1, wheel, _lib.ptr(mu)))
+    ref = oracle.mu_range(oracle.get_kernels("c"), y1, y1 + length - 1)[keep]
     assert np.array_equal(mu, ref), int((mu != ref).sum())
+
+
+def test_tail_wheel_2_and_6_agree(engine, golden, monkeypatch):
+    """The same jobs with the odd-y tail (MT_TAIL_WHEEL=2) and the default
+    coprime-to-6 tail: identical finals and quotients."""
+    G, J = golden
+    for w in ("2", "6"):
+        monkeypatch.setenv("MT_TAIL_WHEEL", w)
+        r = engine.mertens_exact(10**10)
+        assert np.array_equal(r._final, G["e10_final"]) and np.array_equal(r._cp_m, G["e10_cp_m"]), w
+        assert engine.mertens_exact(10**13).value == 599582, w
 
 
 def test_production_sieve_prefix(engine, oracle):
