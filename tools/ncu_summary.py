@@ -4,6 +4,7 @@ the metrics the roofline and DESIGN.md cite.
 
   python tools/ncu_summary.py launches <launches.csv>
   python tools/ncu_summary.py rep <file.ncu-rep> [...]
+  python tools/ncu_summary.py json <out.json> <file.ncu-rep> [...]   (profiles/ncu_metrics.json)
 """
 import csv
 import io
@@ -58,7 +59,53 @@ def rep(path):
                 print(f"  {w:70s} {v[h.index(w)]:>16s} {units[h.index(w)]}")
 
 
+def _num(x):
+    try:
+        return float(x.replace(",", ""))
+    except ValueError:
+        return None
+
+
+def to_json(out_path, paths):
+    """Per-kernel counters (one --set full capture each) for bench.py's roofline fields."""
+    import json
+    import os
+
+    res = {}
+    for path in paths:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        h = rows[0]
+        for v in rows[2:]:
+            g = lambda m: _num(v[h.index(m)]) if m in h else None  # noqa: E731
+            name = v[h.index("Kernel Name")].split("(")[0].split("<")[0].strip()
+            if name.startswith("void "):
+                name = name[5:]
+            dram = (g("dram__bytes_read.sum") or 0) + (g("dram__bytes_write.sum") or 0)
+            conf = sum(g(m) or 0 for m in WANT if "bank_conflicts" in m)
+            res[name] = {
+                "source": f"profiles/{os.path.basename(out_path)} <- ncu --set full --clock-control none, {os.path.basename(path)}",
+                "gpu_time_ms": (g("gpu__time_duration.sum") or 0) / 1e6,
+                "issue_active": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "warps_active": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                "pipe_alu": g("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                "pipe_fma": g("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                "pipe_fp64": g("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                "pipe_lsu": g("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+                "dram_bytes_per_launch": dram,
+                "dram_throughput_pct": g("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                "shared_bank_conflicts": conf,
+                "registers": g("launch__registers_per_thread"),
+                "grid": g("launch__grid_size"), "block": g("launch__block_size"),
+            }
+    json.dump(res, open(out_path, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "json":
+        to_json(sys.argv[2], sys.argv[3:])
+        sys.exit(0)
     f = {"launches": launches, "rep": rep}[sys.argv[1]]
     for p in sys.argv[2:]:
         f(p)
