@@ -313,6 +313,14 @@ extern "C" int mt_mertens_at(const uint64_t* pts, uint64_t npts, int64_t* m_out)
   return MT_OK;
 }
 
+// tiles per segment of the sieve parity ops (MT_TEST_TILES: smaller segments for
+// compute-sanitizer runs; default 256)
+static u64 test_tiles() {
+  const char* e = getenv("MT_TEST_TILES");
+  const u64 t = e ? strtoull(e, nullptr, 10) : 256;
+  return t >= 1 && t <= 4096 ? t : 256;
+}
+
 // production sieve over [y1, y2] (parity tests of mt_sieve2.cu): mu and, when
 // m_out is given, M(y) (then sieving starts at 0 so prefixes are absolute)
 __global__ void k_m16_to_m(const int16_t* __restrict__ M16, const int64_t* __restrict__ bk, u64 n,
@@ -323,7 +331,7 @@ __global__ void k_m16_to_m(const int16_t* __restrict__ M16, const int64_t* __res
 
 extern "C" int mt_sieve_fast(uint64_t y1, uint64_t y2, int8_t* mu_out, int64_t* m_out) {
   if (y2 < y1) { mt_set_error("bad range"); return MT_ERR_VALUE; }
-  const u64 T = MT_S2_TILE, NT = 256, R = T * NT;
+  const u64 T = MT_S2_TILE, NT = test_tiles(), R = T * NT;
   u64 Y0 = m_out ? 0 : (y1 / T) * T;
   const u64 y_last = ((y2 / R) + 1) * R + Y0;
   Sieve2Host* h = nullptr;
@@ -360,7 +368,7 @@ static u64 wheel_ncell(int W, u64 o) {
 // such y in ascending order
 extern "C" int mt_sieve_wheel(uint64_t y1, uint64_t y2, int wheel, int8_t* mu_out) {
   if (wheel != 2 && wheel != 6) { mt_set_error("wheel must be 2 or 6"); return MT_ERR_VALUE; }
-  const u64 SPAN = (u64)MT_S2_TILE * (wheel == 2 ? 2 : 3), NT = 256, RY = SPAN * NT;
+  const u64 SPAN = (u64)MT_S2_TILE * (wheel == 2 ? 2 : 3), NT = test_tiles(), RY = SPAN * NT;
   if (y2 < y1 || y1 < SPAN) { mt_set_error("bad range (the wheel sieve needs y1 >= one tile)"); return MT_ERR_VALUE; }
   u64 Y0 = (y1 / SPAN) * SPAN;
   const u64 first = wheel_ncell(wheel, y1 - 1 - Y0);  // cells of [Y0, y1)

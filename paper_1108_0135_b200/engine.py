@@ -91,6 +91,10 @@ class EngineConfig:
     distributed: bool = False
     stream: int | None = None      # cudaStream_t (int) to run on; None: the engine's own
     checkpoint_seconds: float = 300.0  # with checkpoint_path: after the head, then at most this often
+    # dense full quotient map (capture-all for large n): write it to int32 files
+    # `<path>.qmap.i32` / `<path>.small.i32` and return memory-mapped views instead
+    # of host arrays (at 1e19 each is 12.6 GB)
+    quotient_map_path: str | None = None
 
     def effective_workers(self) -> int:
         return self.workers if self.workers > 0 else (os.cpu_count() or 1)
@@ -307,7 +311,7 @@ def _run_checkpointed(L, job, res, config: EngineConfig, restore_from=None):
 
 
 def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None, cap32=False,
-             restore_from=None):
+             restore_from=None, cap_out=None, small_out=None):
     """One exact job (mt_run, or the plan phases over the process group when
     one is up); returns (finals per n, cap_m, small_m, raw stats)."""
     L = _lib.require_device()
@@ -324,10 +328,12 @@ def _run_job(ns, u, config: EngineConfig, cap_c=None, cap_small=0, acc_out=None,
     res.finals = finals.ctypes.data_as(_lib._pi64)
     cap_m = small_m = None
     if cap_c is not None and cap_c[1] >= cap_c[0]:
-        cap_m = np.zeros(cap_c[1] - cap_c[0] + 1, dtype=cdt)
+        cap_m = cap_out if cap_out is not None else np.zeros(cap_c[1] - cap_c[0] + 1, dtype=cdt)
+        assert cap_m.dtype == cdt and len(cap_m) == cap_c[1] - cap_c[0] + 1
         res.cap_m_out = cap_m.ctypes.data_as(_lib._pi64)
     if cap_small:
-        small_m = np.zeros(cap_small + 1, dtype=cdt)
+        small_m = small_out if small_out is not None else np.zeros(cap_small + 1, dtype=cdt)
+        assert small_m.dtype == cdt and len(small_m) == cap_small + 1
         res.small_m_out = small_m.ctypes.data_as(_lib._pi64)
     if acc_out is not None:
         res.acc_out = acc_out.ctypes.data_as(_lib._pu64)
@@ -395,7 +401,15 @@ def _mertens_exact(n: int, config: EngineConfig | None = None, restore_from: str
         # capture-all (engine.py:242-252) as a dense map instead of ~2*sqrt(n)
         # (q, M) pairs: M(n//c) for K < c <= s from the quotient table, M(y) for
         # y <= s from the head sieve, both int32 (|M(y)| < 2^31 for y <= u)
-        finals, qmap, small, raw = _run_job([n], u, config, (K + 1, s), s, cap32=True, restore_from=restore_from)
+        qo = so = None
+        if config.quotient_map_path:  # memory-mapped int32 files instead of host arrays
+            qo = np.memmap(config.quotient_map_path + ".qmap.i32", dtype=np.int32, mode="w+", shape=(s - K,))
+            so = np.memmap(config.quotient_map_path + ".small.i32", dtype=np.int32, mode="w+", shape=(s + 1,))
+        finals, qmap, small, raw = _run_job([n], u, config, (K + 1, s), s, cap32=True, restore_from=restore_from,
+                                            cap_out=qo, small_out=so)
+        if qo is not None:
+            qo.flush()
+            so.flush()
         st = _stats_from(raw, u, n, config)
         return MertensResult(n, int(finals[0][0]), u, finals[0], stats=st, elapsed=time.perf_counter() - t0,
                              backend=BACKEND_NAME, qmap=qmap, small=small)
@@ -490,21 +504,39 @@ def mertens_naive(n: int, config: EngineConfig | None = None, checkpoints=None):
     return m_final, np.array([lut.get(int(q), 0) for q in cp.tolist()], dtype=np.int64)
 
 
-def mertens_identity_residual(result: MertensResult) -> int:
-    """sum_{x=1..n} M(floor(n/x)) - 1 over the quotient map (engine.py:606-616)."""
+def mertens_identity_residual(result: MertensResult, chunk: int = 1 << 24) -> int:
+    """sum_{x=1..n} M(floor(n/x)) - 1 over the quotient map (engine.py:606-616).
+    The dense map (capture-all for large n, possibly memory-mapped) is summed in
+    chunks of `chunk` entries (no n-sized temporaries) modulo 2^64."""
     n = result.n
-    if result._qmap is not None and n < 2**63:  # dense map: vectorised over c <= isqrt(n) and y <= isqrt(n)
+    if result._qmap is not None and n < 2**63:
         s = isqrt(n)
         K = len(result._final)
-        c = np.arange(1, s + 1, dtype=np.int64)
-        q = n // c
-        mult_c = n // q - n // (q + 1)  # number of x with floor(n/x) = q
-        mc = np.concatenate([result._final.astype(np.int64), result._qmap.astype(np.int64)])[:s]
-        tot = int((mult_c * mc).sum())
-        ymax = min(int(q[-1]) - 1, s)  # quotients below floor(n/s); y in (s, n//s) has multiplicity 0
-        y = np.arange(1, ymax + 1, dtype=np.int64)
-        mult_y = n // y - n // (y + 1)
-        tot += int((mult_y * result._small[1:ymax + 1].astype(np.int64)).sum())
+        tot = 0
+        # c <= isqrt(n): multiplicity of q = n // c is n//q - n//(q+1)
+        for c0 in range(1, s + 1, chunk):
+            c = np.arange(c0, min(s, c0 + chunk - 1) + 1, dtype=np.int64)
+            q = n // c
+            mult = n // q - n // (q + 1)
+            i0, i1 = c0 - 1, c0 - 1 + len(c)  # index into finals ++ qmap
+            parts = []
+            if i0 < K:
+                parts.append(result._final[i0:min(i1, K)].astype(np.int64))
+            if i1 > K:
+                parts.append(np.asarray(result._qmap[max(i0, K) - K:i1 - K]).astype(np.int64))
+            m = np.concatenate(parts) if len(parts) > 1 else parts[0]
+            tot += int((mult * m).sum())
+        # y < floor(n/s): the quotients below the c-range, multiplicity n//y - n//(y+1)
+        ymax = min(n // s - 1, s)
+        for y0 in range(1, ymax + 1, chunk):
+            y = np.arange(y0, min(ymax, y0 + chunk - 1) + 1, dtype=np.int64)
+            mult = n // y - n // (y + 1)
+            tot += int((mult * np.asarray(result._small[y0:y0 + len(y)]).astype(np.int64)).sum())
+        # int64 products and chunk sums wrap mod 2^64 (exact there); the identity's
+        # total is small, so the signed residue mod 2^64 is the exact value
+        tot %= 1 << 64
+        if tot >= 1 << 63:
+            tot -= 1 << 64
         return tot - 1
     total = 0
     for _, q, m in result.quotients():

@@ -493,6 +493,23 @@ def test_dense_full_quotient_map(engine, oracle):
     assert r.quotient(10) == engine.mertens_exact(10**13).value == 599582
 
 
+@pytest.mark.slow
+def test_dense_quotient_map_memmap_1e16(engine, tmp_path):
+    """North_star's "all M(floor(n/c))" as a streamed output: the dense map written
+    to memory-mapped int32 files (quotient_map_path), the identity over the whole
+    map summed in chunks = 0, and sampled quotients against the paper / oracle."""
+    from math import isqrt
+
+    n = 10**16
+    path = str(tmp_path / "e16")
+    r = engine.mertens_exact(n, engine.EngineConfig(quotient_budget=10**12, quotient_map_path=path))
+    assert r.value == -3195437 and isinstance(r._qmap, np.memmap) and isinstance(r._small, np.memmap)
+    assert len(r._qmap) == isqrt(n) - len(r._final) and len(r._small) == isqrt(n) + 1
+    assert engine.mertens_identity_residual(r, chunk=1 << 22) == 0
+    assert r.quotient(10) == -3216373 and r.quotient(1000) == 599582  # M(1e15), M(1e13)
+    assert r.quotient(10**8) == int(r._small[10**8]) == 1928  # M(1e8)
+
+
 def test_checkpoint_resume(engine, golden, tmp_path):
     """Checkpoint after the head and between tail segments, then resume
     (engine.py:646-741): identical finals and quotients; the file starts with the
