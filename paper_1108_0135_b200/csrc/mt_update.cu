@@ -456,7 +456,16 @@ __device__ __forceinline__ void mbar_wait(u32 bar, u32 phase) {
       : "memory");
 }
 
-__global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
+#ifndef DW_NT
+#define DW_NT 256   // threads per window-walk CTA (one 64 KB window each)
+#endif
+#ifndef DW_MINB
+#define DW_MINB 1
+#endif
+#ifndef DW_CTAS
+#define DW_CTAS 3   // resident window-walk CTAs per SM (64 KB of shared memory each)
+#endif
+__global__ void __launch_bounds__(DW_NT, DW_MINB) k_dwin(WinArgs a) {
   extern __shared__ __align__(128) int4 smem_win[];
   int16_t* sw = (int16_t*)smem_win;
   const u32 swbase = (u32)__cvta_generic_to_shared(sw);
@@ -494,13 +503,13 @@ __global__ void __launch_bounds__(256) k_dwin(WinArgs a) {
     const i64 base = a.bk[w];
     const bool wide = a.G.wide[g] || a.force_wide;
     const u64 e0g = a.G.start[g], e1 = a.G.start[g + 1];
-    // groups smaller than the CTA: S = 256/A threads per element, each walking a
+    // groups smaller than the CTA: S = DW_NT/A threads per element, each walking a
     // contiguous slice of the element's d-range in this window
     const u32 A = (u32)(e1 - e0g);
-    const u32 S = A < 256 ? 256 / A : 1;
-    const u32 slice = A < 256 ? tid / A : 0;
-    const u64 efirst = A < 256 ? e0g + tid % A : e0g + tid;
-    for (u64 e = efirst; e < e1 && slice < S; e += (A < 256 ? e1 : 256)) {
+    const u32 S = A < DW_NT ? DW_NT / A : 1;
+    const u32 slice = A < DW_NT ? tid / A : 0;
+    const u64 efirst = A < DW_NT ? e0g + tid % A : e0g + tid;
+    for (u64 e = efirst; e < e1 && slice < S; e += (A < DW_NT ? e1 : DW_NT)) {
       const u64 xc = a.E.xcut[e];
       u64 lw = a.E.lo_w[e];
       const u64 sp = a.E.d_sp[e];
@@ -813,7 +822,7 @@ int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const 
     WinArgs a{E, c->acc, c->G, c->guoff, c->gwfirst, M16, bk, Y0, c->counter + 1,
               c->sh.rank, c->sh.world, (c->sh.flags & MT_FLAG_FORCE_WIDE) ? 1u : 0u};
     c->kt->begin(KT_DWIN, st);
-    k_dwin<<<c->nsm * 3, 256, MT_BLK * 2, st>>>(a);
+    k_dwin<<<c->nsm * DW_CTAS, DW_NT, MT_BLK * 2, st>>>(a);
     c->kt->end(st);
     c->launches++;
     MT_CUDA_CHECK(cudaGetLastError());

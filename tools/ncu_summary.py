@@ -75,9 +75,15 @@ def to_json(out_path, paths):
     for path in paths:
         out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(out)))
-        h = rows[0]
+        h, units = rows[0], rows[1]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                 "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9}
         for v in rows[2:]:
-            g = lambda m: _num(v[h.index(m)]) if m in h else None  # noqa: E731
+            def g(m):
+                if m not in h:
+                    return None
+                x = _num(v[h.index(m)])
+                return None if x is None else x * scale.get(units[h.index(m)], 1)
             name = v[h.index("Kernel Name")].split("(")[0].split("<")[0].strip()
             if name.startswith("void "):
                 name = name[5:]
