@@ -114,6 +114,16 @@ int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, double* ms_out);
 int mt_udiv128_batch(const uint64_t* v_lo, const uint64_t* v_hi, const uint64_t* m, uint64_t n,
                      uint64_t* q_lo, uint64_t* q_hi);
 
+/* the paper's approximate algorithm (Eq. 2):
+ * out[j] = q_n = 2 sum_{i<n_terms} a[i] cos(z[i] * delta_j + b[i]) in fp64, over a
+ * shifted table (b[i] = b'_i for the table's x0; delta = ln x - x0).
+ * mt_q_batch: the grid delta_j = delta0 + j * step, j < count (rotation recurrence
+ * re-seeded every 32 points); mt_q_points: arbitrary delta[j]. */
+int mt_q_batch(const double* z, const double* a, const double* b, uint64_t n_terms, double delta0,
+               double step, uint64_t count, double* out);
+int mt_q_points(const double* z, const double* a, const double* b, uint64_t n_terms, const double* delta,
+                uint64_t count, double* out);
+
 /* ---- 2. job-level production entry ----------------------------------------- */
 
 typedef struct {

@@ -6,7 +6,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(HERE, "csrc", f) for f in ("mt_engine.cu", "mt_sieve.cu", "mt_sieve2.cu", "mt_update.cu")]
+SRC = [os.path.join(HERE, "csrc", f) for f in ("mt_engine.cu", "mt_sieve.cu", "mt_sieve2.cu", "mt_update.cu", "mt_qsum.cu")]
 OUT = os.path.join(HERE, "libmertens_sm100.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
