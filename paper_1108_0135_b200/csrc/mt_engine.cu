@@ -627,22 +627,6 @@ __global__ void k_group_meta(const u64* __restrict__ gstart, u64 ng, const u64* 
   if (threadIdx.x == 0) { ylo[g] = rmn; yhi[g] = rmx; wide[g] = (uint8_t)sw; }
 }
 
-__global__ void k_tile_meta(u64 n_elem, const u64* __restrict__ mcut, const uint8_t* __restrict__ vbits,
-                            u64* __restrict__ tmax, uint8_t* __restrict__ tbits) {
-  u64 t = blockIdx.x;
-  u64 e = t * MT_CT + threadIdx.x;
-  u64 m = 0;
-  int b = 0;
-  if (e < n_elem) { m = mcut[e]; b = vbits[e]; }
-  typedef cub::BlockReduce<u64, MT_CT> BR;
-  typedef cub::BlockReduce<int, MT_CT> BRi;
-  __shared__ typename BR::TempStorage s1;
-  __shared__ typename BRi::TempStorage s2;
-  u64 mx = BR(s1).Reduce(m, cub::Max());
-  int bx = BRi(s2).Reduce(b, cub::Max());
-  if (threadIdx.x == 0) { tmax[t] = mx; tbits[t] = (uint8_t)bx; }
-}
-
 // per-target reductions: max mcut, sum mcut, sum dense items, max windowed y
 __global__ void k_elem_stats(u64 n_elem, const uint32_t* __restrict__ tgt, const u64* __restrict__ mcut,
                              const u64* __restrict__ xcut, const u64* __restrict__ lo,
@@ -833,9 +817,9 @@ struct mt_plan {
   u64 counted_items = 0, dense_items = 0, Ymc = 0;
   // elements
   DevBuf d_nlo, d_nhi, d_e0, d_vd, d_vlo, d_vhi, d_vb, d_k, d_tgt, d_D, d_x, d_mc, d_lo, d_low, d_dq,
-      d_acc, d_mmc, d_dsp, d_J, d_gs, d_gylo, d_gyhi, d_gw, d_tmax, d_tbits, d_fin;
+      d_acc, d_mmc, d_dsp, d_J, d_gs, d_gylo, d_gyhi, d_gw, d_fin;
   std::vector<u64> gstart;
-  u64 ng = 0, ntiles = 0;
+  u64 ng = 0;
   // quotient tables Q_t[j - jq0] = M(floor(n_t/j)), j in [jq0, jq1]
   std::vector<u64> J, jq0, jq1;
   std::vector<DevBuf> d_Q;
@@ -1056,10 +1040,6 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   if (head_end > u) head_end = u;
   P->head_end = head_end;
 
-  // tiles metadata for the counted walk
-  const u64 ntiles = P->ntiles = (NE + MT_CT - 1) / MT_CT;
-  RC(dalloc(P->d_tmax, ntiles * 8)); RC(dalloc(P->d_tbits, ntiles));
-  if (ntiles) k_tile_meta<<<(unsigned)ntiles, MT_CT, 0, st>>>(NE, P->d_mc.as<u64>(), P->d_vb.as<uint8_t>(), P->d_tmax.as<u64>(), P->d_tbits.as<uint8_t>());
 
   // ---- segments (production sieve tiles of 2^17 cells)
   // default tail segment = 6 tiles per SM (the persistent sieve CTAs each take 6
@@ -1130,8 +1110,8 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   E.lo = P->d_lo.as<u64>(); E.lo_w = P->d_low.as<u64>(); E.dq_hi = P->d_dq.as<u64>(); E.d_sp = P->d_dsp.as<u64>(); E.n = NE;
   Shard sh;
   sh.rank = P->rank; sh.world = P->world; sh.flags = P->flags;
-  RC(mt_update_create(&P->uc, E, P->d_acc.as<u64>(), P->d_mmc.as<int32_t>(), P->d_tmax.as<u64>(), P->d_tbits.as<uint8_t>(),
-                      ntiles, P->tdev.data(), N, grp, sh, &P->kt, st));
+  RC(mt_update_create(&P->uc, E, P->d_acc.as<u64>(), P->d_mmc.as<int32_t>(), P->K.data(), P->tdev.data(), N, grp, sh,
+                      &P->kt, st));
   MT_CUDA_CHECK(cudaStreamSynchronize(st));
   P->ms_setup = ms_since(T0);
   return MT_OK;

@@ -11,7 +11,9 @@
 #define MT_WHEEL 13860u
 #define MT_WHEEL_WORDS (MT_WHEEL / 4)
 #define MT_CT 256               // elements per counted-walk tile (threads per CTA)
-#define MT_CM 2048              // m values per counted-walk work unit
+#ifndef MT_CM
+#define MT_CM 2048              // list capacity of a counted-walk work unit (odd m of 2*MT_CM consecutive m)
+#endif
 #define MT_BLK 32768u           // M16 block: values stored relative to M(block start - 1)
 #define MT_WIN_SPLIT 64         // d_sp = ceil(sqrt(v)/64): windowed walk up to y ~ 64 sqrt(v)
 
@@ -220,9 +222,23 @@ struct Shard {
   uint32_t rank = 0, world = 1;
   uint32_t flags = 0;  // MT_FLAG_* (force-wide arithmetic paths for tests)
 };
-int mt_update_create(UpdateCtx** ctx, const ElemDev& E, uint64_t* acc, int32_t* Mmc,
-                     const uint64_t* tile_mcut_max, const uint8_t* tile_vbits_max,
-                     uint64_t ntiles, const TargetDev* tgts, int ntgt, const GroupDev& grp,
+// counted-walk entries (mt_update.cu): the elements, then the virtual halves
+// v = floor(v_k / 2) of the elements with 2k > K; each adds S_o(v, lim1) to acc[t1]
+// and subtracts S_o(v, lim2) from acc[t2] (t = 0xFFFFFFFF: none)
+struct CountedEntries {
+  double* vd;
+  uint64_t* vlo;
+  uint64_t* vhi;
+  uint8_t* vbits;
+  uint64_t* lim1;
+  uint64_t* lim2;
+  uint32_t* t1;
+  uint32_t* t2;
+  uint64_t n;
+};
+// Kt: K of every target (host), in element order
+int mt_update_create(UpdateCtx** ctx, const ElemDev& E, uint64_t* acc, int32_t* Mmc, const uint64_t* Kt,
+                     const TargetDev* tgts, int ntgt, const GroupDev& grp,
                      const Shard& sh, KTimer* kt, cudaStream_t st);
 void mt_update_destroy(UpdateCtx* ctx);
 int mt_update_head_segment(UpdateCtx* ctx, uint64_t Y0, uint64_t R, const int8_t* mu,

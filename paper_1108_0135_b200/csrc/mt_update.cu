@@ -11,9 +11,10 @@
 // (floor(v/(mcut+1)) <= xcut always), so it needs only mu(m) != 0 (61% of m),
 // one exact division per item and no prefix values.  acc_k is therefore
 // computed as (all mod 2^64):
-//   counted  : tiles of (256 elements x 2048 m) per head segment; the tile's
+//   counted  : tiles of (256 entries x 4096 m) per head segment; the tile's odd
 //              squarefree m are staged in shared memory as (1/m, m) and every
-//              thread walks them with the fp64-reciprocal exact division.
+//              thread walks them with the fp64-reciprocal exact division (the
+//              even m come from element 2k's walk: S(v,x) = S_o(v,x) - S_o(v/2,x/2)).
 //   windowed : dense items whose quotient y = v/d lies in the head, gathered
 //              from the segment's M array (load-balanced item ranges).
 //   Q-gather : dense items with k*d <= J read M(floor(n/(kd))) straight from
@@ -33,8 +34,9 @@ struct UpdateCtx {
   ElemDev E;
   uint64_t* acc;
   int32_t* Mmc;
-  const uint64_t* tile_mcut_max;
-  const uint8_t* tile_vbits_max;
+  CountedEntries C;          // counted-walk entries (elements + virtual halves)
+  uint64_t* tile_max;        // [ntiles] max walk limit of each MT_CT-entry tile
+  uint8_t* tile_vbits;       // [ntiles] max bit length of v in the tile
   uint64_t ntiles;
   TargetDev* tgts;  // device
   std::vector<TargetDev> tgts_h;  // host copy (windows are set per Q-gather pass)
@@ -60,19 +62,71 @@ struct UpdateCtx {
 };
 
 // ---------------------------------------------------------------- counted walk
-__global__ void k_counted_plan(const uint64_t* __restrict__ tile_mcut_max, uint64_t ntiles, u64 Y0,
+// Odd-m form (round 2).  With S(v, x) = sum_{m<=x} mu(m) floor(v/m) and S_o the
+// same sum over odd m only, mu(2m') = -mu(m') for odd m' and floor(v/(2m')) =
+// floor(floor(v/2)/m') give
+//   S(v, x) = S_o(v, x) - S_o(floor(v/2), floor(x/2)),
+// and floor(v_k/2) = v_{2k}.  So the counted sum of element k,
+//   C_k = S(v_k, mcut_k) = S_o(v_k, mcut_k) - S_o(v_{2k}, floor(mcut_k/2)),
+// needs only odd m, and its second term is a prefix of element 2k's own odd walk.
+// Every "counted entry" walks the odd squarefree m up to max(lim1, lim2) and adds
+//   + S_o(v, lim1) to acc[t1]   (its own C_k part, lim1 = mcut_k)
+//   - S_o(v, lim2) to acc[t2]   (the half part of element k/2: lim2 = floor(mcut_{k/2}/2))
+// Entries 0..NE-1 are the elements; elements with 2k > K get a virtual entry
+// v = floor(v_k/2), lim1 = 0, lim2 = floor(mcut_k/2), t2 = k.  The work drops from
+// 6/pi^2 to 4/pi^2 of the m per element (plus the virtual halves): 24 % fewer items.
+// Work units are (tile of MT_CT entries) x (MT_CU consecutive m, i.e. MT_CM odd m).
+#define MT_CU (2 * MT_CM)  // m per counted unit (its odd m fill one list of MT_CM)
+
+__global__ void k_counted_plan(const uint64_t* __restrict__ tile_max, uint64_t ntiles, u64 Y0,
                                u64 R, uint64_t* __restrict__ units) {
   u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (t > ntiles) return;
   if (t == ntiles) { units[t] = 0; return; }
-  u64 mx = tile_mcut_max[t];
+  u64 mx = tile_max[t];
   u64 n = 0;
   if (mx >= Y0 && mx >= 1) {
-    n = (mx - Y0) / MT_CM + 1;
-    u64 cap = R / MT_CM;
+    n = (mx - Y0) / MT_CU + 1;
+    u64 cap = R / MT_CU;
     if (n > cap) n = cap;
   }
   units[t] = n;
+}
+
+// counted entries from the elements (one thread per element): the element's own
+// entry at e, and for 2k > K its virtual half entry at vbase[t] + (k - floor(K/2) - 1)
+__global__ void k_ce_init(ElemDev E, const u64* __restrict__ Kt, const u64* __restrict__ vbase, CountedEntries C) {
+  const u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E.n) return;
+  const u64 k = E.k[e];
+  const uint32_t t = E.tgt[e];
+  const u64 K = Kt[t];
+  const u64 mc = E.mcut[e];
+  C.vd[e] = E.vd[e]; C.vlo[e] = E.vlo[e]; C.vhi[e] = E.vhi[e]; C.vbits[e] = E.vbits[e];
+  C.lim1[e] = mc; C.t1[e] = (u32)e;
+  if (k % 2 == 0) { C.lim2[e] = E.mcut[e - k / 2] / 2; C.t2[e] = (u32)(e - k / 2); }
+  else { C.lim2[e] = 0; C.t2[e] = 0xFFFFFFFFu; }
+  if (2 * k > K) {  // v_{2k} = floor(v_k / 2) < 2^64 (2k > K = floor(n/u): v_{2k} <= 2u)
+    const u64 c = vbase[t] + (k - K / 2 - 1);
+    const u64 vh = (E.vhi[e] << 63) | (E.vlo[e] >> 1);
+    C.vd[c] = __ull2double_rn(vh); C.vlo[c] = vh; C.vhi[c] = 0; C.vbits[c] = (uint8_t)(vh ? 64 - __clzll((long long)vh) : 0);
+    C.lim1[c] = 0; C.t1[c] = 0xFFFFFFFFu;
+    C.lim2[c] = mc / 2; C.t2[c] = (u32)e;
+  }
+}
+
+__global__ void k_ce_tiles(CountedEntries C, uint64_t* __restrict__ tmax, uint8_t* __restrict__ tbits) {
+  const u64 t = blockIdx.x, c = t * MT_CT + threadIdx.x;
+  u64 m = 0;
+  int b = 0;
+  if (c < C.n) { m = max(C.lim1[c], C.lim2[c]); b = C.vbits[c]; }
+  typedef cub::BlockReduce<u64, MT_CT> BR;
+  typedef cub::BlockReduce<int, MT_CT> BRi;
+  __shared__ typename BR::TempStorage s1;
+  __shared__ typename BRi::TempStorage s2;
+  const u64 mx = BR(s1).Reduce(m, cub::Max());
+  const int bx = BRi(s2).Reduce(b, cub::Max());
+  if (threadIdx.x == 0) { tmax[t] = mx; tbits[t] = (uint8_t)bx; }
 }
 
 __device__ __forceinline__ u64 upper_idx(const uint64_t* __restrict__ off, u64 n, u64 x) {
@@ -104,10 +158,10 @@ __device__ __forceinline__ u64 upper_idx_warp(const uint64_t* __restrict__ off, 
 }
 
 struct CountedArgs {
-  ElemDev E;
+  CountedEntries C;
   uint64_t* acc;
-  const uint64_t* tile_mcut_max;
-  const uint8_t* tile_vbits_max;
+  const uint64_t* tile_max;
+  const uint8_t* tile_vbits;
   const uint64_t* off;  // [ntiles+1] exclusive scan of units
   uint64_t ntiles;
   const int8_t* mu;     // segment mu
@@ -116,14 +170,14 @@ struct CountedArgs {
   u32 rank, world, force_wide;
 };
 
-// One element's walk over the unit's squarefree lists (all paths).  Returns
-// the signed sum S; the caller adds it to acc[e].
-__device__ __forceinline__ u64 counted_one(const CountedArgs& a, u64 e, u64 tau, u64 mlo, u64 mhi, int bp_, int bn_,
+// S_o over the first bp plus-list and bn minus-list entries for one entry (all
+// paths; the caller picks it for units off the fast path).  Returns the signed sum.
+__device__ __noinline__ u64 counted_one(const CountedArgs& a, u64 c, u64 tau, u64 mlo, u64 mhi, int bp_, int bn_,
                                            const double* rmL, const u32* mL) {
   const u64 mhw = mlo & 0xFFFFFFFF00000000ull;  // high word shared by the chunk
-  const double vd = a.E.vd[e];
-  const u64 vlo = a.E.vlo[e];
-  const int vb = a.tile_vbits_max[tau];
+  const double vd = a.C.vd[c];
+  const u64 vlo = a.C.vlo[c];
+  const int vb = a.tile_vbits[tau];
   const bool ok = !(a.force_wide & MT_FLAG_FORCE_SLOWDIV) && ((vb <= 50) || (mlo >= (1ull << (vb - 50))));
   if (ok && mhi <= (1ull << 31) && !(a.force_wide & MT_FLAG_FORCE_WIDE)) {
     const u32 v32 = (u32)vlo;
@@ -160,8 +214,8 @@ __device__ __forceinline__ u64 counted_one(const CountedArgs& a, u64 e, u64 tau,
     }
     return (ap - cp) - (an - cn);
   }
-  // exact slow path (small m with wide v)
-  const u64 vhi = a.E.vhi[e];
+  // exact path (small m with wide v): reciprocal 128/64 division with correction
+  const u64 vhi = a.C.vhi[c];
   u64 sp = 0, sn = 0;
   for (int i = 0; i < bp_; i++) sp += (u64)udiv128(vlo, vhi, mhw | (0u - mL[i]));
   for (int i = 0; i < bn_; i++) sn += (u64)udiv128(vlo, vhi, mhw | (0u - mL[MT_CM - 1 - i]));
@@ -180,10 +234,76 @@ __device__ __forceinline__ int count_le(const u32* mL, u64 mhw, int tot, u64 mc,
   return lo;
 }
 
-// Two elements per thread (e and e + MT_CT/2 of the unit's tile): every list
+// fast-path walks over list entries [i0, i1): two entries jointly (every entry
+// read from shared memory serves both) or one alone.  Sums of the estimates'
+// double bits and counts of negative 32-bit remainders (the corrections).
+template <bool MINUS>
+__device__ __forceinline__ void walk2(const double* rmL, const u32* mL, int i0, int i1, double vdA, u32 vA,
+                                      double vdB, u32 vB, u64& pA, u32& cA, u64& pB, u32& cB) {
+#pragma unroll 8
+  for (int i = i0; i < i1; i++) {
+    const int idx = MINUS ? MT_CM - 1 - i : i;
+    const double r = rmL[idx];
+    const u32 m = mL[idx];
+    const u64 bA = (u64)__double_as_longlong(fma(vdA, r, MT_TWO52));
+    const u64 bB = (u64)__double_as_longlong(fma(vdB, r, MT_TWO52));
+    pA += bA; cA += (vA + (u32)bA * m) >> 31;
+    pB += bB; cB += (vB + (u32)bB * m) >> 31;
+  }
+}
+template <bool MINUS>
+__device__ __forceinline__ void walk1(const double* rmL, const u32* mL, int i0, int i1, double vd, u32 v, u64& p,
+                                      u32& c) {
+#pragma unroll 2
+  for (int i = i0; i < i1; i++) {
+    const int idx = MINUS ? MT_CM - 1 - i : i;
+    const u64 b = (u64)__double_as_longlong(fma(vd, rmL[idx], MT_TWO52));
+    p += b; c += (v + (u32)b * mL[idx]) >> 31;
+  }
+}
+
+// one list (plus or minus) for the thread's two entries with prefix lengths
+// (lA1, lA2) and (lB1, lB2): the walk is cut at every prefix end, the two entries
+// walk jointly while both still need entries, and each prefix's value
+// (sum of floor(v/m) = bits - L*2^52*... - corrections) is recorded
+template <bool MINUS>
+__device__ __forceinline__ void walk_list(const double* rmL, const u32* mL, double vdA, u32 vA, double vdB, u32 vB,
+                                          int lA1, int lA2, int lB1, int lB2, u64* outA, u64* outB) {
+  int cut[4] = {lA1, lA2, lB1, lB2};
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3 - i; j++)
+      if (cut[j] > cut[j + 1]) { const int t = cut[j]; cut[j] = cut[j + 1]; cut[j + 1] = t; }
+  // distinct positive cuts, ascending: in the common case every thread has one
+  // (the whole list), so the walks of a warp stay in lockstep
+  int nc = 0, cc[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+    if (cut[i] > 0 && (i == 0 || cut[i] != cut[i - 1])) { cc[nc] = cut[i]; nc++; }
+  const int mA = max(lA1, lA2), mB = max(lB1, lB2);
+  u64 pA = 0, pB = 0;
+  u32 cA = 0, cB = 0;
+  int pos = 0;
+  outA[0] = outA[1] = outB[0] = outB[1] = 0;
+#pragma unroll 1
+  for (int k = 0; k < nc; k++) {
+    const int c = cc[k];
+    if (mA > pos && mB > pos) walk2<MINUS>(rmL, mL, pos, c, vdA, vA, vdB, vB, pA, cA, pB, cB);
+    else if (mA > pos) walk1<MINUS>(rmL, mL, pos, c, vdA, vA, pA, cA);
+    else walk1<MINUS>(rmL, mL, pos, c, vdB, vB, pB, cB);
+    pos = c;
+    const u64 vAv = pA - (u64)c * MT_EXP52 - cA, vBv = pB - (u64)c * MT_EXP52 - cB;
+    if (c == lA1) outA[0] = vAv;
+    if (c == lA2) outA[1] = vAv;
+    if (c == lB1) outB[0] = vBv;
+    if (c == lB2) outB[1] = vBv;
+  }
+}
+
+// Two entries per thread (c and c + MT_CT/2 of the unit's tile): every list
 // entry read from shared memory serves both walks, which cuts the loads and
-// loop overhead per item (the walk is issue-bound: ncu 70 % issue-active, with
-// LSU at 35 % and ALU at 57 % of peak in the one-element version).
+// loop overhead per item (the walk is issue-bound).
 #define CT_THREADS (MT_CT / 2)
 #ifndef CT_MINB
 #define CT_MINB 1
@@ -205,21 +325,21 @@ __global__ void __launch_bounds__(CT_THREADS, CT_MINB) k_counted(CountedArgs a) 
     if (unit >= total) break;
     if (tid == 0) nxt = atomicAdd((unsigned long long*)a.counter, 1ull) * a.world + a.rank;
     const u64 tau = upper_idx_warp(a.off, a.ntiles + 1, unit);
-    const u64 c = unit - a.off[tau];
-    const u64 mlo = a.Y0 + c * MT_CM;
-    u64 mhi = mlo + MT_CM;  // exclusive
-    const u64 mx = a.tile_mcut_max[tau];
+    const u64 cu = unit - a.off[tau];
+    const u64 mlo = a.Y0 + cu * MT_CU;  // even (Y0 and MT_CU are)
+    u64 mhi = mlo + MT_CU;  // exclusive
+    const u64 mx = a.tile_max[tau];
     if (mhi > mx + 1) mhi = mx + 1;
 
-    // ---- build the squarefree lists: plus from the front, minus from the back
-    constexpr int PER = MT_CM / CT_THREADS;  // 16 m per thread
+    // ---- the unit's odd squarefree m: plus from the front, minus from the back
+    constexpr int PER = MT_CU / CT_THREADS;  // 32 m (16 odd) per thread
     const u64 m0 = mlo + (u64)tid * PER;
     u64 bits[PER / 8];
 #pragma unroll
     for (int q = 0; q < PER / 8; q++) bits[q] = m0 + 8 * q < mhi ? *(const u64*)(a.mu + (m0 + 8 * q - a.Y0)) : 0;
     int np = 0, nn = 0;
 #pragma unroll
-    for (int b = 0; b < PER; b++) {
+    for (int b = 1; b < PER; b += 2) {  // odd m only (m0 is even)
       const int8_t mu = (int8_t)((bits[b >> 3] >> (8 * (b & 7))) & 0xff);
       const bool in = m0 + b < mhi;
       np += (in && mu > 0);
@@ -242,94 +362,60 @@ __global__ void __launch_bounds__(CT_THREADS, CT_MINB) k_counted(CountedArgs a) 
     }
     int op = bp + ip - np, on = bn + in_ - nn;
 #pragma unroll
-    for (int b = 0; b < PER; b++) {
+    for (int b = 1; b < PER; b += 2) {
       const int8_t mu = (int8_t)((bits[b >> 3] >> (8 * (b & 7))) & 0xff);
       const u64 m = m0 + b;
       if (m < mhi && mu != 0) {
         const double r = __drcp_rn((double)m);
         if (mu > 0) { rmL[op] = r; mL[op] = 0u - (u32)m; op++; }
-        else { const int idx = MT_CM - 1 - on; rmL[idx] = r; mL[idx] = 0u - (u32)m; on++; }  // chunks never straddle 2^32
+        else { const int idx = MT_CM - 1 - on; rmL[idx] = r; mL[idx] = 0u - (u32)m; on++; }  // units never straddle 2^32
       }
     }
     __syncthreads();
 
-    // ---- the two elements' walks
+    // ---- the two entries' walks: prefix lengths for (lim1, lim2) in both lists
     const u64 mhw = mlo & 0xFFFFFFFF00000000ull;
-    const u64 eA = tau * MT_CT + tid, eB = eA + CT_THREADS;
-    bool actA = false, actB = false;
-    int bpA = 0, bnA = 0, bpB = 0, bnB = 0;
-    if (eA < a.E.n) {
-      const u64 mc = a.E.mcut[eA];
-      if (mc >= mlo) {
-        actA = true;
-        bpA = totp; bnA = totn;
-        if (mc + 1 < mhi) { bpA = count_le(mL, mhw, totp, mc, false); bnA = count_le(mL, mhw, totn, mc, true); }
-      }
+    const u64 cA = tau * MT_CT + tid, cB = cA + CT_THREADS;
+    int pA1 = 0, pA2 = 0, nA1 = 0, nA2 = 0, pB1 = 0, pB2 = 0, nB1 = 0, nB2 = 0;
+    u32 tA1 = 0xFFFFFFFFu, tA2 = 0xFFFFFFFFu, tB1 = 0xFFFFFFFFu, tB2 = 0xFFFFFFFFu;
+    auto lens = [&](u64 lim, int& pl, int& nl) {
+      if (lim < mlo) { pl = nl = 0; return; }
+      if (lim + 1 >= mhi) { pl = totp; nl = totn; return; }
+      pl = count_le(mL, mhw, totp, lim, false);
+      nl = count_le(mL, mhw, totn, lim, true);
+    };
+    if (cA < a.C.n) {
+      tA1 = a.C.t1[cA]; tA2 = a.C.t2[cA];
+      if (tA1 != 0xFFFFFFFFu) lens(a.C.lim1[cA], pA1, nA1);
+      if (tA2 != 0xFFFFFFFFu) lens(a.C.lim2[cA], pA2, nA2);
     }
-    if (eB < a.E.n) {
-      const u64 mc = a.E.mcut[eB];
-      if (mc >= mlo) {
-        actB = true;
-        bpB = totp; bnB = totn;
-        if (mc + 1 < mhi) { bpB = count_le(mL, mhw, totp, mc, false); bnB = count_le(mL, mhw, totn, mc, true); }
-      }
+    if (cB < a.C.n) {
+      tB1 = a.C.t1[cB]; tB2 = a.C.t2[cB];
+      if (tB1 != 0xFFFFFFFFu) lens(a.C.lim1[cB], pB1, nB1);
+      if (tB2 != 0xFFFFFFFFu) lens(a.C.lim2[cB], pB2, nB2);
     }
-    const int vb = a.tile_vbits_max[tau];
+    const int vb = a.tile_vbits[tau];
     const bool fast = !(a.force_wide & (MT_FLAG_FORCE_SLOWDIV | MT_FLAG_FORCE_WIDE)) &&
                       ((vb <= 50) || (mlo >= (1ull << (vb - 50)))) && mhi <= (1ull << 31);
-    if (fast && actA && actB) {
-      const double vdA = a.E.vd[eA], vdB = a.E.vd[eB];
-      const u32 vA = (u32)a.E.vlo[eA], vB = (u32)a.E.vlo[eB];
-      u64 pA = 0, pB = 0, nA = 0, nB = 0;
-      u32 cpA = 0, cpB = 0, cnA = 0, cnB = 0;
-      const int jp = min(bpA, bpB), jn = min(bnA, bnB);
-#pragma unroll 8
-      for (int i = 0; i < jp; i++) {
-        const double r = rmL[i];
-        const u32 m = mL[i];
-        const u64 bA = (u64)__double_as_longlong(fma(vdA, r, MT_TWO52));
-        const u64 bB = (u64)__double_as_longlong(fma(vdB, r, MT_TWO52));
-        pA += bA; cpA += (vA + (u32)bA * m) >> 31;
-        pB += bB; cpB += (vB + (u32)bB * m) >> 31;
-      }
-#pragma unroll 8
-      for (int i = 0; i < jn; i++) {
-        const int idx = MT_CM - 1 - i;
-        const double r = rmL[idx];
-        const u32 m = mL[idx];
-        const u64 bA = (u64)__double_as_longlong(fma(vdA, r, MT_TWO52));
-        const u64 bB = (u64)__double_as_longlong(fma(vdB, r, MT_TWO52));
-        nA += bA; cnA += (vA + (u32)bA * m) >> 31;
-        nB += bB; cnB += (vB + (u32)bB * m) >> 31;
-      }
-      // the longer element finishes alone (partial elements only)
-      const bool aLonger = bpA > jp || bnA > jn;
-      const double vdL = aLonger ? vdA : vdB;
-      const u32 vL = aLonger ? vA : vB;
-      const int ep = aLonger ? bpA : bpB, en = aLonger ? bnA : bnB;
-      u64 pL = 0, nL = 0;
-      u32 cpL = 0, cnL = 0;
-      for (int i = jp; i < ep; i++) {
-        const u64 b = (u64)__double_as_longlong(fma(vdL, rmL[i], MT_TWO52));
-        pL += b; cpL += (vL + (u32)b * mL[i]) >> 31;
-      }
-      for (int i = jn; i < en; i++) {
-        const int idx = MT_CM - 1 - i;
-        const u64 b = (u64)__double_as_longlong(fma(vdL, rmL[idx], MT_TWO52));
-        nL += b; cnL += (vL + (u32)b * mL[idx]) >> 31;
-      }
-      if (aLonger) { pA += pL; cpA += cpL; nA += nL; cnA += cnL; }
-      else { pB += pL; cpB += cpL; nB += nL; cnB += cnL; }
-      const u64 SA = (pA - (u64)bpA * MT_EXP52 - cpA) - (nA - (u64)bnA * MT_EXP52 - cnA);
-      const u64 SB = (pB - (u64)bpB * MT_EXP52 - cpB) - (nB - (u64)bnB * MT_EXP52 - cnB);
-      if (bpA + bnA) atomicAdd((unsigned long long*)(a.acc + eA), (unsigned long long)SA);
-      if (bpB + bnB) atomicAdd((unsigned long long*)(a.acc + eB), (unsigned long long)SB);
+    u64 SA1 = 0, SA2 = 0, SB1 = 0, SB2 = 0;
+    if (fast) {
+      const double vdA = cA < a.C.n ? a.C.vd[cA] : 0.0, vdB = cB < a.C.n ? a.C.vd[cB] : 0.0;
+      const u32 vA = cA < a.C.n ? (u32)a.C.vlo[cA] : 0u, vB = cB < a.C.n ? (u32)a.C.vlo[cB] : 0u;
+      u64 PA[2], PB[2], NA[2], NB[2];
+      walk_list<false>(rmL, mL, vdA, vA, vdB, vB, pA1, pA2, pB1, pB2, PA, PB);
+      walk_list<true>(rmL, mL, vdA, vA, vdB, vB, nA1, nA2, nB1, nB2, NA, NB);
+      SA1 = PA[0] - NA[0]; SA2 = PA[1] - NA[1];
+      SB1 = PB[0] - NB[0]; SB2 = PB[1] - NB[1];
     } else {
-      if (actA && bpA + bnA)
-        atomicAdd((unsigned long long*)(a.acc + eA), (unsigned long long)counted_one(a, eA, tau, mlo, mhi, bpA, bnA, rmL, mL));
-      if (actB && bpB + bnB)
-        atomicAdd((unsigned long long*)(a.acc + eB), (unsigned long long)counted_one(a, eB, tau, mlo, mhi, bpB, bnB, rmL, mL));
+      if (pA1 + nA1) SA1 = counted_one(a, cA, tau, mlo, mhi, pA1, nA1, rmL, mL);
+      if (pA2 + nA2) SA2 = counted_one(a, cA, tau, mlo, mhi, pA2, nA2, rmL, mL);
+      if (pB1 + nB1) SB1 = counted_one(a, cB, tau, mlo, mhi, pB1, nB1, rmL, mL);
+      if (pB2 + nB2) SB2 = counted_one(a, cB, tau, mlo, mhi, pB2, nB2, rmL, mL);
     }
+    if (pA1 + nA1) atomicAdd((unsigned long long*)(a.acc + tA1), (unsigned long long)SA1);
+    if (pA2 + nA2) atomicAdd((unsigned long long*)(a.acc + tA2), (unsigned long long)(0ull - SA2));
+    if (pB1 + nB1) atomicAdd((unsigned long long*)(a.acc + tB1), (unsigned long long)SB1);
+    if (pB2 + nB2) atomicAdd((unsigned long long*)(a.acc + tB2), (unsigned long long)(0ull - SB2));
     __syncthreads();
   }
 }
@@ -745,8 +831,7 @@ static int scan_u64(UpdateCtx* c, const uint64_t* in, uint64_t* out, uint64_t n,
   return MT_OK;
 }
 
-int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* Mmc,
-                     const uint64_t* tile_mcut_max, const uint8_t* tile_vbits_max, uint64_t ntiles,
+int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* Mmc, const uint64_t* Kt,
                      const TargetDev* tgts, int ntgt, const GroupDev& grp, const Shard& sh,
                      KTimer* kt, cudaStream_t st) {
   UpdateCtx* c = new UpdateCtx();
@@ -754,13 +839,39 @@ int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* 
   c->kt = kt;
   c->G = grp;
   c->E = E; c->acc = acc; c->Mmc = Mmc;
-  c->tile_mcut_max = tile_mcut_max; c->tile_vbits_max = tile_vbits_max; c->ntiles = ntiles;
   c->ntgt = ntgt;
   c->launches = 0;
   *out = c;
   MT_CUDA_CHECK(cudaMalloc(&c->tgts, sizeof(TargetDev) * (ntgt ? ntgt : 1)));
   c->tgts_h.assign(tgts, tgts + ntgt);
   MT_CUDA_CHECK(cudaMemcpyAsync(c->tgts, tgts, sizeof(TargetDev) * ntgt, cudaMemcpyHostToDevice, st));
+  // counted entries: the NE elements, then per target the virtual halves of k > K/2
+  std::vector<u64> vbase(ntgt ? ntgt : 1), Kv(Kt, Kt + ntgt);
+  u64 nce = E.n;
+  for (int t = 0; t < ntgt; t++) { vbase[t] = nce; nce += Kt[t] - Kt[t] / 2; }
+  CountedEntries& C = c->C;
+  C.n = nce;
+  const u64 na = nce ? nce : 1;
+  MT_CUDA_CHECK(cudaMalloc(&C.vd, na * 8)); MT_CUDA_CHECK(cudaMalloc(&C.vlo, na * 8)); MT_CUDA_CHECK(cudaMalloc(&C.vhi, na * 8));
+  MT_CUDA_CHECK(cudaMalloc(&C.vbits, na)); MT_CUDA_CHECK(cudaMalloc(&C.lim1, na * 8)); MT_CUDA_CHECK(cudaMalloc(&C.lim2, na * 8));
+  MT_CUDA_CHECK(cudaMalloc(&C.t1, na * 4)); MT_CUDA_CHECK(cudaMalloc(&C.t2, na * 4));
+  c->ntiles = (nce + MT_CT - 1) / MT_CT;
+  MT_CUDA_CHECK(cudaMalloc(&c->tile_max, (c->ntiles + 1) * 8));
+  MT_CUDA_CHECK(cudaMalloc(&c->tile_vbits, c->ntiles + 1));
+  {
+    u64 *dK = nullptr, *dvb = nullptr;
+    MT_CUDA_CHECK(cudaMalloc(&dK, 8 * (ntgt ? ntgt : 1)));
+    MT_CUDA_CHECK(cudaMalloc(&dvb, 8 * (ntgt ? ntgt : 1)));
+    MT_CUDA_CHECK(cudaMemcpyAsync(dK, Kv.data(), 8 * ntgt, cudaMemcpyHostToDevice, st));
+    MT_CUDA_CHECK(cudaMemcpyAsync(dvb, vbase.data(), 8 * ntgt, cudaMemcpyHostToDevice, st));
+    if (E.n) k_ce_init<<<(unsigned)((E.n + 255) / 256), 256, 0, st>>>(E, dK, dvb, C);
+    if (c->ntiles) k_ce_tiles<<<(unsigned)c->ntiles, MT_CT, 0, st>>>(C, c->tile_max, c->tile_vbits);
+    MT_CUDA_CHECK(cudaGetLastError());
+    MT_CUDA_CHECK(cudaStreamSynchronize(st));
+    cudaFree(dK);
+    cudaFree(dvb);
+  }
+  const u64 ntiles = c->ntiles;
   MT_CUDA_CHECK(cudaMalloc(&c->units, sizeof(uint64_t) * (ntiles + 1) * 2));
   MT_CUDA_CHECK(cudaMalloc(&c->cnt, sizeof(uint64_t) * (E.n + 1)));
   MT_CUDA_CHECK(cudaMalloc(&c->dtop, sizeof(uint64_t) * (E.n + 1)));
@@ -780,6 +891,8 @@ int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* 
 
 void mt_update_destroy(UpdateCtx* c) {
   if (!c) return;
+  cudaFree(c->C.vd); cudaFree(c->C.vlo); cudaFree(c->C.vhi); cudaFree(c->C.vbits); cudaFree(c->C.lim1);
+  cudaFree(c->C.lim2); cudaFree(c->C.t1); cudaFree(c->C.t2); cudaFree(c->tile_max); cudaFree(c->tile_vbits);
   cudaFree(c->tgts); cudaFree(c->units); cudaFree(c->cnt); cudaFree(c->dtop); cudaFree(c->off);
   cudaFree(c->qcnt); cudaFree(c->qoff); cudaFree(c->counter);
   cudaFree(c->gunits); cudaFree(c->guoff); cudaFree(c->gwfirst);
@@ -797,12 +910,12 @@ int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const 
   {
     uint64_t* units = c->units;
     uint64_t* off = c->units + (c->ntiles + 1);
-    k_counted_plan<<<(unsigned)((c->ntiles + 1 + 255) / 256), 256, 0, st>>>(c->tile_mcut_max, c->ntiles, Y0, R, units);
+    k_counted_plan<<<(unsigned)((c->ntiles + 1 + 255) / 256), 256, 0, st>>>(c->tile_max, c->ntiles, Y0, R, units);
     c->launches++;
     int rc = scan_u64(c, units, off, c->ntiles + 1, st);
     if (rc) return rc;
     MT_CUDA_CHECK(cudaMemsetAsync(c->counter, 0, sizeof(uint64_t) * 4, st));
-    CountedArgs a{E, c->acc, c->tile_mcut_max, c->tile_vbits_max, off, c->ntiles, mu, Y0, c->counter,
+    CountedArgs a{c->C, c->acc, c->tile_max, c->tile_vbits, off, c->ntiles, mu, Y0, c->counter,
                   c->sh.rank, c->sh.world, c->sh.flags};
     c->kt->begin(KT_COUNTED, st);
     k_counted<<<c->nsm * 12, CT_THREADS, 0, st>>>(a);

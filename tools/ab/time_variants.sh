@@ -3,7 +3,7 @@
 # usage: tools/ab/time_variants.sh [n=1e19] [reps=2]
 cd "$(dirname "$0")/../.."
 n=${1:-1e19}; reps=${2:-2}
-for lib in paper_1108_0135_b200/libmertens_sm100.so tools/ab/lib_*.so; do
+for lib in paper_1108_0135_b200/libmertens_sm100.so $(ls tools/ab/lib_*.so 2>/dev/null); do
   echo "== $lib"
   MT_LIB=$lib MT_TIMING=1 timeout 900 python tools/prof_job.py $n $reps 2>&1 | tail -1 | python -c "
 import sys, ast
