@@ -77,6 +77,7 @@ struct UpdateCtx {
 // 6/pi^2 to 4/pi^2 of the m per element (plus the virtual halves): 24 % fewer items.
 // Work units are (tile of MT_CT entries) x (MT_CU consecutive m, i.e. MT_CM odd m).
 #define MT_CU (2 * MT_CM)  // m per counted unit (its odd m fill one list of MT_CM)
+static_assert((MT_CU & (MT_CU - 1)) == 0, "counted units must be powers of two (units never straddle 2^32)");
 
 __global__ void k_counted_plan(const uint64_t* __restrict__ tile_max, uint64_t ntiles, u64 Y0,
                                u64 R, uint64_t* __restrict__ units) {
