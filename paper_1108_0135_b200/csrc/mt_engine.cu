@@ -1043,13 +1043,13 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
 
   // ---- segments (production sieve tiles of 2^17 cells)
   // default tail segment = 6 tiles per SM (the persistent sieve CTAs each take 6
-  // contiguous tiles; measured at 1e19: 2 % faster than 4, fewer per-segment
-  // fill setups and finish launches); head segments default to 2 tiles per SM: the head's sparse
-  // walk gathers M(y) from the segment's 2-byte table, which then stays in L2
-  // (measured at 1e19: head phase -6 %, the head's sieve share is negligible)
+  // contiguous tiles; fewer per-segment fill setups and finish launches); head
+  // segments default to 1 tile per SM: the head's sparse walk gathers M(y) from the
+  // segment's 2-byte table, and at 39 MB it stays in the L2 half of each die (ncu:
+  // 62 % L2 hits with 2 tiles per SM; measured at 1e19: head phase -1 %)
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P->device);
-  u64 tiles_per_sm = 6, tiles_per_sm_head = 2;
+  u64 tiles_per_sm = 6, tiles_per_sm_head = 1;
   if (const char* e = getenv("MT_SEG_TILES_PER_SM")) tiles_per_sm = strtoull(e, nullptr, 10);
   if (const char* e = getenv("MT_SEG_TILES_PER_SM_HEAD")) tiles_per_sm_head = strtoull(e, nullptr, 10);
   P->Rh = job->seg_log2_head ? 1ull << job->seg_log2_head : (u64)nsm * tiles_per_sm_head * MT_S2_TILE;

@@ -132,7 +132,9 @@ __device__ __forceinline__ void first_hits(u64 C0, double Cd, double rm, u64 m, 
 // write per hit (ncu: the scattered stores were 60% of the stalls).  Entries
 // past a full bin, and all square flags, are stored directly.
 #define FBATCH 1024  // streams per batch
+#ifndef FITEM
 #define FITEM 32     // hits per item (1024 items per round: ~32k hits over the tiles)
+#endif
 template <int W>
 __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
   constexpr int NS = Wheel<W>::NS;

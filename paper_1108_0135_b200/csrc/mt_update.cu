@@ -310,8 +310,10 @@ __device__ __forceinline__ void walk_list(const double* rmL, const u32* mL, doub
 #define CT_MINB 1
 #endif
 __global__ void __launch_bounds__(CT_THREADS, CT_MINB) k_counted(CountedArgs a) {
-  __shared__ double rmL[MT_CM];
-  __shared__ u32 mL[MT_CM];  // low word of m, stored NEGATED: the 32-bit remainder is one IMAD (v + q * (-m))
+  // dynamic: rmL[MT_CM] (1/m), then mL[MT_CM]: the low word of m, stored NEGATED (the
+  // 32-bit remainder is one IMAD, v + q * (-m))
+  extern __shared__ __align__(16) double rmL[];
+  u32* mL = (u32*)(rmL + MT_CM);
   __shared__ u64 s_unit;
   __shared__ int wp[CT_THREADS / 32], wn[CT_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -469,32 +471,35 @@ __device__ __forceinline__ int walk_window32(u64 vlo, u64 vhi, double vd, int vb
   const double rd = __drcp_rn((double)dh64);
   const u64 y0 = qdiv_ok(vb, dh64) ? qdiv64(vd, rd, vlo, dh64) : (u64)udiv128(vlo, vhi, dh64);
   u32 delta = (u32)((double)y0 * rd);
-  u32 d = (u32)dh64;
-  const u32 dl = (u32)dl64;
-  u32 r = (u32)vlo - (u32)y0 * d;
-  u32 yo = (u32)(y0 - W0);  // offset in the window
+  // all arithmetic mod 2^32 (the true ts lies in (-d, 2d)): the walk keeps -d, the
+  // low word of y (the window offset is y - W0, so the load address is
+  // (swbase - 2 W0) + 2 y), the remainder r and the increment delta
+  int nd = -(int)(u32)dh64;
+  const int ndl = -(int)(u32)dl64;
+  u32 r = (u32)vlo - (u32)y0 * (u32)dh64;
+  u32 yw = (u32)y0;
+  u32 base = swbase - 2u * (u32)W0;
   int s = 0;
-  bool lbad = false;
-  u32 swb = swbase;
+  u32 accb = 0;
   for (;;) {
-    asm volatile("" : "+r"(swb));  // keep the window base live (no per-item rematerialisation)
+    asm volatile("" : "+r"(base));  // keep the window base live (no per-item rematerialisation)
     short m16;
-    asm volatile("ld.shared.s16 %0, [%1];" : "=h"(m16) : "r"(swb + 2 * yo));
+    asm volatile("ld.shared.s16 %0, [%1];" : "=h"(m16) : "r"(base + 2 * yw));
     s += m16;
-    if (d == dl) break;
-    --d;
-    const int ts = (int)(r + (yo + (u32)W0) - delta * d);  // (y + r) - delta*d in (-d, 2d)
-    const int neg = ts >> 31;                                 // -1 if ts < 0
-    const int over = (int)(ts >= (int)d);                     // 1 if ts >= d
-    delta += (u32)(over + neg);
-    const u32 t = (u32)(ts + ((int)d & neg) - ((int)d & -over));
-    // t < d always holds when y/d^2 <= 1 (one correction suffices); the check is
-    // folded into one predicate per step and a violation re-walks exactly
-    lbad |= t >= d;
-    r = t;
-    yo += delta;
+    if (nd == ndl) break;
+    ++nd;                                              // d - 1
+    const int ts = (int)(r + yw) + (int)delta * nd;    // (y + r) - delta*d in (-d, 2d)
+    // c = +1 if ts >= d, -1 if ts < 0, else 0 (from the two sign bits, no predicates)
+    const int c = ((ts + nd) >> 31) + (ts >> 31) + 1;
+    delta += (u32)c;
+    const int t = ts + c * nd;                         // ts - c*d
+    // t in [0, d) always holds when y/d^2 <= 1/2 but for rare floor patterns: its two
+    // sign conditions are OR-ed into one word and a violation re-walks exactly
+    accb |= (u32)(t | ~(t + nd));
+    r = (u32)t;
+    yw += delta;
   }
-  bad = lbad;
+  bad = (accb >> 31) != 0;
   return s;
 }
 
@@ -884,6 +889,7 @@ int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* 
   MT_CUDA_CHECK(cudaMalloc(&c->guoff, sizeof(uint64_t) * (grp.ng + 1)));
   MT_CUDA_CHECK(cudaMalloc(&c->gwfirst, sizeof(uint64_t) * (grp.ng + 1)));
   MT_CUDA_CHECK(cudaFuncSetAttribute(k_dwin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(MT_BLK * 2)));
+  MT_CUDA_CHECK(cudaFuncSetAttribute(k_counted, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(MT_CM * 12)));
   c->cub_tmp = nullptr; c->cub_bytes = 0;
   int dev; cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -919,7 +925,7 @@ int mt_update_head_segment(UpdateCtx* c, u64 Y0, u64 R, const int8_t* mu, const 
     CountedArgs a{c->C, c->acc, c->tile_max, c->tile_vbits, off, c->ntiles, mu, Y0, c->counter,
                   c->sh.rank, c->sh.world, c->sh.flags};
     c->kt->begin(KT_COUNTED, st);
-    k_counted<<<c->nsm * 12, CT_THREADS, 0, st>>>(a);
+    k_counted<<<c->nsm * 12, CT_THREADS, MT_CM * 12, st>>>(a);
     c->kt->end(st);
     c->launches++;
     MT_CUDA_CHECK(cudaGetLastError());
