@@ -381,6 +381,7 @@ def main():
     _one(plan, world, res)
     barrier()
     stats_last = _lib.stats_dict(res.stats)
+    stats_last["_n"], stats_last["_u"] = n, u
     kms = dict(stats_last["kernel_ms"])
     kcnt = dict(stats_last["kernel_count"])
     plan.close()
@@ -507,14 +508,16 @@ def _rooflines(st, kms, kcnt, nsm):
     roof_u = None
     upd_ms = kms.get("counted", 0.0)
     if upd_ms > 0:
-        items = 6 / 3.141592653589793 ** 2 * st["counted_items"]
+        items = _counted_units(st)
         A = items / (upd_ms * 1e-3) / 1e12
         Pk = 32.0 * nsm * mhz * 1e6 / 1e12
         m = nm.get("k_counted", {})
         roof_u = {"kernel": "counted", "bound": "issue", "achieved": A, "peak": Pk, "unit": "T items/s",
                   "frac": A / Pk,
-                  "per_unit": "one squarefree m: DFMA (fp64 reciprocal quotient) + IMAD (remainder) + 2 ALU "
-                              "(accumulate, correction) = 4 issue slots",
+                  "per_unit": "one odd squarefree m of a walk entry (DESIGN.md §2.1: entries walk odd m up to "
+                              "their largest prefix limit; 4/pi^2 of those m): DFMA (fp64 reciprocal quotient) + IMAD "
+                              "(remainder) + 2 ALU (accumulate, correction) = 4 issue slots",
+                  "units_per_step": items,
                   "peak_source": "4 warp-instructions/clk/SM x 32 lanes / 4 slots x SMs x sm_max_mhz; the "
                                  "FP64 and IMAD pipes alone allow 63.8 units/clk/SM (profiles/r01_microbench.txt)",
                   "reference_count_rate": st["counted_items"] / (upd_ms * 1e-3),
@@ -528,6 +531,32 @@ def _rooflines(st, kms, kcnt, nsm):
     out["roofline_sieve"] = roof_s
     out["roofline_update"] = roof_u
     return out
+
+
+def _counted_units(st):
+    """Odd squarefree m the counted walk processes in one step, in closed form: every
+    element k walks odd m up to max(mcut_k, floor(mcut_{k/2}/2)) (the second limit for even
+    k), and every k with 2k > K adds a virtual half walk up to floor(mcut_k/2); 4/pi^2 of
+    the m are odd and squarefree.  mcut is the reference's (engine.py:144-158)."""
+    n, u = int(st["_n"]), int(st["_u"])
+    K = n // u
+    k = np.arange(1, K + 1, dtype=np.uint64)
+    v = np.uint64(n) // k
+    s = np.sqrt(v.astype(np.float64)).astype(np.uint64)
+    s += (s * s < v)  # ceil sqrt (float start, corrected)
+    s -= ((s - np.uint64(1)) * (s - np.uint64(1)) >= v) & (s > 0)
+    x2 = np.uint64(2) * s
+    t = np.uint64(1) << np.ceil(np.log2(x2.astype(np.float64))).astype(np.uint64)
+    t = np.where(t < x2, t << np.uint64(1), t)
+    t = np.where((t >> np.uint64(1)) >= x2, t >> np.uint64(1), t)
+    D = v // np.uint64(u + 1)
+    xc = np.maximum(np.maximum(D, v // t), np.uint64(1))
+    mc = (v // (xc + np.uint64(1))).astype(np.float64)
+    lim = mc.copy()
+    even = np.arange(2, K + 1, 2)
+    lim[even - 1] = np.maximum(mc[even - 1], np.floor(mc[even // 2 - 1] / 2))
+    total = float(lim.sum()) + float(np.floor(mc[K // 2:] / 2).sum())
+    return 4 / 3.141592653589793 ** 2 * total
 
 
 class _SinglePlan:
