@@ -327,6 +327,9 @@ def main():
     torch.cuda.set_device(dev)
     if world > 1:
         if args.dist_backend == "nccl":
+            # communicator init lines (nranks) for the record, also when launched by torchrun
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group("gloo")
