@@ -509,29 +509,29 @@ def mertens_identity_residual(result: MertensResult, chunk: int = 1 << 24) -> in
     The dense map (capture-all for large n, possibly memory-mapped) is summed in
     chunks of `chunk` entries (no n-sized temporaries) modulo 2^64."""
     n = result.n
-    if result._qmap is not None and n < 2**63:
+    if result._qmap is not None and n < 2**64:
         s = isqrt(n)
         K = len(result._final)
         tot = 0
-        # c <= isqrt(n): multiplicity of q = n // c is n//q - n//(q+1)
-        for c0 in range(1, s + 1, chunk):
-            c = np.arange(c0, min(s, c0 + chunk - 1) + 1, dtype=np.int64)
-            q = n // c
-            mult = n // q - n // (q + 1)
-            i0, i1 = c0 - 1, c0 - 1 + len(c)  # index into finals ++ qmap
-            parts = []
+        # c < s: q = n // c >= s + 1, whose preimage (n/(q+1), n/q] is shorter than 1,
+        # so every such quotient occurs once (at x = c); c = s is added exactly below
+        for c0 in range(1, s, chunk):
+            i0, i1 = c0 - 1, min(s - 1, c0 + chunk - 1)  # indices into finals ++ qmap
             if i0 < K:
-                parts.append(result._final[i0:min(i1, K)].astype(np.int64))
+                tot += int(result._final[i0:min(i1, K)].astype(np.int64).sum())
             if i1 > K:
-                parts.append(np.asarray(result._qmap[max(i0, K) - K:i1 - K]).astype(np.int64))
-            m = np.concatenate(parts) if len(parts) > 1 else parts[0]
-            tot += int((mult * m).sum())
-        # y < floor(n/s): the quotients below the c-range, multiplicity n//y - n//(y+1)
+                tot += int(np.asarray(result._qmap[max(i0, K) - K:i1 - K]).astype(np.int64).sum())
+        q = n // s
+        ms = int(result._final[s - 1]) if s - 1 < K else int(result._qmap[s - 1 - K])
+        tot += (n // q - n // (q + 1)) * ms
+        # y < floor(n/s): multiplicity n//y - n//(y+1) (uint64 quotients, one division each)
         ymax = min(n // s - 1, s)
+        nn = np.uint64(n)
         for y0 in range(1, ymax + 1, chunk):
-            y = np.arange(y0, min(ymax, y0 + chunk - 1) + 1, dtype=np.int64)
-            mult = n // y - n // (y + 1)
-            tot += int((mult * np.asarray(result._small[y0:y0 + len(y)]).astype(np.int64)).sum())
+            y1 = min(ymax, y0 + chunk - 1)
+            d = nn // np.arange(y0, y1 + 2, dtype=np.uint64)
+            mult = (d[:-1] - d[1:]).astype(np.int64)
+            tot += int((mult * np.asarray(result._small[y0:y1 + 1]).astype(np.int64)).sum())
         # int64 products and chunk sums wrap mod 2^64 (exact there); the identity's
         # total is small, so the signed residue mod 2^64 is the exact value
         tot %= 1 << 64

@@ -154,3 +154,21 @@ def test_bench_gpus_spawns_ranks():
     assert p.returncode == 0, p.stderr[-2000:]
     lines = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
     assert sorted(d["rank"] for d in lines) == [0, 1, 2] and all(d["world"] == 3 for d in lines)
+
+
+@pytest.mark.parametrize("n", [10**6, 999_983, 1000 * 1001, 1000 * 1001 - 1, 1001**2 - 1, 2 * 10**6 + 7])
+@pytest.mark.parametrize("chunk", [1 << 24, 97])
+def test_identity_residual_dense_map(n, chunk, oracle):
+    """mertens_identity_residual over a dense map built from the oracle's M table:
+    zero, including n = s(s+1) - 1, s(s+1) and (s+1)^2 - 1 where c = s is special."""
+    M = np.concatenate([[0], oracle.mertens_table(n)])
+    s = math.isqrt(n)
+    K = max(1, round(n ** (1 / 3)))
+    c = np.arange(1, s + 1)
+    mq = M[n // c].astype(np.int32)
+    r = PE.MertensResult(n, int(M[n]), 0, mq[:K].astype(np.int64), qmap=mq[K:], small=M[: s + 1].astype(np.int32))
+    assert PE.mertens_identity_residual(r, chunk=chunk) == 0
+    bad = mq[K:].copy()
+    bad[-1] += 1
+    r2 = PE.MertensResult(n, int(M[n]), 0, mq[:K].astype(np.int64), qmap=bad, small=M[: s + 1].astype(np.int32))
+    assert PE.mertens_identity_residual(r2, chunk=chunk) != 0
