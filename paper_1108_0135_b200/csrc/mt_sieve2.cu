@@ -52,8 +52,14 @@
 #ifndef S2_B2_MIN
 #define S2_B2_MIN (1u << 15)     // in-tile primes from here on hit <= 4 times per tile (measured: 2^15 > 2^14 > 2^13)
 #endif
+#ifndef S2_LIST_PREFETCH
+#define S2_LIST_PREFETCH 0       // L2 bulk prefetch of the tile's bucket lists at the tile start
+#endif
 #ifndef S2_DLOADS
 #define S2_DLOADS 1              // 16-byte bucket vectors in flight per lane (measured: 1 > 2)
+#endif
+#ifndef S2_DPAIR
+#define S2_DPAIR 1               // D: two bucket lists per fetch, walked as one
 #endif
 
 __device__ __forceinline__ void red_add(u32 saddr, u32 v) {
@@ -134,6 +140,9 @@ __device__ __forceinline__ void first_hits(u64 C0, double Cd, double rm, u64 m, 
 #define FBATCH 1024  // streams per batch
 #ifndef FITEM
 #define FITEM 32     // hits per item (1024 items per round: ~32k hits over the tiles)
+#endif
+#ifndef FILL_CONTIG
+#define FILL_CONTIG 1  // a thread's items of a round are contiguous (one search per round)
 #endif
 template <int W>
 __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
@@ -229,6 +238,23 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
     __syncthreads();
     if (tid == 0) s_hits = 0;
     for (u32 r0 = 0; r0 < nit; r0 += 1024 * per) {
+#if FILL_CONTIG
+      // thread tid takes the round's items [r0 + tid*per, r0 + (tid+1)*per): one search,
+      // then the stream index only moves forward
+      const u32 it0 = r0 + tid * per, it1 = min(min(nit, r0 + 1024 * per), it0 + per);
+      u32 kc = 0;
+      if (it0 < it1) {
+        u32 lo = 0, hi = FBATCH;  // largest k with s_ipre[k] <= it0
+        while (hi - lo > 1) {
+          const u32 mid = (lo + hi) >> 1;
+          if (s_ipre[mid] <= it0) lo = mid; else hi = mid;
+        }
+        kc = lo;
+      }
+      for (u32 it = it0; it < it1; it++) {
+        while (s_ipre[kc + 1] <= it) kc++;
+        const u32 k = kc, ci = it - s_ipre[k];
+#else
       for (u32 it = r0 + tid; it < min(nit, r0 + 1024 * per); it += 1024) {
         u32 lo = 0, hi = FBATCH;  // largest k with s_ipre[k] <= it
         while (hi - lo > 1) {
@@ -236,6 +262,7 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
           if (s_ipre[mid] <= it) lo = mid; else hi = mid;
         }
         const u32 k = lo, ci = it - s_ipre[k];
+#endif
         const u32 step = s_step[k], val = s_val[k];
         u32 pos = s_q0[k] + ci * FITEM * step;
         const u32 end = (u32)min((u64)R, (u64)pos + (u64)FITEM * step);
@@ -352,6 +379,31 @@ __device__ __forceinline__ u32 carry(u32 j, u32 tm, u32 stride) { return j >= tm
 // outputs are tile-relative; k_s3_finish makes them absolute.
 // ----------------------------------------------------------------------------
 
+// an overflowed bucket list (more hits than its capacity): producer b's hits on
+// the tile at cell Ct, recomputed from the primes by one warp (rare)
+template <int W>
+__device__ __noinline__ void d_overflow(const u32* __restrict__ primes, const double* __restrict__ rprimes,
+                                       const uint8_t* __restrict__ logs, u32 p_lo, u32 p_hi, u32 q_lo, u32 q_hi,
+                                       u32 nprod, unsigned long long* ovf, u32 b, u64 Ct, u32 sbase, int lane) {
+  constexpr int NS = Wheel<W>::NS;
+  if (lane == 0) atomicAdd(ovf, 1ull);
+  const double Cd = (double)Ct;
+  u64 j[NS];
+  for (u64 i = (u64)p_lo + b + (u64)lane * nprod; i < p_hi; i += 32ull * nprod) {
+    const u32 p = primes[i];
+    first_hits<W>(Ct, Cd, rprimes[i], p, j);
+    for (int s = 0; s < NS; s++)
+      for (u64 jj = j[s]; jj < S2_T; jj += NS * p)
+        red_add(sbase + ((u32)jj & ~3u), (u32)logs[i] << (((u32)jj & 3) * 8));
+  }
+  for (u64 i = (u64)q_lo + b + (u64)lane * nprod; i < q_hi; i += 32ull * nprod) {
+    const u64 p = primes[i];
+    first_hits<W>(Ct, Cd, __drcp_rn((double)(p * p)), p * p, j);
+    for (int s = 0; s < NS; s++)
+      if (j[s] < S2_T) red_or(sbase + ((u32)j[s] & ~3u), 0x80u << (((u32)j[s] & 3) * 8));
+  }
+}
+
 template <int W>
 __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
   constexpr int NS = Wheel<W>::NS;
@@ -417,7 +469,18 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
       const u32* __restrict__ w2 = a.w2 + (u32)((Ct % a.w2_period4) >> 2);
       for (int i = tid; i < (int)S2_W; i += S2_NT) st[i] = w1[i] + w2[i];
     }
-    for (u32 b = tid; b < a.nprod && b < S2_MAXPROD; b += S2_NT) s_cnt[b] = a.counts[(u64)b * a.ntiles + tile];
+    for (u32 b = tid; b < a.nprod && b < S2_MAXPROD; b += S2_NT) {
+      const u32 cw = a.counts[(u64)b * a.ntiles + tile];
+      s_cnt[b] = cw;
+#if S2_LIST_PREFETCH
+      // the tile's bucket lists (~140 KB, written by the fill, mostly in DRAM) start
+      // moving into L2 now and are read in phase D after the presieve and marks
+      if (cw != 0xFFFFFFFFu && (cw & 0xFFFF)) {
+        const u32* L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(L), "r"((cw & 0xFFFF) * 4u) : "memory");
+      }
+#endif
+    }
     __syncthreads();
     // 2. marks
     // A: warp per prime (W = 6: half-warp per stream), snake order over the warps
@@ -521,55 +584,58 @@ __global__ void __launch_bounds__(S2_NT, 1) k_sieve3(Sieve2Args a) {
       if (li == 0) offC[s * nC + k] = carry(j0, tmC[k], stride);
     }
     // D: bucket lists (primes > big_min, squares > 2^17), dealt to warps from a
-    //    shared counter so warps that finished A-C early take more lists
+    //    shared counter so warps that finished A-C early take more lists; with
+    //    S2_DPAIR a warp takes two lists (b, b + 1) and walks them as one run
+    //    (more loads in flight, fuller lanes on short lists, half the fetches)
     if (a.nprod) {
-      const double Cd = (double)Ct;
+      const u32 dn_s = (u32)__cvta_generic_to_shared(&s_dnext);
+      constexpr u32 DP = S2_DPAIR ? 2 : 1;
       for (;;) {
         u32 b = 0;
-        if (lane == 0) b = atomicAdd(&s_dnext, 1u);
+        if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(b) : "r"(dn_s), "n"(DP) : "memory");
         b = __shfl_sync(0xffffffffu, b, 0);
         if (b >= a.nprod) break;
-        const u32 cw = b < S2_MAXPROD ? s_cnt[b] : a.counts[(u64)b * a.ntiles + tile];
-        const u32* __restrict__ L = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
-        if (cw != 0xFFFFFFFFu) {
-          const u32 n = cw & 0xFFFF, nsq = cw >> 16;
-          // log entries (front): n is a multiple of 4 (the fill pads every run with
-          // no-op zero entries), so the list is read as 16-byte vectors,
-          // S2_DLOADS per lane in flight
-          const uint4* __restrict__ L4 = (const uint4*)L;
-          const u32 n4 = n >> 2;
-          for (u32 k = lane; k < n4; k += 32 * S2_DLOADS) {
-            uint4 e[S2_DLOADS];
+        u32 cw0 = b < S2_MAXPROD ? s_cnt[b] : a.counts[(u64)b * a.ntiles + tile];
+        u32 cw1 = 0;
+        if (DP == 2 && b + 1 < a.nprod) cw1 = b + 1 < S2_MAXPROD ? s_cnt[b + 1] : a.counts[(u64)(b + 1) * a.ntiles + tile];
+        // overflowed list: this producer's hits on the tile, recomputed exactly
+        for (u32 h = 0; h < DP; h++) {
+          u32& cw = h ? cw1 : cw0;
+          if (cw != 0xFFFFFFFFu) continue;
+          d_overflow<W>(a.primes, a.rprimes, a.logs, a.p_lo, a.p_hi, a.q_lo, a.q_hi, a.nprod, a.overflow, b + h, Ct,
+                        sbase, lane);
+          cw = 0;
+        }
+        const u32* __restrict__ L0 = a.buf + ((u64)b * a.ntiles + tile) * a.cap;
+        const u32* __restrict__ L1 = L0 + (u64)a.ntiles * a.cap;  // list b + 1 of the tile
+        // log entries (front): every run is a multiple of 4 (the fill pads it with
+        // no-op zero entries), so the lists are read as 16-byte vectors, S2_DLOADS
+        // per lane in flight; vector k < n0 is list b's, k >= n0 list b + 1's
+        const u32 n0 = (cw0 & 0xFFFF) >> 2, n4 = n0 + ((cw1 & 0xFFFF) >> 2);
+        const uint4* __restrict__ A4 = (const uint4*)L0;
+        const uint4* __restrict__ B4 = (const uint4*)L1 - n0;
+        for (u32 k = lane; k < n4; k += 32 * S2_DLOADS) {
+          uint4 e[S2_DLOADS];
 #pragma unroll
-            for (int h = 0; h < S2_DLOADS; h++) e[h] = k + 32 * h < n4 ? L4[k + 32 * h] : make_uint4(0u, 0u, 0u, 0u);
+          for (int h = 0; h < S2_DLOADS; h++) {
+            const u32 kk = k + 32 * h;
+            e[h] = kk < n4 ? (kk < n0 ? A4 : B4)[kk] : make_uint4(0u, 0u, 0u, 0u);
+          }
 #pragma unroll
-            for (int h = 0; h < S2_DLOADS; h++) {
-              red_add(sbase + (e[h].x & 0x1FFFCu), (e[h].x >> 17) << ((e[h].x & 3) * 8));
-              red_add(sbase + (e[h].y & 0x1FFFCu), (e[h].y >> 17) << ((e[h].y & 3) * 8));
-              red_add(sbase + (e[h].z & 0x1FFFCu), (e[h].z >> 17) << ((e[h].z & 3) * 8));
-              red_add(sbase + (e[h].w & 0x1FFFCu), (e[h].w >> 17) << ((e[h].w & 3) * 8));
-            }
+          for (int h = 0; h < S2_DLOADS; h++) {
+            red_add(sbase + (e[h].x & 0x1FFFCu), (e[h].x >> 17) << ((e[h].x & 3) * 8));
+            red_add(sbase + (e[h].y & 0x1FFFCu), (e[h].y >> 17) << ((e[h].y & 3) * 8));
+            red_add(sbase + (e[h].z & 0x1FFFCu), (e[h].z >> 17) << ((e[h].z & 3) * 8));
+            red_add(sbase + (e[h].w & 0x1FFFCu), (e[h].w >> 17) << ((e[h].w & 3) * 8));
           }
-          for (u32 k = lane; k < nsq; k += 32) {  // square flags (back)
-            const u32 e = L[a.cap - 1 - k];
-            red_or(sbase + (e & 0x1FFFCu), 0x80u << ((e & 3) * 8));
-          }
-        } else {  // overflowed list: this producer's hits on the tile, recomputed exactly
-          if (lane == 0) atomicAdd(a.overflow, 1ull);
-          u64 j[NS];
-          for (u64 i = (u64)a.p_lo + b + (u64)lane * a.nprod; i < a.p_hi; i += 32ull * a.nprod) {
-            const u32 p = a.primes[i];
-            first_hits<W>(Ct, Cd, a.rprimes[i], p, j);
-            for (int s = 0; s < NS; s++)
-              for (u64 jj = j[s]; jj < S2_T; jj += NS * p)
-                red_add(sbase + ((u32)jj & ~3u), (u32)a.logs[i] << (((u32)jj & 3) * 8));
-          }
-          for (u64 i = (u64)a.q_lo + b + (u64)lane * a.nprod; i < a.q_hi; i += 32ull * a.nprod) {
-            const u64 p = a.primes[i];
-            first_hits<W>(Ct, Cd, __drcp_rn((double)(p * p)), p * p, j);
-            for (int s = 0; s < NS; s++)
-              if (j[s] < S2_T) red_or(sbase + ((u32)j[s] & ~3u), 0x80u << (((u32)j[s] & 3) * 8));
-          }
+        }
+        // square flags (back of each list)
+        const u32 s0 = cw0 >> 16, ns = s0 + (cw1 >> 16);
+        const u32* __restrict__ Q0 = L0 + a.cap - 1;
+        const u32* __restrict__ Q1 = L1 + a.cap - 1 + s0;
+        for (u32 k = lane; k < ns; k += 32) {
+          const u32 e = *((k < s0 ? Q0 : Q1) - k);
+          red_or(sbase + (e & 0x1FFFCu), 0x80u << ((e & 3) * 8));
         }
       }
     }

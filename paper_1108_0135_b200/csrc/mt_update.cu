@@ -238,28 +238,74 @@ __device__ __forceinline__ int count_le(const u32* mL, u64 mhw, int tot, u64 mc,
 // fast-path walks over list entries [i0, i1): two entries jointly (every entry
 // read from shared memory serves both) or one alone.  Sums of the estimates'
 // double bits and counts of negative 32-bit remainders (the corrections).
+#ifndef CT_VEC
+#define CT_VEC 1  // list entries read as 16-byte vectors (4 entries: 2 x 16 B of 1/m, 16 B of m)
+#endif
+#ifndef CT_VUNROLL
+#define CT_VUNROLL 2  // 4-entry blocks per iteration of the joint walk
+#endif
+#define MT_PRAGMA_(x) _Pragma(#x)
+#define MT_UNROLL(n) MT_PRAGMA_(unroll n)
 template <bool MINUS>
 __device__ __forceinline__ void walk2(const double* rmL, const u32* mL, int i0, int i1, double vdA, u32 vA,
                                       double vdB, u32 vB, u64& pA, u32& cA, u64& pB, u32& cB) {
-#pragma unroll 8
-  for (int i = i0; i < i1; i++) {
-    const int idx = MINUS ? MT_CM - 1 - i : i;
-    const double r = rmL[idx];
-    const u32 m = mL[idx];
+  auto item = [&](double r, u32 m) {
     const u64 bA = (u64)__double_as_longlong(fma(vdA, r, MT_TWO52));
     const u64 bB = (u64)__double_as_longlong(fma(vdB, r, MT_TWO52));
     pA += bA; cA += (vA + (u32)bA * m) >> 31;
     pB += bB; cB += (vB + (u32)bB * m) >> 31;
+  };
+  int i = i0;
+#if CT_VEC
+  // blocks of 4 entries at indices 4k.. (minus list: MT_CM - 4 - 4k.., read in any
+  // order: only the set summed matters), scalar entries before and after
+#pragma unroll 1
+  for (; i < i1 && (i & 3); i++) {
+    const int idx = MINUS ? MT_CM - 1 - i : i;
+    item(rmL[idx], mL[idx]);
+  }
+  MT_UNROLL(CT_VUNROLL)
+  for (; i + 4 <= i1; i += 4) {
+    const int b = MINUS ? MT_CM - 4 - i : i;
+    const double2 r01 = *(const double2*)(rmL + b), r23 = *(const double2*)(rmL + b + 2);
+    const uint4 m4 = *(const uint4*)(mL + b);
+    item(r01.x, m4.x); item(r01.y, m4.y); item(r23.x, m4.z); item(r23.y, m4.w);
+  }
+#else
+#pragma unroll 8
+#endif
+  for (; i < i1; i++) {
+    const int idx = MINUS ? MT_CM - 1 - i : i;
+    item(rmL[idx], mL[idx]);
   }
 }
 template <bool MINUS>
 __device__ __forceinline__ void walk1(const double* rmL, const u32* mL, int i0, int i1, double vd, u32 v, u64& p,
                                       u32& c) {
-#pragma unroll 2
-  for (int i = i0; i < i1; i++) {
+  auto item = [&](double r, u32 m) {
+    const u64 b = (u64)__double_as_longlong(fma(vd, r, MT_TWO52));
+    p += b; c += (v + (u32)b * m) >> 31;
+  };
+  int i = i0;
+#if CT_VEC
+#pragma unroll 1
+  for (; i < i1 && (i & 3); i++) {
     const int idx = MINUS ? MT_CM - 1 - i : i;
-    const u64 b = (u64)__double_as_longlong(fma(vd, rmL[idx], MT_TWO52));
-    p += b; c += (v + (u32)b * mL[idx]) >> 31;
+    item(rmL[idx], mL[idx]);
+  }
+#pragma unroll 1
+  for (; i + 4 <= i1; i += 4) {
+    const int b = MINUS ? MT_CM - 4 - i : i;
+    const double2 r01 = *(const double2*)(rmL + b), r23 = *(const double2*)(rmL + b + 2);
+    const uint4 m4 = *(const uint4*)(mL + b);
+    item(r01.x, m4.x); item(r01.y, m4.y); item(r23.x, m4.z); item(r23.y, m4.w);
+  }
+#else
+#pragma unroll 2
+#endif
+  for (; i < i1; i++) {
+    const int idx = MINUS ? MT_CM - 1 - i : i;
+    item(rmL[idx], mL[idx]);
   }
 }
 
