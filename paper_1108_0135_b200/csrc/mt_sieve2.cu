@@ -141,9 +141,6 @@ __device__ __forceinline__ void first_hits(u64 C0, double Cd, double rm, u64 m, 
 #ifndef FITEM
 #define FITEM 32     // hits per item (1024 items per round: ~32k hits over the tiles)
 #endif
-#ifndef FILL_CONTIG
-#define FILL_CONTIG 1  // a thread's items of a round are contiguous (one search per round)
-#endif
 template <int W>
 __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
   constexpr int NS = Wheel<W>::NS;
@@ -238,23 +235,6 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
     __syncthreads();
     if (tid == 0) s_hits = 0;
     for (u32 r0 = 0; r0 < nit; r0 += 1024 * per) {
-#if FILL_CONTIG
-      // thread tid takes the round's items [r0 + tid*per, r0 + (tid+1)*per): one search,
-      // then the stream index only moves forward
-      const u32 it0 = r0 + tid * per, it1 = min(min(nit, r0 + 1024 * per), it0 + per);
-      u32 kc = 0;
-      if (it0 < it1) {
-        u32 lo = 0, hi = FBATCH;  // largest k with s_ipre[k] <= it0
-        while (hi - lo > 1) {
-          const u32 mid = (lo + hi) >> 1;
-          if (s_ipre[mid] <= it0) lo = mid; else hi = mid;
-        }
-        kc = lo;
-      }
-      for (u32 it = it0; it < it1; it++) {
-        while (s_ipre[kc + 1] <= it) kc++;
-        const u32 k = kc, ci = it - s_ipre[k];
-#else
       for (u32 it = r0 + tid; it < min(nit, r0 + 1024 * per); it += 1024) {
         u32 lo = 0, hi = FBATCH;  // largest k with s_ipre[k] <= it
         while (hi - lo > 1) {
@@ -262,7 +242,6 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
           if (s_ipre[mid] <= it) lo = mid; else hi = mid;
         }
         const u32 k = lo, ci = it - s_ipre[k];
-#endif
         const u32 step = s_step[k], val = s_val[k];
         u32 pos = s_q0[k] + ci * FITEM * step;
         const u32 end = (u32)min((u64)R, (u64)pos + (u64)FITEM * step);
