@@ -517,8 +517,8 @@ def _rooflines(st, kms, kcnt, nsm):
         m = nm.get("k_counted", {})
         roof_u = {"kernel": "counted", "bound": "issue", "achieved": A, "peak": Pk, "unit": "T items/s",
                   "frac": A / Pk,
-                  "per_unit": "one odd squarefree m of a walk entry (DESIGN.md §2.1: entries walk odd m up to "
-                              "their largest prefix limit; 4/pi^2 of those m): DFMA (fp64 reciprocal quotient) + IMAD "
+                  "per_unit": "one squarefree m coprime to 6 of a walk entry (DESIGN.md §2.1: entries walk those "
+                              "m up to their largest role limit; 3/pi^2 of the m): DFMA (fp64 reciprocal quotient) + IMAD "
                               "(remainder) + 2 ALU (accumulate, correction) = 4 issue slots",
                   "units_per_step": items,
                   "peak_source": "4 warp-instructions/clk/SM x 32 lanes / 4 slots x SMs x sm_max_mhz; the "
@@ -537,10 +537,11 @@ def _rooflines(st, kms, kcnt, nsm):
 
 
 def _counted_units(st):
-    """Odd squarefree m the counted walk processes in one step, in closed form: every
-    element k walks odd m up to max(mcut_k, floor(mcut_{k/2}/2)) (the second limit for even
-    k), and every k with 2k > K adds a virtual half walk up to floor(mcut_k/2); 4/pi^2 of
-    the m are odd and squarefree.  mcut is the reference's (engine.py:144-158)."""
+    """Squarefree m coprime to 6 the counted walk processes in one step, in closed form:
+    entry j (an element j <= K, or a virtual j = 2k, 3k, 6k > K) walks up to the largest
+    of its role limits, mcut_j (own, j <= K) and floor(mcut_{j/d}/d) for d = 2, 3, 6 with
+    d | j and j/d <= K; 3/pi^2 of the m are squarefree and coprime to 6.
+    mcut is the reference's (engine.py:144-158)."""
     n, u = int(st["_n"]), int(st["_u"])
     K = n // u
     k = np.arange(1, K + 1, dtype=np.uint64)
@@ -555,11 +556,12 @@ def _counted_units(st):
     D = v // np.uint64(u + 1)
     xc = np.maximum(np.maximum(D, v // t), np.uint64(1))
     mc = (v // (xc + np.uint64(1))).astype(np.float64)
-    lim = mc.copy()
-    even = np.arange(2, K + 1, 2)
-    lim[even - 1] = np.maximum(mc[even - 1], np.floor(mc[even // 2 - 1] / 2))
-    total = float(lim.sum()) + float(np.floor(mc[K // 2:] / 2).sum())
-    return 4 / 3.141592653589793 ** 2 * total
+    lim = np.zeros(6 * K + 1)
+    lim[1:K + 1] = mc
+    kk = np.arange(1, K + 1)
+    for d in (2, 3, 6):
+        lim[d * kk] = np.maximum(lim[d * kk], np.floor(mc / d))
+    return 3 / 3.141592653589793 ** 2 * float(lim.sum())
 
 
 class _SinglePlan:

@@ -12,7 +12,7 @@
 #define MT_WHEEL_WORDS (MT_WHEEL / 4)
 #define MT_CT 256               // elements per counted-walk tile (threads per CTA)
 #ifndef MT_CM
-#define MT_CM 2048              // list capacity of a counted-walk work unit (odd m of 2*MT_CM consecutive m)
+#define MT_CM 1376              // list capacity of a counted-walk work unit (the m coprime to 6 of MT_CU consecutive m)
 #endif
 #define MT_BLK 32768u           // M16 block: values stored relative to M(block start - 1)
 #define MT_WIN_SPLIT 64         // d_sp = ceil(sqrt(v)/64): windowed walk up to y ~ 64 sqrt(v)
@@ -225,15 +225,17 @@ struct Shard {
 // counted-walk entries (mt_update.cu): the elements, then the virtual halves
 // v = floor(v_k / 2) of the elements with 2k > K; each adds S_o(v, lim1) to acc[t1]
 // and subtracts S_o(v, lim2) from acc[t2] (t = 0xFFFFFFFF: none)
+// counted-walk entries: the elements and the virtual values floor(n/j),
+// j = 2k, 3k, 6k > K.  Role r of an entry adds mu(d) S_6(v, lim[r]) to acc[tg[r]],
+// d = 1, 2, 3, 6 for r = 0..3 (tg = 0xFFFFFFFF: no such role)
+#define CE_ROLES 4
 struct CountedEntries {
   double* vd;
   uint64_t* vlo;
   uint64_t* vhi;
   uint8_t* vbits;
-  uint64_t* lim1;
-  uint64_t* lim2;
-  uint32_t* t1;
-  uint32_t* t2;
+  uint64_t* lim[CE_ROLES];
+  uint32_t* tg[CE_ROLES];
   uint64_t n;
 };
 // Kt: K of every target (host), in element order

@@ -34,7 +34,7 @@ struct UpdateCtx {
   ElemDev E;
   uint64_t* acc;
   int32_t* Mmc;
-  CountedEntries C;          // counted-walk entries (elements + virtual halves)
+  CountedEntries C;          // counted-walk entries (elements + virtual j = 2k, 3k, 6k > K)
   uint64_t* tile_max;        // [ntiles] max walk limit of each MT_CT-entry tile
   uint8_t* tile_vbits;       // [ntiles] max bit length of v in the tile
   uint64_t ntiles;
@@ -62,22 +62,25 @@ struct UpdateCtx {
 };
 
 // ---------------------------------------------------------------- counted walk
-// Odd-m form (round 2).  With S(v, x) = sum_{m<=x} mu(m) floor(v/m) and S_o the
-// same sum over odd m only, mu(2m') = -mu(m') for odd m' and floor(v/(2m')) =
-// floor(floor(v/2)/m') give
-//   S(v, x) = S_o(v, x) - S_o(floor(v/2), floor(x/2)),
-// and floor(v_k/2) = v_{2k}.  So the counted sum of element k,
-//   C_k = S(v_k, mcut_k) = S_o(v_k, mcut_k) - S_o(v_{2k}, floor(mcut_k/2)),
-// needs only odd m, and its second term is a prefix of element 2k's own odd walk.
-// Every "counted entry" walks the odd squarefree m up to max(lim1, lim2) and adds
-//   + S_o(v, lim1) to acc[t1]   (its own C_k part, lim1 = mcut_k)
-//   - S_o(v, lim2) to acc[t2]   (the half part of element k/2: lim2 = floor(mcut_{k/2}/2))
-// Entries 0..NE-1 are the elements; elements with 2k > K get a virtual entry
-// v = floor(v_k/2), lim1 = 0, lim2 = floor(mcut_k/2), t2 = k.  The work drops from
-// 6/pi^2 to 4/pi^2 of the m per element (plus the virtual halves): 24 % fewer items.
-// Work units are (tile of MT_CT entries) x (MT_CU consecutive m, i.e. MT_CM odd m).
-#define MT_CU (2 * MT_CM)  // m per counted unit (its odd m fill one list of MT_CM)
+// Wheel-6 form (round 2).  With S(v, x) = sum_{m<=x} mu(m) floor(v/m) and S_6 the
+// same sum over the m coprime to 6, mu(d m') = mu(d) mu(m') for d | 6 and m'
+// coprime to 6, and floor(v/(d m')) = floor(floor(v/d)/m') give
+//   S(v, x) = S_6(v, x) - S_6(v/2, x/2) - S_6(v/3, x/3) + S_6(v/6, x/6)
+// (floors throughout), and floor(v_k/d) = v_{dk}.  So the counted sum of element k,
+// C_k = S(v_k, mcut_k), needs only the m coprime to 6 (a third of the m), and its
+// d-parts are prefixes of the walks of entries dk.  Every "counted entry" j walks
+// the squarefree m coprime to 6 up to its largest limit and, for each role
+//   r = 0 (d = 1): + S_6(v_j, mcut_j)          to acc[j]      (its own part)
+//   r = 1, 2, 3 (d = 2, 3, 6), d | j:
+//          mu(d) S_6(v_j, floor(mcut_{j/d} / d)) to acc[j/d]
+// Entries 0..NE-1 are the elements; the values floor(n/j) with j = 2k, 3k, 6k > K
+// (k <= K) get virtual entries (roles r >= 1 only, k_ce_virtual).  Work per element
+// drops from the odd m (4/pi^2 of the m) to 3/pi^2 of them, plus the virtual parts.
+// Work units are (tile of MT_CT entries) x (MT_CU consecutive m, <= MT_CM of them
+// coprime to 6).
+#define MT_CU 4096  // m per counted unit
 static_assert((MT_CU & (MT_CU - 1)) == 0, "counted units must be powers of two (units never straddle 2^32)");
+static_assert(MT_CM >= MT_CU / 3 + 1 && MT_CM % 4 == 0, "the list holds a unit's m coprime to 6, in 4-entry blocks");
 
 __global__ void k_counted_plan(const uint64_t* __restrict__ tile_max, uint64_t ntiles, u64 Y0,
                                u64 R, uint64_t* __restrict__ units) {
@@ -94,25 +97,71 @@ __global__ void k_counted_plan(const uint64_t* __restrict__ tile_max, uint64_t n
   units[t] = n;
 }
 
-// counted entries from the elements (one thread per element): the element's own
-// entry at e, and for 2k > K its virtual half entry at vbase[t] + (k - floor(K/2) - 1)
-__global__ void k_ce_init(ElemDev E, const u64* __restrict__ Kt, const u64* __restrict__ vbase, CountedEntries C) {
+// counted entries from the elements (one thread per element): roles 0 (own) and
+// d = 2, 3, 6 for d | k (the d-part of element k/d, at index e - (k - k/d))
+__global__ void k_ce_init(ElemDev E, CountedEntries C) {
   const u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E.n) return;
   const u64 k = E.k[e];
-  const uint32_t t = E.tgt[e];
-  const u64 K = Kt[t];
-  const u64 mc = E.mcut[e];
   C.vd[e] = E.vd[e]; C.vlo[e] = E.vlo[e]; C.vhi[e] = E.vhi[e]; C.vbits[e] = E.vbits[e];
-  C.lim1[e] = mc; C.t1[e] = (u32)e;
-  if (k % 2 == 0) { C.lim2[e] = E.mcut[e - k / 2] / 2; C.t2[e] = (u32)(e - k / 2); }
-  else { C.lim2[e] = 0; C.t2[e] = 0xFFFFFFFFu; }
-  if (2 * k > K) {  // v_{2k} = floor(v_k / 2) < 2^64 (2k > K = floor(n/u): v_{2k} <= 2u)
-    const u64 c = vbase[t] + (k - K / 2 - 1);
-    const u64 vh = (E.vhi[e] << 63) | (E.vlo[e] >> 1);
-    C.vd[c] = __ull2double_rn(vh); C.vlo[c] = vh; C.vhi[c] = 0; C.vbits[c] = (uint8_t)(vh ? 64 - __clzll((long long)vh) : 0);
-    C.lim1[c] = 0; C.t1[c] = 0xFFFFFFFFu;
-    C.lim2[c] = mc / 2; C.t2[c] = (u32)e;
+  C.lim[0][e] = E.mcut[e]; C.tg[0][e] = (u32)e;
+  const u32 dd[3] = {2, 3, 6};
+#pragma unroll
+  for (int r = 1; r < CE_ROLES; r++) {
+    const u32 d = dd[r - 1];
+    if (k % d == 0) {
+      const u64 ep = e - (k - k / d);
+      C.lim[r][e] = E.mcut[ep] / d; C.tg[r][e] = (u32)ep;
+    } else {
+      C.lim[r][e] = 0; C.tg[r][e] = 0xFFFFFFFFu;
+    }
+  }
+}
+
+// j <= x with j mod 6 in {0, 2, 3, 4} (the j divisible by 2 or 3)
+__host__ __device__ __forceinline__ u64 ce_cnt23(u64 x) { const u64 r = x % 6; return 4 * (x / 6) + (r >= 2) + (r >= 3) + (r >= 4); }
+
+// virtual entries of one target (K, its first element index ebase): the j > K of the
+// form 2k, 3k, 6k (k <= K) in increasing j: A = j in (K, 2K] divisible by 2 or 3,
+// B = 3i in (2K, 3K], C = 6i in (3K, 6K]; VirtSpec holds per target the first
+// entry index and the A/B/C counts
+struct VirtSpec { u64 base, K, ebase, nA, nB, nC; };
+__global__ void k_ce_virtual(ElemDev E, const VirtSpec* __restrict__ vs, int ntgt, u64 ntot, CountedEntries C) {
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntot) return;
+  int t = 0;
+  while (t + 1 < ntgt && vs[t + 1].base <= vs[0].base + i) t++;
+  const VirtSpec S = vs[t];
+  const u64 c = vs[0].base + i, s = c - S.base, K = S.K;
+  u64 j;
+  if (s < S.nA) {
+    const u64 q = ce_cnt23(K) + s;  // 0-based rank among the j divisible by 2 or 3
+    const u64 r = q % 4;
+    j = 6 * (q / 4) + (r == 0 ? 2 : r == 1 ? 3 : r == 2 ? 4 : 6);
+  } else if (s < S.nA + S.nB) {
+    j = 3 * ((2 * K) / 3 + 1 + (s - S.nA));
+  } else {
+    j = 6 * (K / 2 + 1 + (s - S.nA - S.nB));
+  }
+  C.lim[0][c] = 0; C.tg[0][c] = 0xFFFFFFFFu;
+  const u32 dd[3] = {2, 3, 6};
+  bool have = false;
+#pragma unroll
+  for (int r = 1; r < CE_ROLES; r++) {
+    const u32 d = dd[r - 1];
+    if (j % d == 0 && j / d <= K) {
+      const u64 ep = S.ebase + j / d - 1;
+      C.lim[r][c] = E.mcut[ep] / d; C.tg[r][c] = (u32)ep;
+      if (!have) {  // v_j = floor(v_{j/d} / d) (< 2^64: j > K = floor(n/u) gives v_j <= u)
+        const u128 v = (((u128)E.vhi[ep] << 64) | E.vlo[ep]) / d;
+        const u64 vl = (u64)v;
+        C.vd[c] = __ull2double_rn(vl); C.vlo[c] = vl; C.vhi[c] = 0;
+        C.vbits[c] = (uint8_t)(vl ? 64 - __clzll((long long)vl) : 0);
+        have = true;
+      }
+    } else {
+      C.lim[r][c] = 0; C.tg[r][c] = 0xFFFFFFFFu;
+    }
   }
 }
 
@@ -120,7 +169,11 @@ __global__ void k_ce_tiles(CountedEntries C, uint64_t* __restrict__ tmax, uint8_
   const u64 t = blockIdx.x, c = t * MT_CT + threadIdx.x;
   u64 m = 0;
   int b = 0;
-  if (c < C.n) { m = max(C.lim1[c], C.lim2[c]); b = C.vbits[c]; }
+  if (c < C.n) {
+#pragma unroll
+    for (int r = 0; r < CE_ROLES; r++) m = max(m, C.lim[r][c]);
+    b = C.vbits[c];
+  }
   typedef cub::BlockReduce<u64, MT_CT> BR;
   typedef cub::BlockReduce<int, MT_CT> BRi;
   __shared__ typename BR::TempStorage s1;
@@ -309,42 +362,44 @@ __device__ __forceinline__ void walk1(const double* rmL, const u32* mL, int i0, 
   }
 }
 
-// one list (plus or minus) for the thread's two entries with prefix lengths
-// (lA1, lA2) and (lB1, lB2): the walk is cut at every prefix end, the two entries
-// walk jointly while both still need entries, and each prefix's value
-// (sum of floor(v/m) = bits - L*2^52*... - corrections) is recorded
+// one list (plus or minus) for the thread's two entries A, B with the prefix
+// lengths lA[r], lB[r] of their roles r (0 = none): the walk is cut at every
+// distinct positive length in ascending order (in the common case every thread
+// has one, the whole list, so the walks of a warp stay in lockstep), the two
+// entries walk jointly while both still need entries, and at a role's cut its
+// prefix value (sum of floor(v/m) = bits - L*2^52 - corrections), signed by the
+// role and the list, goes straight to the role's accumulator
 template <bool MINUS>
 __device__ __forceinline__ void walk_list(const double* rmL, const u32* mL, double vdA, u32 vA, double vdB, u32 vB,
-                                          int lA1, int lA2, int lB1, int lB2, u64* outA, u64* outB) {
-  int cut[4] = {lA1, lA2, lB1, lB2};
+                                          const int (&lA)[CE_ROLES], const int (&lB)[CE_ROLES],
+                                          const u32 (&tA)[CE_ROLES], const u32 (&tB)[CE_ROLES], uint64_t* acc) {
+  int mA = 0, mB = 0;
 #pragma unroll
-  for (int i = 0; i < 3; i++)
-#pragma unroll
-    for (int j = 0; j < 3 - i; j++)
-      if (cut[j] > cut[j + 1]) { const int t = cut[j]; cut[j] = cut[j + 1]; cut[j + 1] = t; }
-  // distinct positive cuts, ascending: in the common case every thread has one
-  // (the whole list), so the walks of a warp stay in lockstep
-  int nc = 0, cc[4];
-#pragma unroll
-  for (int i = 0; i < 4; i++)
-    if (cut[i] > 0 && (i == 0 || cut[i] != cut[i - 1])) { cc[nc] = cut[i]; nc++; }
-  const int mA = max(lA1, lA2), mB = max(lB1, lB2);
+  for (int r = 0; r < CE_ROLES; r++) { mA = max(mA, lA[r]); mB = max(mB, lB[r]); }
   u64 pA = 0, pB = 0;
   u32 cA = 0, cB = 0;
   int pos = 0;
-  outA[0] = outA[1] = outB[0] = outB[1] = 0;
 #pragma unroll 1
-  for (int k = 0; k < nc; k++) {
-    const int c = cc[k];
+  for (;;) {
+    int c = 0x7FFFFFFF;
+#pragma unroll
+    for (int r = 0; r < CE_ROLES; r++) {
+      if (lA[r] > pos) c = min(c, lA[r]);
+      if (lB[r] > pos) c = min(c, lB[r]);
+    }
+    if (c == 0x7FFFFFFF) break;
     if (mA > pos && mB > pos) walk2<MINUS>(rmL, mL, pos, c, vdA, vA, vdB, vB, pA, cA, pB, cB);
     else if (mA > pos) walk1<MINUS>(rmL, mL, pos, c, vdA, vA, pA, cA);
     else walk1<MINUS>(rmL, mL, pos, c, vdB, vB, pB, cB);
     pos = c;
     const u64 vAv = pA - (u64)c * MT_EXP52 - cA, vBv = pB - (u64)c * MT_EXP52 - cB;
-    if (c == lA1) outA[0] = vAv;
-    if (c == lA2) outA[1] = vAv;
-    if (c == lB1) outB[0] = vBv;
-    if (c == lB2) outB[1] = vBv;
+#pragma unroll
+    for (int r = 0; r < CE_ROLES; r++) {
+      // role sign mu(d) (d = 1, 2, 3, 6: + - - +), negated on the minus list
+      const bool neg = ((r == 1 || r == 2) != MINUS);
+      if (lA[r] == c) atomicAdd((unsigned long long*)(acc + tA[r]), (unsigned long long)(neg ? 0ull - vAv : vAv));
+      if (lB[r] == c) atomicAdd((unsigned long long*)(acc + tB[r]), (unsigned long long)(neg ? 0ull - vBv : vBv));
+    }
   }
 }
 
@@ -380,16 +435,18 @@ __global__ void __launch_bounds__(CT_THREADS, CT_MINB) k_counted(CountedArgs a) 
     const u64 mx = a.tile_max[tau];
     if (mhi > mx + 1) mhi = mx + 1;
 
-    // ---- the unit's odd squarefree m: plus from the front, minus from the back
-    constexpr int PER = MT_CU / CT_THREADS;  // 32 m (16 odd) per thread
+    // ---- the unit's squarefree m coprime to 6: plus from the front, minus from the back
+    constexpr int PER = MT_CU / CT_THREADS;  // 32 m per thread
     const u64 m0 = mlo + (u64)tid * PER;
+    const u32 r3 = (u32)(m0 % 3);
     u64 bits[PER / 8];
 #pragma unroll
     for (int q = 0; q < PER / 8; q++) bits[q] = m0 + 8 * q < mhi ? *(const u64*)(a.mu + (m0 + 8 * q - a.Y0)) : 0;
     int np = 0, nn = 0;
 #pragma unroll
-    for (int b = 1; b < PER; b += 2) {  // odd m only (m0 is even)
-      const int8_t mu = (int8_t)((bits[b >> 3] >> (8 * (b & 7))) & 0xff);
+    for (int b = 1; b < PER; b += 2) {  // odd m (m0 is even) not divisible by 3
+      const u32 s3 = r3 + (u32)(b % 3);
+      const int8_t mu = (s3 == 0 || s3 == 3) ? 0 : (int8_t)((bits[b >> 3] >> (8 * (b & 7))) & 0xff);
       const bool in = m0 + b < mhi;
       np += (in && mu > 0);
       nn += (in && mu < 0);
@@ -412,7 +469,8 @@ __global__ void __launch_bounds__(CT_THREADS, CT_MINB) k_counted(CountedArgs a) 
     int op = bp + ip - np, on = bn + in_ - nn;
 #pragma unroll
     for (int b = 1; b < PER; b += 2) {
-      const int8_t mu = (int8_t)((bits[b >> 3] >> (8 * (b & 7))) & 0xff);
+      const u32 s3 = r3 + (u32)(b % 3);
+      const int8_t mu = (s3 == 0 || s3 == 3) ? 0 : (int8_t)((bits[b >> 3] >> (8 * (b & 7))) & 0xff);
       const u64 m = m0 + b;
       if (m < mhi && mu != 0) {
         const double r = __drcp_rn((double)m);
@@ -422,49 +480,47 @@ __global__ void __launch_bounds__(CT_THREADS, CT_MINB) k_counted(CountedArgs a) 
     }
     __syncthreads();
 
-    // ---- the two entries' walks: prefix lengths for (lim1, lim2) in both lists
+    // ---- the two entries' roles: prefix lengths of every role's limit in both lists
     const u64 mhw = mlo & 0xFFFFFFFF00000000ull;
     const u64 cA = tau * MT_CT + tid, cB = cA + CT_THREADS;
-    int pA1 = 0, pA2 = 0, nA1 = 0, nA2 = 0, pB1 = 0, pB2 = 0, nB1 = 0, nB2 = 0;
-    u32 tA1 = 0xFFFFFFFFu, tA2 = 0xFFFFFFFFu, tB1 = 0xFFFFFFFFu, tB2 = 0xFFFFFFFFu;
+    int pA[CE_ROLES], nA[CE_ROLES], pB[CE_ROLES], nB[CE_ROLES];
+    u32 tA[CE_ROLES], tB[CE_ROLES];
     auto lens = [&](u64 lim, int& pl, int& nl) {
       if (lim < mlo) { pl = nl = 0; return; }
       if (lim + 1 >= mhi) { pl = totp; nl = totn; return; }
       pl = count_le(mL, mhw, totp, lim, false);
       nl = count_le(mL, mhw, totn, lim, true);
     };
-    if (cA < a.C.n) {
-      tA1 = a.C.t1[cA]; tA2 = a.C.t2[cA];
-      if (tA1 != 0xFFFFFFFFu) lens(a.C.lim1[cA], pA1, nA1);
-      if (tA2 != 0xFFFFFFFFu) lens(a.C.lim2[cA], pA2, nA2);
-    }
-    if (cB < a.C.n) {
-      tB1 = a.C.t1[cB]; tB2 = a.C.t2[cB];
-      if (tB1 != 0xFFFFFFFFu) lens(a.C.lim1[cB], pB1, nB1);
-      if (tB2 != 0xFFFFFFFFu) lens(a.C.lim2[cB], pB2, nB2);
+#pragma unroll
+    for (int r = 0; r < CE_ROLES; r++) {
+      pA[r] = nA[r] = pB[r] = nB[r] = 0;
+      tA[r] = cA < a.C.n ? a.C.tg[r][cA] : 0xFFFFFFFFu;
+      tB[r] = cB < a.C.n ? a.C.tg[r][cB] : 0xFFFFFFFFu;
+      if (tA[r] != 0xFFFFFFFFu) lens(a.C.lim[r][cA], pA[r], nA[r]);
+      if (tB[r] != 0xFFFFFFFFu) lens(a.C.lim[r][cB], pB[r], nB[r]);
     }
     const int vb = a.tile_vbits[tau];
     const bool fast = !(a.force_wide & (MT_FLAG_FORCE_SLOWDIV | MT_FLAG_FORCE_WIDE)) &&
                       ((vb <= 50) || (mlo >= (1ull << (vb - 50)))) && mhi <= (1ull << 31);
-    u64 SA1 = 0, SA2 = 0, SB1 = 0, SB2 = 0;
     if (fast) {
       const double vdA = cA < a.C.n ? a.C.vd[cA] : 0.0, vdB = cB < a.C.n ? a.C.vd[cB] : 0.0;
       const u32 vA = cA < a.C.n ? (u32)a.C.vlo[cA] : 0u, vB = cB < a.C.n ? (u32)a.C.vlo[cB] : 0u;
-      u64 PA[2], PB[2], NA[2], NB[2];
-      walk_list<false>(rmL, mL, vdA, vA, vdB, vB, pA1, pA2, pB1, pB2, PA, PB);
-      walk_list<true>(rmL, mL, vdA, vA, vdB, vB, nA1, nA2, nB1, nB2, NA, NB);
-      SA1 = PA[0] - NA[0]; SA2 = PA[1] - NA[1];
-      SB1 = PB[0] - NB[0]; SB2 = PB[1] - NB[1];
+      walk_list<false>(rmL, mL, vdA, vA, vdB, vB, pA, pB, tA, tB, a.acc);
+      walk_list<true>(rmL, mL, vdA, vA, vdB, vB, nA, nB, tA, tB, a.acc);
     } else {
-      if (pA1 + nA1) SA1 = counted_one(a, cA, tau, mlo, mhi, pA1, nA1, rmL, mL);
-      if (pA2 + nA2) SA2 = counted_one(a, cA, tau, mlo, mhi, pA2, nA2, rmL, mL);
-      if (pB1 + nB1) SB1 = counted_one(a, cB, tau, mlo, mhi, pB1, nB1, rmL, mL);
-      if (pB2 + nB2) SB2 = counted_one(a, cB, tau, mlo, mhi, pB2, nB2, rmL, mL);
+#pragma unroll 1
+      for (int r = 0; r < CE_ROLES; r++) {
+        const bool neg = (r == 1 || r == 2);
+        if (pA[r] + nA[r]) {
+          const u64 S = counted_one(a, cA, tau, mlo, mhi, pA[r], nA[r], rmL, mL);
+          atomicAdd((unsigned long long*)(a.acc + tA[r]), (unsigned long long)(neg ? 0ull - S : S));
+        }
+        if (pB[r] + nB[r]) {
+          const u64 S = counted_one(a, cB, tau, mlo, mhi, pB[r], nB[r], rmL, mL);
+          atomicAdd((unsigned long long*)(a.acc + tB[r]), (unsigned long long)(neg ? 0ull - S : S));
+        }
+      }
     }
-    if (pA1 + nA1) atomicAdd((unsigned long long*)(a.acc + tA1), (unsigned long long)SA1);
-    if (pA2 + nA2) atomicAdd((unsigned long long*)(a.acc + tA2), (unsigned long long)(0ull - SA2));
-    if (pB1 + nB1) atomicAdd((unsigned long long*)(a.acc + tB1), (unsigned long long)SB1);
-    if (pB2 + nB2) atomicAdd((unsigned long long*)(a.acc + tB2), (unsigned long long)(0ull - SB2));
     __syncthreads();
   }
 }
@@ -897,31 +953,43 @@ int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* 
   MT_CUDA_CHECK(cudaMalloc(&c->tgts, sizeof(TargetDev) * (ntgt ? ntgt : 1)));
   c->tgts_h.assign(tgts, tgts + ntgt);
   MT_CUDA_CHECK(cudaMemcpyAsync(c->tgts, tgts, sizeof(TargetDev) * ntgt, cudaMemcpyHostToDevice, st));
-  // counted entries: the NE elements, then per target the virtual halves of k > K/2
-  std::vector<u64> vbase(ntgt ? ntgt : 1), Kv(Kt, Kt + ntgt);
-  u64 nce = E.n;
-  for (int t = 0; t < ntgt; t++) { vbase[t] = nce; nce += Kt[t] - Kt[t] / 2; }
+  // counted entries: the NE elements (target t's k = 1..K_t from ebase_t on), then
+  // per target its virtual entries (k_ce_virtual)
+  std::vector<VirtSpec> vs(ntgt ? ntgt : 1);
+  u64 nce = E.n, eb = 0;
+  for (int t = 0; t < ntgt; t++) {
+    const u64 K = Kt[t];
+    VirtSpec& v = vs[t];
+    v.base = nce; v.K = K; v.ebase = eb;
+    v.nA = ce_cnt23(2 * K) - ce_cnt23(K);
+    v.nB = K - (2 * K) / 3;
+    v.nC = K - K / 2;
+    nce += v.nA + v.nB + v.nC;
+    eb += K;
+  }
   CountedEntries& C = c->C;
   C.n = nce;
   const u64 na = nce ? nce : 1;
   MT_CUDA_CHECK(cudaMalloc(&C.vd, na * 8)); MT_CUDA_CHECK(cudaMalloc(&C.vlo, na * 8)); MT_CUDA_CHECK(cudaMalloc(&C.vhi, na * 8));
-  MT_CUDA_CHECK(cudaMalloc(&C.vbits, na)); MT_CUDA_CHECK(cudaMalloc(&C.lim1, na * 8)); MT_CUDA_CHECK(cudaMalloc(&C.lim2, na * 8));
-  MT_CUDA_CHECK(cudaMalloc(&C.t1, na * 4)); MT_CUDA_CHECK(cudaMalloc(&C.t2, na * 4));
+  MT_CUDA_CHECK(cudaMalloc(&C.vbits, na));
+  for (int r = 0; r < CE_ROLES; r++) {
+    MT_CUDA_CHECK(cudaMalloc(&C.lim[r], na * 8));
+    MT_CUDA_CHECK(cudaMalloc(&C.tg[r], na * 4));
+  }
   c->ntiles = (nce + MT_CT - 1) / MT_CT;
   MT_CUDA_CHECK(cudaMalloc(&c->tile_max, (c->ntiles + 1) * 8));
   MT_CUDA_CHECK(cudaMalloc(&c->tile_vbits, c->ntiles + 1));
   {
-    u64 *dK = nullptr, *dvb = nullptr;
-    MT_CUDA_CHECK(cudaMalloc(&dK, 8 * (ntgt ? ntgt : 1)));
-    MT_CUDA_CHECK(cudaMalloc(&dvb, 8 * (ntgt ? ntgt : 1)));
-    MT_CUDA_CHECK(cudaMemcpyAsync(dK, Kv.data(), 8 * ntgt, cudaMemcpyHostToDevice, st));
-    MT_CUDA_CHECK(cudaMemcpyAsync(dvb, vbase.data(), 8 * ntgt, cudaMemcpyHostToDevice, st));
-    if (E.n) k_ce_init<<<(unsigned)((E.n + 255) / 256), 256, 0, st>>>(E, dK, dvb, C);
+    VirtSpec* dvs = nullptr;
+    MT_CUDA_CHECK(cudaMalloc(&dvs, sizeof(VirtSpec) * vs.size()));
+    MT_CUDA_CHECK(cudaMemcpyAsync(dvs, vs.data(), sizeof(VirtSpec) * ntgt, cudaMemcpyHostToDevice, st));
+    if (E.n) k_ce_init<<<(unsigned)((E.n + 255) / 256), 256, 0, st>>>(E, C);
+    const u64 nv = nce - E.n;
+    if (nv) k_ce_virtual<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(E, dvs, ntgt, nv, C);
     if (c->ntiles) k_ce_tiles<<<(unsigned)c->ntiles, MT_CT, 0, st>>>(C, c->tile_max, c->tile_vbits);
     MT_CUDA_CHECK(cudaGetLastError());
     MT_CUDA_CHECK(cudaStreamSynchronize(st));
-    cudaFree(dK);
-    cudaFree(dvb);
+    cudaFree(dvs);
   }
   const u64 ntiles = c->ntiles;
   MT_CUDA_CHECK(cudaMalloc(&c->units, sizeof(uint64_t) * (ntiles + 1) * 2));
@@ -944,8 +1012,9 @@ int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* 
 
 void mt_update_destroy(UpdateCtx* c) {
   if (!c) return;
-  cudaFree(c->C.vd); cudaFree(c->C.vlo); cudaFree(c->C.vhi); cudaFree(c->C.vbits); cudaFree(c->C.lim1);
-  cudaFree(c->C.lim2); cudaFree(c->C.t1); cudaFree(c->C.t2); cudaFree(c->tile_max); cudaFree(c->tile_vbits);
+  cudaFree(c->C.vd); cudaFree(c->C.vlo); cudaFree(c->C.vhi); cudaFree(c->C.vbits);
+  for (int r = 0; r < CE_ROLES; r++) { cudaFree(c->C.lim[r]); cudaFree(c->C.tg[r]); }
+  cudaFree(c->tile_max); cudaFree(c->tile_vbits);
   cudaFree(c->tgts); cudaFree(c->units); cudaFree(c->cnt); cudaFree(c->dtop); cudaFree(c->off);
   cudaFree(c->qcnt); cudaFree(c->qoff); cudaFree(c->counter);
   cudaFree(c->gunits); cudaFree(c->guoff); cudaFree(c->gwfirst);
