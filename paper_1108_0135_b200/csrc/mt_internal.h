@@ -12,7 +12,7 @@
 #define MT_WHEEL_WORDS (MT_WHEEL / 4)
 #define MT_CT 256               // elements per counted-walk tile (threads per CTA)
 #ifndef MT_CM
-#define MT_CM 1376              // list capacity of a counted-walk work unit (the m coprime to 6 of MT_CU consecutive m)
+#define MT_CM 2736              // list capacity of a counted-walk work unit (the m coprime to 6 of MT_CU consecutive m)
 #endif
 #define MT_BLK 32768u           // M16 block: values stored relative to M(block start - 1)
 #define MT_WIN_SPLIT 64         // d_sp = ceil(sqrt(v)/64): windowed walk up to y ~ 64 sqrt(v)

@@ -792,13 +792,23 @@ __global__ void __launch_bounds__(256) k_s3_finish(const int* __restrict__ tile_
   const i64 base = s_base;
   if (bk && tid < 4) bk[(u64)t * 4 + tid] = base + bkrel[(u64)t * 4 + tid];
   const u64 Yt = Y0 + (u64)t * span;
-  for (int c = 0; c < n_cap; c++) {
-    const CaptureTarget2& ct = caps[c];
-    u64 jhi = Yt ? udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt) : ~0ull;
-    u64 jlo = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt + span) + 1;
-    if (jlo < ct.jq0) jlo = ct.jq0;
-    if (jhi > ct.jq1) jhi = ct.jq1;
-    for (u64 j = jlo + tid; j <= jhi; j += blockDim.x) ct.Q[j - ct.jq0] += (int)base;
+  // the tile's j range of every capture target, one thread per target (two divisions each)
+  __shared__ u64 s_j[2][S2_MAXCAP];
+  for (int c0 = 0; c0 < n_cap; c0 += S2_MAXCAP) {
+    const int nc = min(n_cap - c0, S2_MAXCAP);
+    __syncthreads();
+    if (tid < nc) {
+      const CaptureTarget2& ct = caps[c0 + tid];
+      const u64 jhi = Yt ? udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt) : ~0ull;
+      const u64 jlo = udiv_any(ct.n_lo, ct.n_hi, ct.nd, ct.nbits, Yt + span) + 1;
+      s_j[0][tid] = jlo < ct.jq0 ? ct.jq0 : jlo;
+      s_j[1][tid] = jhi > ct.jq1 ? ct.jq1 : jhi;
+    }
+    __syncthreads();
+    for (int c = 0; c < nc; c++) {
+      const CaptureTarget2& ct = caps[c0 + c];
+      for (u64 j = s_j[0][c] + tid; j <= s_j[1][c]; j += blockDim.x) ct.Q[j - ct.jq0] += (int)base;
+    }
   }
   if (tid == 0) {
     if (t == ntiles - 1) ((volatile i64*)done)[1] = base + tile_sum[t];

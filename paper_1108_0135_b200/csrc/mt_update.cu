@@ -78,7 +78,9 @@ struct UpdateCtx {
 // drops from the odd m (4/pi^2 of the m) to 3/pi^2 of them, plus the virtual parts.
 // Work units are (tile of MT_CT entries) x (MT_CU consecutive m, <= MT_CM of them
 // coprime to 6).
-#define MT_CU 4096  // m per counted unit
+#ifndef MT_CU
+#define MT_CU 8192  // m per counted unit (measured: 8192 > 4096)
+#endif
 static_assert((MT_CU & (MT_CU - 1)) == 0, "counted units must be powers of two (units never straddle 2^32)");
 static_assert(MT_CM >= MT_CU / 3 + 1 && MT_CM % 4 == 0, "the list holds a unit's m coprime to 6, in 4-entry blocks");
 
@@ -408,7 +410,7 @@ __device__ __forceinline__ void walk_list(const double* rmL, const u32* mL, doub
 // loop overhead per item (the walk is issue-bound).
 #define CT_THREADS (MT_CT / 2)
 #ifndef CT_MINB
-#define CT_MINB 1
+#define CT_MINB 5  // 5 CTAs of 128 threads per SM (<= 102 registers; measured: 5 > 4 > 6)
 #endif
 __global__ void __launch_bounds__(CT_THREADS, CT_MINB) k_counted(CountedArgs a) {
   // dynamic: rmL[MT_CM] (1/m), then mL[MT_CM]: the low word of m, stored NEGATED (the
@@ -436,7 +438,7 @@ __global__ void __launch_bounds__(CT_THREADS, CT_MINB) k_counted(CountedArgs a) 
     if (mhi > mx + 1) mhi = mx + 1;
 
     // ---- the unit's squarefree m coprime to 6: plus from the front, minus from the back
-    constexpr int PER = MT_CU / CT_THREADS;  // 32 m per thread
+    constexpr int PER = MT_CU / CT_THREADS;  // 64 m per thread
     const u64 m0 = mlo + (u64)tid * PER;
     const u32 r3 = (u32)(m0 % 3);
     u64 bits[PER / 8];
