@@ -497,7 +497,7 @@ def _rooflines(st, kms, kcnt, nsm):
         m = nm.get("k_sieve3", {})
         roof_s = {"kernel": "sieve_tile", "bound": "hbm", "achieved": A, "peak": P_, "unit": "GB/s", "frac": A / P_,
                   "traffic": m.get("dram_bytes_per_launch"),
-                  "per_unit": "10 B per sieved value (SURVEY.md §8(d)); tail cells are odd y only",
+                  "per_unit": "10 B per sieved value (SURVEY.md §8(d)); a tail cell is a y coprime to 6",
                   "units_per_launch": cells / n_l, "avg_launch_ms": avg, "launches": n_l,
                   "y_covered_per_launch": (st["head_cells"] + 2 * st["tail_cells"]) / n_l,
                   "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in pk else "fallback",

@@ -114,6 +114,11 @@ int mt_sieve_bench(uint64_t Y0, uint64_t nseg, uint64_t y_last, double* ms_out);
 int mt_udiv128_batch(const uint64_t* v_lo, const uint64_t* v_hi, const uint64_t* m, uint64_t n,
                      uint64_t* q_lo, uint64_t* q_hi);
 
+/* the engine keeps its device buffers in the current device's memory pool between
+ * calls (a 1e19 plan maps several GB; re-mapping them per call costs ~0.1 s);
+ * this returns the cached blocks to the driver (no reference counterpart) */
+int mt_trim_device_memory(void);
+
 /* the paper's approximate algorithm (Eq. 2):
  * out[j] = q_n = 2 sum_{i<n_terms} a[i] cos(z[i] * delta_j + b[i]) in fp64, over a
  * shifted table (b[i] = b'_i for the table's x0; delta = ln x - x0).

@@ -105,6 +105,7 @@ def lib():
         "mt_sieve_odd": [_u64, _u64, vp],
         "mt_sieve_wheel": [_u64, _u64, ctypes.c_int, vp],
         "mt_udiv128_batch": [vp, vp, vp, _u64, vp, vp],
+        "mt_trim_device_memory": [],
         "mt_q_batch": [vp, vp, vp, _u64, ctypes.c_double, ctypes.c_double, _u64, vp],
         "mt_q_points": [vp, vp, vp, _u64, vp, _u64, vp],
         "mt_run": [ctypes.POINTER(MtJob), ctypes.POINTER(MtResult)],
@@ -163,7 +164,7 @@ EXPORTED_SYMBOLS = (
     "mt_last_error", "mt_abi_version", "mt_device_count", "mt_set_device",
     "mt_sieve_logprime", "mt_logprime_states", "mt_sieve_naive", "mt_apply_block",
     "mt_finalize", "mt_build_divisor_arrays", "mt_mertens_range", "mt_mertens_at", "mt_sieve_fast", "mt_sieve_odd", "mt_sieve_wheel", "mt_sieve_bench",
-    "mt_sieve_bench2", "mt_udiv128_batch", "mt_q_batch", "mt_q_points", "mt_run",
+    "mt_sieve_bench2", "mt_udiv128_batch", "mt_trim_device_memory", "mt_q_batch", "mt_q_points", "mt_run",
     "mt_plan_create", "mt_plan_sieve_update", "mt_plan_sieve_step", "mt_plan_checkpoint", "mt_plan_restore",
     "mt_plan_tail_offset", "mt_plan_q_slice", "mt_plan_cap_window", "mt_plan_acc",
     "mt_plan_gather", "mt_plan_resolve", "mt_plan_destroy",

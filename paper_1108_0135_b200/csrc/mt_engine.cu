@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -31,6 +32,70 @@
 #include "mt_internal.h"
 
 static thread_local char g_err[2048];
+
+// ------------------------------------------------------------ device memory
+namespace {
+struct PoolState {
+  bool init = false, on = false;
+  cudaStream_t st = nullptr;
+  cudaMemPool_t mp = nullptr;
+};
+PoolState g_pool[64];
+std::mutex g_pool_mu;
+PoolState& pool_for_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  PoolState& P = g_pool[dev & 63];
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!P.init) {
+    P.init = true;
+    const char* e = getenv("MT_POOL");
+    int sup = 0;
+    cudaDeviceGetAttribute(&sup, cudaDevAttrMemoryPoolsSupported, dev);
+    if (sup && !(e && atoi(e) == 0)) {
+      cudaMemPool_t mp;
+      if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+        P.mp = mp;
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+        if (cudaStreamCreateWithFlags(&P.st, cudaStreamNonBlocking) == cudaSuccess) P.on = true;
+      }
+    }
+    cudaGetLastError();
+  }
+  return P;
+}
+}  // namespace
+
+cudaError_t mt_dmalloc_raw(void** p, size_t bytes) {
+  PoolState& P = pool_for_device();
+  if (!P.on) return cudaMalloc(p, bytes);
+  cudaError_t e = cudaMallocAsync(p, bytes, P.st);
+  if (e == cudaErrorMemoryAllocation) {  // the pool's cached blocks do not fit: return them, retry
+    cudaGetLastError();
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(P.mp, 0);
+    e = cudaMallocAsync(p, bytes, P.st);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(P.st);  // usable from any stream
+  return e;
+}
+
+extern "C" int mt_trim_device_memory(void) {
+  PoolState& P = pool_for_device();
+  if (!P.on) return MT_OK;
+  cudaDeviceSynchronize();
+  cudaMemPoolTrimTo(P.mp, 0);
+  return cudaGetLastError() == cudaSuccess ? MT_OK : MT_ERR_CUDA;
+}
+
+void mt_dfree(void* p) {
+  if (!p) return;
+  PoolState& P = pool_for_device();
+  if (!P.on) { cudaFree(p); return; }
+  cudaDeviceSynchronize();
+  cudaFreeAsync(p, P.st);
+}
 
 void mt_set_error(const char* fmt, ...) {
   va_list ap;
@@ -78,12 +143,12 @@ struct DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
-  ~DevBuf() { if (p) cudaFree(p); }
+  ~DevBuf() { if (p) mt_dfree(p); }
   template <class T> T* as() { return (T*)p; }
 };
 static int dalloc(DevBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
-  cudaError_t e = cudaMalloc(&b.p, bytes);
+  cudaError_t e = mt_dmalloc(&b.p, bytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
     mt_set_error("device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));

@@ -6,6 +6,15 @@
 
 #include "../../include/mertens_sm100.h"
 
+// Device allocations of the engine: stream-ordered from the device's default memory
+// pool with its release threshold raised, so a plan's buffers (several GB at 1e19)
+// are reused by the next plan instead of being mapped and unmapped per call.
+// MT_POOL=0 falls back to cudaMalloc / cudaFree.  mt_dfree waits for the device
+// first (as cudaFree does), so no buffer is recycled while a kernel may use it.
+cudaError_t mt_dmalloc_raw(void** p, size_t bytes);
+void mt_dfree(void* p);
+template <class T> inline cudaError_t mt_dmalloc(T** p, size_t bytes) { return mt_dmalloc_raw((void**)p, bytes); }
+
 #define MT_TILE 65536u          // sieve tile: cells (bytes) held in shared memory
 #define MT_SIEVE_THREADS 512    // threads per sieve tile (128 cells each)
 #define MT_WHEEL 13860u

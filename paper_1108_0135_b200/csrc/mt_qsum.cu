@@ -76,16 +76,16 @@ static int qsum(const double* z, const double* a, const double* b, uint64_t nt, 
     return MT_OK;
   }
   double *dz = nullptr, *da = nullptr, *db = nullptr, *dp = nullptr, *dout = nullptr;
-  struct F { double** p[5]; ~F() { for (auto q : p) if (*q) cudaFree(*q); } } f{{&dz, &da, &db, &dp, &dout}};
-  MT_CUDA_CHECK(cudaMalloc(&dz, nt * 8));
-  MT_CUDA_CHECK(cudaMalloc(&da, nt * 8));
-  MT_CUDA_CHECK(cudaMalloc(&db, nt * 8));
-  MT_CUDA_CHECK(cudaMalloc(&dout, count * 8));
+  struct F { double** p[5]; ~F() { for (auto q : p) if (*q) mt_dfree(*q); } } f{{&dz, &da, &db, &dp, &dout}};
+  MT_CUDA_CHECK(mt_dmalloc(&dz, nt * 8));
+  MT_CUDA_CHECK(mt_dmalloc(&da, nt * 8));
+  MT_CUDA_CHECK(mt_dmalloc(&db, nt * 8));
+  MT_CUDA_CHECK(mt_dmalloc(&dout, count * 8));
   MT_CUDA_CHECK(cudaMemcpy(dz, z, nt * 8, cudaMemcpyHostToDevice));
   MT_CUDA_CHECK(cudaMemcpy(da, a, nt * 8, cudaMemcpyHostToDevice));
   MT_CUDA_CHECK(cudaMemcpy(db, b, nt * 8, cudaMemcpyHostToDevice));
   if (pts) {
-    MT_CUDA_CHECK(cudaMalloc(&dp, count * 8));
+    MT_CUDA_CHECK(mt_dmalloc(&dp, count * 8));
     MT_CUDA_CHECK(cudaMemcpy(dp, pts, count * 8, cudaMemcpyHostToDevice));
   }
   k_qgrid<<<(unsigned)((count + QB - 1) / QB), QT>>>(dz, da, db, nt, d0, h, count, dp, dout);

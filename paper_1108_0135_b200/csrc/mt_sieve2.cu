@@ -871,11 +871,11 @@ int mt_sieve2_segment(const Sieve2Segment& g, cudaStream_t st, KTimer* kt) {
 namespace {
 struct Buf {
   void* p = nullptr;
-  ~Buf() { if (p) cudaFree(p); }
+  ~Buf() { if (p) mt_dfree(p); }
 };
 int balloc(Buf& b, size_t n) {
   if (!n) n = 16;
-  cudaError_t e = cudaMalloc(&b.p, n);
+  cudaError_t e = mt_dmalloc(&b.p, n);
   if (e != cudaSuccess) {
     cudaGetLastError();
     mt_set_error("device allocation of %zu bytes failed: %s", n, cudaGetErrorString(e));

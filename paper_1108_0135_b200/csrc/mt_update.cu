@@ -932,8 +932,8 @@ static int scan_u64(UpdateCtx* c, const uint64_t* in, uint64_t* out, uint64_t n,
   size_t need = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, (int64_t)n, st);
   if (need > c->cub_bytes) {
-    if (c->cub_tmp) cudaFree(c->cub_tmp);
-    MT_CUDA_CHECK(cudaMalloc(&c->cub_tmp, need));
+    if (c->cub_tmp) mt_dfree(c->cub_tmp);
+    MT_CUDA_CHECK(mt_dmalloc(&c->cub_tmp, need));
     c->cub_bytes = need;
   }
   MT_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, need, in, out, (int64_t)n, st));
@@ -952,7 +952,7 @@ int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* 
   c->ntgt = ntgt;
   c->launches = 0;
   *out = c;
-  MT_CUDA_CHECK(cudaMalloc(&c->tgts, sizeof(TargetDev) * (ntgt ? ntgt : 1)));
+  MT_CUDA_CHECK(mt_dmalloc(&c->tgts, sizeof(TargetDev) * (ntgt ? ntgt : 1)));
   c->tgts_h.assign(tgts, tgts + ntgt);
   MT_CUDA_CHECK(cudaMemcpyAsync(c->tgts, tgts, sizeof(TargetDev) * ntgt, cudaMemcpyHostToDevice, st));
   // counted entries: the NE elements (target t's k = 1..K_t from ebase_t on), then
@@ -972,18 +972,18 @@ int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* 
   CountedEntries& C = c->C;
   C.n = nce;
   const u64 na = nce ? nce : 1;
-  MT_CUDA_CHECK(cudaMalloc(&C.vd, na * 8)); MT_CUDA_CHECK(cudaMalloc(&C.vlo, na * 8)); MT_CUDA_CHECK(cudaMalloc(&C.vhi, na * 8));
-  MT_CUDA_CHECK(cudaMalloc(&C.vbits, na));
+  MT_CUDA_CHECK(mt_dmalloc(&C.vd, na * 8)); MT_CUDA_CHECK(mt_dmalloc(&C.vlo, na * 8)); MT_CUDA_CHECK(mt_dmalloc(&C.vhi, na * 8));
+  MT_CUDA_CHECK(mt_dmalloc(&C.vbits, na));
   for (int r = 0; r < CE_ROLES; r++) {
-    MT_CUDA_CHECK(cudaMalloc(&C.lim[r], na * 8));
-    MT_CUDA_CHECK(cudaMalloc(&C.tg[r], na * 4));
+    MT_CUDA_CHECK(mt_dmalloc(&C.lim[r], na * 8));
+    MT_CUDA_CHECK(mt_dmalloc(&C.tg[r], na * 4));
   }
   c->ntiles = (nce + MT_CT - 1) / MT_CT;
-  MT_CUDA_CHECK(cudaMalloc(&c->tile_max, (c->ntiles + 1) * 8));
-  MT_CUDA_CHECK(cudaMalloc(&c->tile_vbits, c->ntiles + 1));
+  MT_CUDA_CHECK(mt_dmalloc(&c->tile_max, (c->ntiles + 1) * 8));
+  MT_CUDA_CHECK(mt_dmalloc(&c->tile_vbits, c->ntiles + 1));
   {
     VirtSpec* dvs = nullptr;
-    MT_CUDA_CHECK(cudaMalloc(&dvs, sizeof(VirtSpec) * vs.size()));
+    MT_CUDA_CHECK(mt_dmalloc(&dvs, sizeof(VirtSpec) * vs.size()));
     MT_CUDA_CHECK(cudaMemcpyAsync(dvs, vs.data(), sizeof(VirtSpec) * ntgt, cudaMemcpyHostToDevice, st));
     if (E.n) k_ce_init<<<(unsigned)((E.n + 255) / 256), 256, 0, st>>>(E, C);
     const u64 nv = nce - E.n;
@@ -991,19 +991,19 @@ int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* 
     if (c->ntiles) k_ce_tiles<<<(unsigned)c->ntiles, MT_CT, 0, st>>>(C, c->tile_max, c->tile_vbits);
     MT_CUDA_CHECK(cudaGetLastError());
     MT_CUDA_CHECK(cudaStreamSynchronize(st));
-    cudaFree(dvs);
+    mt_dfree(dvs);
   }
   const u64 ntiles = c->ntiles;
-  MT_CUDA_CHECK(cudaMalloc(&c->units, sizeof(uint64_t) * (ntiles + 1) * 2));
-  MT_CUDA_CHECK(cudaMalloc(&c->cnt, sizeof(uint64_t) * (E.n + 1)));
-  MT_CUDA_CHECK(cudaMalloc(&c->dtop, sizeof(uint64_t) * (E.n + 1)));
-  MT_CUDA_CHECK(cudaMalloc(&c->off, sizeof(uint64_t) * (E.n + 1)));
-  MT_CUDA_CHECK(cudaMalloc(&c->qcnt, sizeof(uint64_t) * (E.n + 1)));
-  MT_CUDA_CHECK(cudaMalloc(&c->qoff, sizeof(uint64_t) * (E.n + 1)));
-  MT_CUDA_CHECK(cudaMalloc(&c->counter, sizeof(uint64_t) * 4));
-  MT_CUDA_CHECK(cudaMalloc(&c->gunits, sizeof(uint64_t) * (grp.ng + 1)));
-  MT_CUDA_CHECK(cudaMalloc(&c->guoff, sizeof(uint64_t) * (grp.ng + 1)));
-  MT_CUDA_CHECK(cudaMalloc(&c->gwfirst, sizeof(uint64_t) * (grp.ng + 1)));
+  MT_CUDA_CHECK(mt_dmalloc(&c->units, sizeof(uint64_t) * (ntiles + 1) * 2));
+  MT_CUDA_CHECK(mt_dmalloc(&c->cnt, sizeof(uint64_t) * (E.n + 1)));
+  MT_CUDA_CHECK(mt_dmalloc(&c->dtop, sizeof(uint64_t) * (E.n + 1)));
+  MT_CUDA_CHECK(mt_dmalloc(&c->off, sizeof(uint64_t) * (E.n + 1)));
+  MT_CUDA_CHECK(mt_dmalloc(&c->qcnt, sizeof(uint64_t) * (E.n + 1)));
+  MT_CUDA_CHECK(mt_dmalloc(&c->qoff, sizeof(uint64_t) * (E.n + 1)));
+  MT_CUDA_CHECK(mt_dmalloc(&c->counter, sizeof(uint64_t) * 4));
+  MT_CUDA_CHECK(mt_dmalloc(&c->gunits, sizeof(uint64_t) * (grp.ng + 1)));
+  MT_CUDA_CHECK(mt_dmalloc(&c->guoff, sizeof(uint64_t) * (grp.ng + 1)));
+  MT_CUDA_CHECK(mt_dmalloc(&c->gwfirst, sizeof(uint64_t) * (grp.ng + 1)));
   MT_CUDA_CHECK(cudaFuncSetAttribute(k_dwin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(MT_BLK * 2)));
   MT_CUDA_CHECK(cudaFuncSetAttribute(k_counted, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(MT_CM * 12)));
   c->cub_tmp = nullptr; c->cub_bytes = 0;
@@ -1014,13 +1014,13 @@ int mt_update_create(UpdateCtx** out, const ElemDev& E, uint64_t* acc, int32_t* 
 
 void mt_update_destroy(UpdateCtx* c) {
   if (!c) return;
-  cudaFree(c->C.vd); cudaFree(c->C.vlo); cudaFree(c->C.vhi); cudaFree(c->C.vbits);
-  for (int r = 0; r < CE_ROLES; r++) { cudaFree(c->C.lim[r]); cudaFree(c->C.tg[r]); }
-  cudaFree(c->tile_max); cudaFree(c->tile_vbits);
-  cudaFree(c->tgts); cudaFree(c->units); cudaFree(c->cnt); cudaFree(c->dtop); cudaFree(c->off);
-  cudaFree(c->qcnt); cudaFree(c->qoff); cudaFree(c->counter);
-  cudaFree(c->gunits); cudaFree(c->guoff); cudaFree(c->gwfirst);
-  if (c->cub_tmp) cudaFree(c->cub_tmp);
+  mt_dfree(c->C.vd); mt_dfree(c->C.vlo); mt_dfree(c->C.vhi); mt_dfree(c->C.vbits);
+  for (int r = 0; r < CE_ROLES; r++) { mt_dfree(c->C.lim[r]); mt_dfree(c->C.tg[r]); }
+  mt_dfree(c->tile_max); mt_dfree(c->tile_vbits);
+  mt_dfree(c->tgts); mt_dfree(c->units); mt_dfree(c->cnt); mt_dfree(c->dtop); mt_dfree(c->off);
+  mt_dfree(c->qcnt); mt_dfree(c->qoff); mt_dfree(c->counter);
+  mt_dfree(c->gunits); mt_dfree(c->guoff); mt_dfree(c->gwfirst);
+  if (c->cub_tmp) mt_dfree(c->cub_tmp);
   delete c;
 }
 

@@ -480,6 +480,14 @@ def mertens_exact_big(n: int, config: EngineConfig | None = None, u: int | None 
                          elapsed=time.perf_counter() - t0, backend=BACKEND_NAME)
 
 
+def release_device_memory() -> None:
+    """Return the engine's cached device buffers to the driver.  Plans allocate from
+    the device's memory pool and keep the blocks between calls (no per-call mapping
+    of several GB); this trims the pool (mt_trim_device_memory)."""
+    L = _lib.require_device()
+    _lib.check(L.mt_trim_device_memory())
+
+
 def mertens_naive(n: int, config: EngineConfig | None = None, checkpoints=None):
     """M(n) by one O(n) GPU sieve pass (engine.py:553-603); with `checkpoints`
     (sorted) also returns M at each checkpoint <= n."""

@@ -567,3 +567,14 @@ def test_udiv128_reciprocal(engine):
     got = [(int(h) << 64) | int(l) for l, h in zip(qlo.tolist(), qhi.tolist())]
     bad = [(v, m) for v, m, g in zip(vs, ms, got) if g != v // m]
     assert not bad, bad[:5]
+
+
+def test_device_memory_pool_reuse(engine, golden):
+    """Plans reuse pooled device buffers across calls (and after a trim) with the same
+    results: M(10^16) and its quotients three times around release_device_memory."""
+    r1 = engine.mertens_exact(10**16)
+    r2 = engine.mertens_exact(10**16)
+    engine.release_device_memory()
+    r3 = engine.mertens_exact(10**16)
+    assert r1.value == r2.value == r3.value == -3195437
+    assert np.array_equal(r1._final, r2._final) and np.array_equal(r1._final, r3._final)
