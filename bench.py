@@ -541,7 +541,7 @@ def _counted_units(st):
     entry j (an element j <= K, or a virtual j = 2k, 3k, 6k > K) walks up to the largest
     of its role limits, mcut_j (own, j <= K) and floor(mcut_{j/d}/d) for d = 2, 3, 6 with
     d | j and j/d <= K; 3/pi^2 of the m are squarefree and coprime to 6.
-    mcut is the reference's (engine.py:144-158)."""
+    mcut follows the engine's counted / dense split (MT_XCUT_ALPHA)."""
     n, u = int(st["_n"]), int(st["_u"])
     K = n // u
     k = np.arange(1, K + 1, dtype=np.uint64)
@@ -555,6 +555,9 @@ def _counted_units(st):
     t = np.where((t >> np.uint64(1)) >= x2, t >> np.uint64(1), t)
     D = v // np.uint64(u + 1)
     xc = np.maximum(np.maximum(D, v // t), np.uint64(1))
+    alpha = float(os.environ.get("MT_XCUT_ALPHA", "0.39"))  # the engine's split
+    if alpha > 0:
+        xc = np.maximum(np.maximum(D, (alpha * s.astype(np.float64)).astype(np.uint64)), np.uint64(1))
     mc = (v // (xc + np.uint64(1))).astype(np.float64)
     lim = np.zeros(6 * K + 1)
     lim[1:K + 1] = mc

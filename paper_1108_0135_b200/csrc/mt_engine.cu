@@ -31,6 +31,10 @@
 #include "mt_common.cuh"
 #include "mt_internal.h"
 
+#ifndef MT_XCUT_ALPHA_DEFAULT
+#define MT_XCUT_ALPHA_DEFAULT 0.39  // xcut ~ 0.39 sqrt(v) (measured at 1e19: 0.38-0.40 best, -1.8 % vs the reference's split)
+#endif
+
 static thread_local char g_err[2048];
 
 // ------------------------------------------------------------ device memory
@@ -593,6 +597,8 @@ struct ElemInitArgs {
   u64 n_elem;
   double* vd; u64* vlo; u64* vhi; uint8_t* vbits; u64* k; uint32_t* tgt;
   u64* D; u64* xcut; u64* mcut; u64* lo;
+  double xalpha;                     // > 0: split at xcut = max(D, xalpha sqrt(v)) (else the reference's)
+  unsigned long long* stats;         // [ntgt*4]: max working mcut, sum / max reference mcut, reference dense items
 };
 
 __device__ u64 d_isqrt128(u128 x) {
@@ -619,10 +625,24 @@ __global__ void k_elem_init(ElemInitArgs a) {
   const u64 x2 = 2 * cs;
   u64 tt = 1;
   while (tt < x2) tt <<= 1;  // smallest power of two >= 2*ceil(sqrt v) (engine.py:148-149, :481)
-  u64 xc = (u64)(v / tt);
-  if (xc < D) xc = D;
-  if (xc < 1) xc = 1;
+  u64 xr = (u64)(v / tt);
+  if (xr < D) xr = D;
+  if (xr < 1) xr = 1;
+  // the counted / dense split: any xcut >= D gives the same acc_k (summation by parts);
+  // the reference's (engine.py:144-158) fixes the RunStats counters either way
+  u64 xc = xr;
+  if (a.xalpha > 0) {
+    xc = (u64)(a.xalpha * (double)cs);
+    if (xc < D) xc = D;
+    if (xc < 1) xc = 1;
+  }
   const u64 mc = (u64)(v / ((u128)xc + 1));
+  const u64 mr = (u64)(v / ((u128)xr + 1));
+  const u64 lo = D + 1 > 2 ? D + 1 : 2;
+  atomicMax(&a.stats[4 * t + 0], (unsigned long long)mc);
+  atomicAdd(&a.stats[4 * t + 1], (unsigned long long)mr);
+  if (xr >= lo) atomicAdd(&a.stats[4 * t + 2], (unsigned long long)(xr - lo + 1));
+  atomicMax(&a.stats[4 * t + 3], (unsigned long long)mr);
   a.vlo[e] = (u64)v;
   a.vhi[e] = (u64)(v >> 64);
   a.vd[e] = (v >> 64) ? fma((double)(u64)(v >> 64), 18446744073709551616.0, (double)(u64)v) : __ull2double_rn((u64)v);
@@ -632,7 +652,7 @@ __global__ void k_elem_init(ElemInitArgs a) {
   a.D[e] = D;
   a.xcut[e] = xc;
   a.mcut[e] = mc;
-  a.lo[e] = D + 1 > 2 ? D + 1 : 2;
+  a.lo[e] = lo;
 }
 
 // windowed / Q-gather boundary: Q-gather takes d <= J/k
@@ -693,18 +713,6 @@ __global__ void k_group_meta(const u64* __restrict__ gstart, u64 ng, const u64* 
 }
 
 // per-target reductions: max mcut, sum mcut, sum dense items, max windowed y
-__global__ void k_elem_stats(u64 n_elem, const uint32_t* __restrict__ tgt, const u64* __restrict__ mcut,
-                             const u64* __restrict__ xcut, const u64* __restrict__ lo,
-                             unsigned long long* __restrict__ out /*[ntgt*3]*/) {
-  u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n_elem) return;
-  uint32_t t = tgt[e];
-  atomicMax(&out[3 * t + 0], (unsigned long long)mcut[e]);
-  atomicAdd(&out[3 * t + 1], (unsigned long long)mcut[e]);
-  u64 xc = xcut[e], l = lo[e];
-  if (xc >= l) atomicAdd(&out[3 * t + 2], (unsigned long long)(xc - l + 1));
-}
-
 __global__ void k_window_extent(u64 n_elem, const u64* __restrict__ vlo, const u64* __restrict__ vhi,
                                 const u64* __restrict__ lo_w, const u64* __restrict__ xcut,
                                 unsigned long long* __restrict__ out) {
@@ -879,7 +887,8 @@ struct mt_plan {
   cudaStream_t st = nullptr;
   bool own_stream = false;
   u64 launches = 0;  // kernels of the current execution (reset by the head step)
-  u64 counted_items = 0, dense_items = 0, Ymc = 0;
+  u64 counted_items = 0, dense_items = 0, Ymc = 0, Ymc_ref = 0;  // Ymc: the working split's max mcut
+  double xalpha = 0;  // counted / dense split: xcut = max(D, xalpha ceil(sqrt v)); 0 = the reference's
   // elements
   DevBuf d_nlo, d_nhi, d_e0, d_vd, d_vlo, d_vhi, d_vb, d_k, d_tgt, d_D, d_x, d_mc, d_lo, d_low, d_dq,
       d_acc, d_mmc, d_dsp, d_J, d_gs, d_gylo, d_gyhi, d_gw, d_fin;
@@ -1003,26 +1012,28 @@ static int plan_setup(mt_plan* P, const mt_job* job) {
   MT_CUDA_CHECK(cudaMemcpyAsync(P->d_nlo.p, job->n_lo, N * 8, cudaMemcpyHostToDevice, st));
   MT_CUDA_CHECK(cudaMemcpyAsync(P->d_nhi.p, job->n_hi, N * 8, cudaMemcpyHostToDevice, st));
   MT_CUDA_CHECK(cudaMemcpyAsync(P->d_e0.p, P->e0.data(), (N + 1) * 8, cudaMemcpyHostToDevice, st));
-  {
-    ElemInitArgs a{P->d_nlo.as<u64>(), P->d_nhi.as<u64>(), P->d_e0.as<u64>(), N, u, NE,
-                   P->d_vd.as<double>(), P->d_vlo.as<u64>(), P->d_vhi.as<u64>(), P->d_vb.as<uint8_t>(), P->d_k.as<u64>(),
-                   P->d_tgt.as<uint32_t>(), P->d_D.as<u64>(), P->d_x.as<u64>(), P->d_mc.as<u64>(), P->d_lo.as<u64>()};
-    if (NE) k_elem_init<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(a);
-    MT_CUDA_CHECK(cudaGetLastError());
-  }
-  std::vector<unsigned long long> tstat(3 * N, 0);
+  std::vector<unsigned long long> tstat(4 * N, 0);
   {
     DevBuf d_ts;
-    RC(dalloc(d_ts, 3 * N * 8));
-    MT_CUDA_CHECK(cudaMemsetAsync(d_ts.p, 0, 3 * N * 8, st));
-    if (NE) k_elem_stats<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(NE, P->d_tgt.as<uint32_t>(), P->d_mc.as<u64>(), P->d_x.as<u64>(), P->d_lo.as<u64>(), d_ts.as<unsigned long long>());
-    MT_CUDA_CHECK(cudaMemcpyAsync(tstat.data(), d_ts.p, 3 * N * 8, cudaMemcpyDeviceToHost, st));
+    RC(dalloc(d_ts, 4 * N * 8));
+    MT_CUDA_CHECK(cudaMemsetAsync(d_ts.p, 0, 4 * N * 8, st));
+    P->xalpha = MT_XCUT_ALPHA_DEFAULT;
+    if (const char* e = getenv("MT_XCUT_ALPHA")) P->xalpha = atof(e);
+    const double xalpha = P->xalpha;
+    ElemInitArgs a{P->d_nlo.as<u64>(), P->d_nhi.as<u64>(), P->d_e0.as<u64>(), N, u, NE,
+                   P->d_vd.as<double>(), P->d_vlo.as<u64>(), P->d_vhi.as<u64>(), P->d_vb.as<uint8_t>(), P->d_k.as<u64>(),
+                   P->d_tgt.as<uint32_t>(), P->d_D.as<u64>(), P->d_x.as<u64>(), P->d_mc.as<u64>(), P->d_lo.as<u64>(),
+                   xalpha, d_ts.as<unsigned long long>()};
+    if (NE) k_elem_init<<<(unsigned)((NE + 255) / 256), 256, 0, st>>>(a);
+    MT_CUDA_CHECK(cudaGetLastError());
+    MT_CUDA_CHECK(cudaMemcpyAsync(tstat.data(), d_ts.p, 4 * N * 8, cudaMemcpyDeviceToHost, st));
     MT_CUDA_CHECK(cudaStreamSynchronize(st));
   }
   for (int i = 0; i < N; i++) {
-    P->Ymc = std::max<u64>(P->Ymc, tstat[3 * i]);
-    P->counted_items += tstat[3 * i + 1];
-    P->dense_items += tstat[3 * i + 2];
+    P->Ymc = std::max<u64>(P->Ymc, tstat[4 * i]);
+    P->Ymc_ref = std::max<u64>(P->Ymc_ref, tstat[4 * i + 3]);
+    P->counted_items += tstat[4 * i + 1];
+    P->dense_items += tstat[4 * i + 2];
   }
 
   // ---- quotient tables: Q_t[j] = M(floor(n_t/j)), j in [jq0_t, jq1_t]; the tail
@@ -1294,7 +1305,7 @@ extern "C" int mt_plan_sieve_update(mt_plan* P, int64_t* m_head, int64_t* tail_t
 }
 
 // ---- checkpoint / resume (reference MERTCKP1 header, engine.py:646-680, with
-// version 3 marking the sm100 engine state that follows it)
+// version 4 marking the sm100 engine state that follows it)
 #pragma pack(push, 1)
 struct CkptHead {
   char magic[8];
@@ -1305,7 +1316,7 @@ struct CkptHead {
 };
 #pragma pack(pop)
 static_assert(sizeof(CkptHead) == 72, "MERTCKP1 header is <8sII QQ Q Q Q q Q>");
-#define MT_CKPT_VERSION 3
+#define MT_CKPT_VERSION 4
 
 static int write_all(FILE* f, const void* p, u64 bytes) {
   if (bytes && fwrite(p, 1, bytes, f) != bytes) { mt_set_error("checkpoint write failed (disk full?)"); return MT_ERR_RESOURCE; }
@@ -1354,6 +1365,7 @@ static int ckpt_write(mt_plan* P, FILE* f) {
   h.m_running = P->m_head;
   h.block_len = P->seg_y;
   RC(write_all(f, &h, sizeof(h)));
+  RC(write_all(f, &P->xalpha, 8));  // the counted / dense split the head state was computed with
   RC(write_dev(f, P->d_acc.p, P->NE * 8));
   RC(write_dev(f, P->d_mmc.p, P->NE * 4));
   const u64 qn = P->jq1[0] >= P->jq0[0] ? P->jq1[0] - P->jq0[0] + 1 : 0;
@@ -1403,6 +1415,11 @@ extern "C" int mt_plan_restore(mt_plan* P, const char* path) {
   if (h.n_lo != P->n_lo[0] || h.n_hi != P->n_hi[0] || h.u != P->u || h.K != P->K[0] || h.block_len != P->seg_y ||
       h.flags != (P->rank | (P->world << 16))) {
     mt_set_error("checkpoint built for another job (n, u, K, segment size or rank/world differ)");
+    return MT_ERR_CONTRACT;
+  }
+  double xa = -1;
+  if (fread(&xa, 8, 1, f) != 1 || xa != P->xalpha) {
+    mt_set_error("checkpoint built with another counted / dense split (MT_XCUT_ALPHA)");
     return MT_ERR_CONTRACT;
   }
   RC(read_dev(f, P->d_acc.p, P->NE * 8));
@@ -1585,7 +1602,7 @@ extern "C" int mt_plan_resolve(mt_plan* P, mt_result* out) {
   S.counted_items = P->counted_items;
   S.dense_items = P->dense_items;
   S.head_end = P->head_lim;
-  S.max_mcut = P->Ymc;
+  S.max_mcut = P->Ymc_ref;
   S.n_head_segments = P->head_segs;
   S.n_tail_segments = P->tsegs.size();
   // kernels of this execution: the plan's own, the update context's (cub scans

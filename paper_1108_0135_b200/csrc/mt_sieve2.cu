@@ -298,8 +298,11 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
         const u32 len = (rc + 3) & ~3u;
         u32* so = stage + t * bin;
         u32* go = out + t * cap + g0;
-        if (rc < bin) {
-          for (u32 i = rc; i < len; i++) so[i] = 0u;
+        if (rc < bin) {  // len <= bin: up to three pad words
+          const u32 npad = len - rc;
+          if (npad > 0) so[rc] = 0u;
+          if (npad > 1) so[rc + 1] = 0u;
+          if (npad > 2) so[rc + 2] = 0u;
         } else {
           for (u32 i = rc; i < len; i++) if (g0 + i < cap) go[i] = 0u;
         }

@@ -19,7 +19,8 @@
 //              from the segment's M array (load-balanced item ranges).
 //   Q-gather : dense items with k*d <= J read M(floor(n/(kd))) straight from
 //              the captured quotient table Q[j] (no division at all).
-// The split (xcut, mcut) is the reference's own, so RunStats counters match.
+// The split (xcut, mcut) is the engine's (xcut ~ 0.39 sqrt(v), mt_engine.cu k_elem_init: any
+// split gives the same acc_k); the RunStats counters are the reference's split's.
 #include <cub/cub.cuh>
 
 #include "mt_common.cuh"

@@ -576,7 +576,7 @@ _CKPT_HEAD = struct.Struct("<8sII QQ Q Q Q q Q")  # engine.py:659
 
 def resume_exact(path: str, config: EngineConfig | None = None) -> MertensResult:
     """Continue a checkpointed run to completion (engine.py:731-741).  The file
-    carries the reference's MERTCKP1 header (version 3: this engine's state
+    carries the reference's MERTCKP1 header (version 4: this engine's state
     follows it); u must match the one `config` derives (engine.py:697-698).
     A sharded job (config.distributed under a process group) resumes from the
     per-rank files `path.r{rank}of{world}`."""
@@ -589,7 +589,7 @@ def resume_exact(path: str, config: EngineConfig | None = None) -> MertensResult
     if len(head) != _CKPT_HEAD.size:
         raise ContractViolationError("not a checkpoint file")
     magic, version, flags, n_lo, n_hi, u, _next_y1, _K, _m_running, _bl = _CKPT_HEAD.unpack(head)
-    if magic != b"MERTCKP1" or version != 3:
+    if magic != b"MERTCKP1" or version != 4:
         raise ContractViolationError("not an sm100 checkpoint file")
     n = (n_hi << 64) | n_lo
     if choose_u(n, 1, config.mem_budget, config.u_alpha) != u:

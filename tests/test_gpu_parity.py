@@ -526,7 +526,7 @@ def test_checkpoint_resume(engine, golden, tmp_path):
     assert full.value == 599582
     head = open(path, "rb").read(72)
     magic, version, flags, n_lo, n_hi, u, next_y1, K, m_running, bl = struct.unpack("<8sII QQ Q Q Q q Q", head)
-    assert (magic, version, flags, n_lo, u, K) == (b"MERTCKP1", 3, 1 << 16, n, full.u, len(full._final))
+    assert (magic, version, flags, n_lo, u, K) == (b"MERTCKP1", 4, 1 << 16, n, full.u, len(full._final))
     # resume from the last checkpoint of that run (somewhere in the tail)
     r = engine.resume_exact(path, engine.EngineConfig(seg_log2_tail=18))
     assert r.value == full.value and np.array_equal(r._final, full._final)
