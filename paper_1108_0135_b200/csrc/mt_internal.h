@@ -24,7 +24,9 @@ template <class T> inline cudaError_t mt_dmalloc(T** p, size_t bytes) { return m
 #define MT_CM 2736              // list capacity of a counted-walk work unit (the m coprime to 6 of MT_CU consecutive m)
 #endif
 #define MT_BLK 32768u           // M16 block: values stored relative to M(block start - 1)
+#ifndef MT_WIN_SPLIT
 #define MT_WIN_SPLIT 64         // d_sp = ceil(sqrt(v)/64): windowed walk up to y ~ 64 sqrt(v)
+#endif
 
 struct SieveTileArgs {
   uint64_t Y0;                   // segment start (multiple of MT_TILE)
