@@ -161,6 +161,22 @@ def test_u_invariance(engine):
         assert engine.mertens_exact(n, engine.EngineConfig(u_alpha=alpha)).value == base
 
 
+@pytest.mark.parametrize("n", [10**13, 987654321012345])
+def test_counted_dense_split_invariance(engine, monkeypatch, n):
+    """The counted / dense split xcut = max(D, alpha ceil(sqrt v)) changes the work
+    division, not the result: finals, quotients and the reference-split RunStats
+    counters are identical for the reference's split (alpha = 0) and other alphas."""
+    runs = {}
+    for a in ("0", "0.25", "0.39", "0.5"):
+        monkeypatch.setenv("MT_XCUT_ALPHA", a)
+        runs[a] = engine.mertens_exact(n)
+    ref = runs["0"]
+    for a, r in runs.items():
+        assert r.value == ref.value, a
+        assert np.array_equal(r._final, ref._final), a
+        assert (r.stats.counted_items, r.stats.dense_items) == (ref.stats.counted_items, ref.stats.dense_items), a
+
+
 def test_segment_size_invariance(engine):
     n = 10**13
     a = engine.mertens_exact(n)
