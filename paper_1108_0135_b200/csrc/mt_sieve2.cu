@@ -141,8 +141,48 @@ __device__ __forceinline__ void first_hits(u64 C0, double Cd, double rm, u64 m, 
 #ifndef FITEM
 #define FITEM 32     // hits per item (1024 items per round: ~32k hits over the tiles)
 #endif
+#ifndef FILL_DIRECT
+#define FILL_DIRECT 1  // streams of <= FITEM hits are emitted in phase 1 by their own thread
+#endif
+// one run of a log stream's hits [pos, end) (cell offsets in the segment, stride
+// step): four slot allocations in flight; hits past `end` count into the dummy
+// rcnt[nt].  Shared addresses are explicit 32-bit (the generic stage pointer made
+// the compiler rebuild the window base per store); the common case is one
+// predicated st.shared, a full bin falls back to a direct global store
+__device__ __forceinline__ void fill_run(u32 pos, u32 end, u32 step, u32 val, u32 rcnt_s, u32 stage_s, u32 nt,
+                                         u32 bin, const u32* gcnt, u32* __restrict__ out, u32 cap) {
+  for (; pos < end; pos += 4 * step) {
+    u32 t[4], sl[4];
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+      const u32 ph = pos + h * step;
+      t[h] = ph < end ? ph >> 17 : nt;
+    }
+#pragma unroll
+    for (int h = 0; h < 4; h++)
+      asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(sl[h]) : "r"(rcnt_s + 4 * t[h]) : "memory");
+    bool spill = false;
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+      const u32 e = ((pos + h * step) & (S2_T - 1)) | val;
+      const bool in = t[h] < nt && sl[h] < bin;
+      if (in) asm volatile("st.shared.u32 [%0], %1;" ::"r"(stage_s + 4 * (t[h] * bin + sl[h])), "r"(e) : "memory");
+      spill |= t[h] < nt && sl[h] >= bin;
+    }
+    if (spill) {  // rare: a full bin
+#pragma unroll
+      for (int h = 0; h < 4; h++) {
+        if (t[h] < nt && sl[h] >= bin) {
+          const u32 g = gcnt[t[h]] + sl[h];
+          if (g < cap) out[t[h] * cap + g] = ((pos + h * step) & (S2_T - 1)) | val;
+        }
+      }
+    }
+  }
+}
+
 template <int W>
-__global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
+__global__ void __launch_bounds__(1024, 1) k_bucket_fill(Bucket2Args a) {
   constexpr int NS = Wheel<W>::NS;
   // dynamic: rcnt[ntiles + 1] (round counts; [ntiles] = dummy), gcnt[ntiles]
   // (entries before this round), cnt2[ntiles] (square flags), stage[ntiles][bin]
@@ -159,10 +199,11 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
   __shared__ u32 s_ipre[FBATCH + 1];  // exclusive prefix of items per stream
   __shared__ u32 s_wsum[32];
   __shared__ u32 s_hits;
+  __shared__ u32 s_dhits;  // hits emitted directly in this batch's phase 1
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 b = blockIdx.x, NP = gridDim.x;
   const u32 nt = a.ntiles, bin = a.bin;
-  if (tid == 0) s_hits = 0;
+  if (tid == 0) { s_hits = 0; s_dhits = 0; }
   for (u32 t = tid; t < 3 * nt + 1; t += blockDim.x) dsm[t] = 0;
   const u64 C0 = Wheel<W>::cell0(a.Y0);  // first cell of the segment
   const u32 R = nt * S2_T;                // cells, <= 2^31
@@ -173,6 +214,40 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
   const u32 nlog = a.p_hi > a.p_lo + b ? (a.p_hi - a.p_lo - b + NP - 1) / NP : 0;
   const u32 nsq = a.q_hi > a.q_lo + b ? (a.q_hi - a.q_lo - b + NP - 1) / NP : 0;
   const u32 nstream = (nlog + nsq) * NS;
+  // flush: each tile's run, zero-padded to a multiple of 4 entries (an entry of 0 adds 0
+  // to cell 0: a no-op mark) so every run starts 16-byte aligned, goes out as one bulk
+  // async copy shared -> global (block-uniform call)
+  auto flush = [&]() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    for (u32 t = tid; t < nt; t += blockDim.x) {
+      const u32 rc = rcnt[t], g0 = gcnt[t];
+      if (!rc) continue;
+      const u32 len = (rc + 3) & ~3u;
+      u32* so = stage + t * bin;
+      u32* go = out + t * cap + g0;
+      if (rc < bin) {  // len <= bin: up to three pad words
+        const u32 npad = len - rc;
+        if (npad > 0) so[rc] = 0u;
+        if (npad > 1) so[rc + 1] = 0u;
+        if (npad > 2) so[rc + 2] = 0u;
+      } else {
+        for (u32 i = rc; i < len; i++) if (g0 + i < cap) go[i] = 0u;
+      }
+      const u32 ncp = g0 < cap ? min(min(len, bin), cap - g0) : 0u;
+      if (ncp) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(go), "r"((u32)__cvta_generic_to_shared(so)), "r"(ncp * 4u) : "memory");
+      }
+      gcnt[t] = g0 + len;
+      rcnt[t] = 0;
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncthreads();
+  };
+  u32 pend = 0;  // direct hits staged since the last flush (block-uniform)
   for (u32 base = 0; base < nstream; base += FBATCH) {
     __syncthreads();
     // phase 1: first hit, step, value, item count of one stream per thread
@@ -198,8 +273,15 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
           val = 0x80u << 17;
         }
         const u32 hits = q0 < R ? (R - 1 - q0) / step + 1 : 0;
-        c = (hits + FITEM - 1) / FITEM;
-        if (hits) atomicAdd(&s_hits, hits);
+        if (FILL_DIRECT && hits && hits <= FITEM && !(val & (0x80u << 17))) {
+          // a stream of at most one item (the large primes at n >= 1e21) is emitted
+          // right here by its own thread: no item, no search
+          fill_run(q0, R, step, val, rcnt_s, stage_s, nt, bin, gcnt, out, cap);
+          atomicAdd(&s_dhits, hits);
+        } else {
+          c = (hits + FITEM - 1) / FITEM;
+          if (hits) atomicAdd(&s_hits, hits);
+        }
       }
       s_q0[tid] = q0;
       s_step[tid] = step;
@@ -229,11 +311,12 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
     s_ipre[tid] = s_wsum[warp] + incl - c;
     __syncthreads();
     const u32 nit = s_ipre[FBATCH];
+    pend += s_dhits;
     // items per thread and round: large primes give short items, so a round
     // takes several per thread to fill the bins (~FITEM hits per thread)
     const u32 per = nit ? max(1u, min(16u, (FITEM * nit + s_hits / 2) / max(1u, s_hits))) : 1u;
     __syncthreads();
-    if (tid == 0) s_hits = 0;
+    if (tid == 0) { s_hits = 0; s_dhits = 0; }
     for (u32 r0 = 0; r0 < nit; r0 += 1024 * per) {
       for (u32 it = r0 + tid; it < min(nit, r0 + 1024 * per); it += 1024) {
         u32 lo = 0, hi = FBATCH;  // largest k with s_ipre[k] <= it
@@ -251,34 +334,7 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
           // pointer made the compiler rebuild the window base per store); the
           // common case is one predicated st.shared, a full bin falls back to a
           // direct global store
-          for (; pos < end; pos += 4 * step) {
-            u32 t[4], sl[4];
-#pragma unroll
-            for (int h = 0; h < 4; h++) {
-              const u32 ph = pos + h * step;
-              t[h] = ph < end ? ph >> 17 : nt;
-            }
-#pragma unroll
-            for (int h = 0; h < 4; h++)
-              asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(sl[h]) : "r"(rcnt_s + 4 * t[h]) : "memory");
-            bool spill = false;
-#pragma unroll
-            for (int h = 0; h < 4; h++) {
-              const u32 e = ((pos + h * step) & (S2_T - 1)) | val;
-              const bool in = t[h] < nt && sl[h] < bin;
-              if (in) asm volatile("st.shared.u32 [%0], %1;" ::"r"(stage_s + 4 * (t[h] * bin + sl[h])), "r"(e) : "memory");
-              spill |= t[h] < nt && sl[h] >= bin;
-            }
-            if (spill) {  // rare: a full bin
-#pragma unroll
-              for (int h = 0; h < 4; h++) {
-                if (t[h] < nt && sl[h] >= bin) {
-                  const u32 g = gcnt[t[h]] + sl[h];
-                  if (g < cap) out[t[h] * cap + g] = ((pos + h * step) & (S2_T - 1)) | val;
-                }
-              }
-            }
-          }
+          fill_run(pos, end, step, val, rcnt_s, stage_s, nt, bin, gcnt, out, cap);
         } else {  // square flags fill each list from the back
           for (; pos < end; pos += step) {
             const u32 t = pos >> 17;
@@ -287,39 +343,15 @@ __global__ void __launch_bounds__(1024) k_bucket_fill(Bucket2Args a) {
           }
         }
       }
-      // flush: each tile's run, zero-padded to a multiple of 4 entries (an entry
-      // of 0 adds 0 to cell 0: a no-op mark) so every run starts 16-byte aligned,
-      // goes out as one bulk async copy shared -> global
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
-      for (u32 t = tid; t < nt; t += blockDim.x) {
-        const u32 rc = rcnt[t], g0 = gcnt[t];
-        if (!rc) continue;
-        const u32 len = (rc + 3) & ~3u;
-        u32* so = stage + t * bin;
-        u32* go = out + t * cap + g0;
-        if (rc < bin) {  // len <= bin: up to three pad words
-          const u32 npad = len - rc;
-          if (npad > 0) so[rc] = 0u;
-          if (npad > 1) so[rc + 1] = 0u;
-          if (npad > 2) so[rc + 2] = 0u;
-        } else {
-          for (u32 i = rc; i < len; i++) if (g0 + i < cap) go[i] = 0u;
-        }
-        const u32 ncp = g0 < cap ? min(min(len, bin), cap - g0) : 0u;
-        if (ncp) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                       ::"l"(go), "r"((u32)__cvta_generic_to_shared(so)), "r"(ncp * 4u) : "memory");
-        }
-        gcnt[t] = g0 + len;
-        rcnt[t] = 0;
-      }
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      __syncthreads();
+      flush();
+      pend = 0;
+    }
+    if (pend > (nt * bin) / 2) {  // direct-only batches: flush once the bins are half full
+      flush();
+      pend = 0;
     }
   }
+  if (pend) flush();
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   for (u32 t = tid; t < nt; t += blockDim.x) {
