@@ -142,7 +142,10 @@ __device__ __forceinline__ void first_hits(u64 C0, double Cd, double rm, u64 m, 
 #define FITEM 32     // hits per item (1024 items per round: ~32k hits over the tiles)
 #endif
 #ifndef FILL_DIRECT
-#define FILL_DIRECT 1  // streams of <= FITEM hits are emitted in phase 1 by their own thread
+#define FILL_DIRECT 1  // streams of <= FDIRECT_MAX hits are emitted in phase 1 by their own thread
+#endif
+#ifndef FDIRECT_MAX
+#define FDIRECT_MAX FITEM
 #endif
 // one run of a log stream's hits [pos, end) (cell offsets in the segment, stride
 // step): four slot allocations in flight; hits past `end` count into the dummy
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(1024, 1) k_bucket_fill(Bucket2Args a) {
           val = 0x80u << 17;
         }
         const u32 hits = q0 < R ? (R - 1 - q0) / step + 1 : 0;
-        if (FILL_DIRECT && hits && hits <= FITEM && !(val & (0x80u << 17))) {
+        if (FILL_DIRECT && hits && hits <= FDIRECT_MAX && !(val & (0x80u << 17))) {
           // a stream of at most one item (the large primes at n >= 1e21) is emitted
           // right here by its own thread: no item, no search
           fill_run(q0, R, step, val, rcnt_s, stage_s, nt, bin, gcnt, out, cap);
