@@ -11,10 +11,10 @@
 // (floor(v/(mcut+1)) <= xcut always), so it needs only mu(m) != 0 (61% of m),
 // one exact division per item and no prefix values.  acc_k is therefore
 // computed as (all mod 2^64):
-//   counted  : tiles of (256 entries x 4096 m) per head segment; the tile's odd
-//              squarefree m are staged in shared memory as (1/m, m) and every
-//              thread walks them with the fp64-reciprocal exact division (the
-//              even m come from element 2k's walk: S(v,x) = S_o(v,x) - S_o(v/2,x/2)).
+//   counted  : tiles of (256 entries x 8192 m) per head segment; the tile's
+//              squarefree m coprime to 6 are staged in shared memory as (1/m, m)
+//              and every thread walks them with the fp64-reciprocal exact division
+//              (the other m come from entries dk: S(v,x) = sum_{d|6} mu(d) S_6(v/d, x/d)).
 //   windowed : dense items whose quotient y = v/d lies in the head, gathered
 //              from the segment's M array (load-balanced item ranges).
 //   Q-gather : dense items with k*d <= J read M(floor(n/(kd))) straight from
