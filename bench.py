@@ -260,7 +260,7 @@ def reference_arm(args, n, u, rank, world):
 
 def config_block(n, u, world):
     return {"workload": f"M({n}) plus all M(floor(n/c)) for c <= K (exact, 1 target)", "n": str(n), "u": u,
-            "K": n // u, "parallelism": f"y-shard x{world} (head redundant, odd-y tail ranges, 1 int64 allreduce)",
+            "K": n // u, "parallelism": f"y-shard x{world} (head redundant, tail ranges over the y coprime to 6, 1 int64 allreduce)",
             "l2": "inputs larger than L2: the job streams u sieve cells and a multi-GB quotient table per step"}
 
 
