@@ -297,6 +297,9 @@ __device__ __forceinline__ int count_le(const u32* mL, u64 mhw, int tot, u64 mc,
 #ifndef CT_VEC
 #define CT_VEC 1  // list entries read as 16-byte vectors (4 entries: 2 x 16 B of 1/m, 16 B of m)
 #endif
+#ifndef CT_RCP_PASS
+#define CT_RCP_PASS 1  // reciprocals of the unit's list in a separate uniform pass
+#endif
 #ifndef CT_VUNROLL
 #define CT_VUNROLL 4  // 4-entry blocks per iteration of the joint walk (measured: 4 > 2; 108 registers)
 #endif
@@ -475,16 +478,33 @@ __global__ void __launch_bounds__(CT_THREADS, CT_MINB) k_counted(CountedArgs a) 
       const u32 s3 = r3 + (u32)(b % 3);
       const int8_t mu = (s3 == 0 || s3 == 3) ? 0 : (int8_t)((bits[b >> 3] >> (8 * (b & 7))) & 0xff);
       const u64 m = m0 + b;
+#if CT_RCP_PASS
+      // compaction stores only the (negated) low word; the reciprocals follow in one
+      // uniform pass over the compacted list (no divergent fp64 reciprocal here)
+      if (m < mhi && mu != 0) {
+        const int idx = mu > 0 ? op : MT_CM - 1 - on;
+        mL[idx] = 0u - (u32)m;  // units never straddle 2^32
+        op += mu > 0; on += mu < 0;
+      }
+#else
       if (m < mhi && mu != 0) {
         const double r = __drcp_rn((double)m);
         if (mu > 0) { rmL[op] = r; mL[op] = 0u - (u32)m; op++; }
         else { const int idx = MT_CM - 1 - on; rmL[idx] = r; mL[idx] = 0u - (u32)m; on++; }  // units never straddle 2^32
       }
+#endif
     }
     __syncthreads();
+    const u64 mhw = mlo & 0xFFFFFFFF00000000ull;
+#if CT_RCP_PASS
+    for (int i = tid; i < totp + totn; i += CT_THREADS) {
+      const int idx = i < totp ? i : MT_CM - totn + (i - totp);
+      rmL[idx] = __drcp_rn((double)(mhw | (0u - mL[idx])));
+    }
+    __syncthreads();
+#endif
 
     // ---- the two entries' roles: prefix lengths of every role's limit in both lists
-    const u64 mhw = mlo & 0xFFFFFFFF00000000ull;
     const u64 cA = tau * MT_CT + tid, cB = cA + CT_THREADS;
     int pA[CE_ROLES], nA[CE_ROLES], pB[CE_ROLES], nB[CE_ROLES];
     u32 tA[CE_ROLES], tB[CE_ROLES];
